@@ -1,0 +1,123 @@
+/*
+ * libmace_b200 — C ABI of the B200-native MACE hot path (arXiv 1911.09278).
+ *
+ * Plain pointers and sizes only.  Every int-returning call returns 0 on
+ * success and -1 on failure; mace_last_error() then describes the failure
+ * (thread-local).  Host pointers are borrowed for the duration of the call;
+ * all device memory is owned by the context.
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/macetomo/):
+ *
+ *   mace_sysmat_*          build_system_matrix / _trace_ray   geometry.py:177-258
+ *   mace_load_matrix       SparseViewMatrix.to_csr (device CSR) geometry.py:115-158
+ *   mace_set_prior         PriorParams                          models.py:55-90
+ *   mace_setup_agents      AgentWorkspace.__init__ (stacking)  icd.py:175-201
+ *                          partition_views (caller-supplied)   geometry.py:161-174
+ *   mace_set_agent_params  beta/N, 1/sigma^2, clamp_nonneg     icd.py:178-205
+ *   mace_load_data         ReconProblem y / weights            models.py:211-228
+ *   mace_set_state         AgentWorkspace.set_state            icd.py:218-220
+ *   mace_get_state         AgentWorkspace.state
+ *   mace_get_error         AgentWorkspace.error_sinogram
+ *   mace_refresh           AgentWorkspace.refresh_error        icd.py:210-211
+ *   mace_pass              partial_update_prox / _sweep        icd.py:67-139,272-283
+ *   mace_forward_project   forward_project                     geometry.py:261-270
+ *   mace_cost              likelihood_cost + prior_cost        models.py:235-278
+ *   mace_stack_init        new_stack / w0 + average            mace.py:57-90,283-286
+ *   mace_states_from       agent.set_state(x_init)             mace.py:286-288
+ *   mace_iterate           the _run_outer loop body            mace.py:297-339
+ *   mace_iterate_local /   same, split around the cross-rank all-reduce of
+ *   mace_iterate_finish    the stack sum (multi-GPU agents)
+ *   mace_read_log          ConvergenceLog rows                 mace.py:166-201
+ */
+#ifndef MACE_B200_H
+#define MACE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#define MACE_ABI_VERSION 1
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char* mace_last_error(void);
+int mace_abi_version(void);
+
+/* ---- system-matrix tracer (host, multi-threaded, bit-exact to geometry.py:177-258).
+ * ux, uy, ex, ey: per-view direction cosines computed by the caller exactly as the
+ * reference does (numpy sin/cos); offsets: per-channel lateral offsets. */
+int mace_sysmat_trace(int n_side, double pixel_pitch, int n_views, int n_channels, const double* ux,
+                      const double* uy, const double* ex, const double* ey, const double* offsets, int n_threads,
+                      void** handle);
+int64_t mace_sysmat_view_nnz(void* handle, int view);
+/* copies view `view` out (row_ptr: n_channels+1 int64, cols: nnz int32, lens: nnz float64) and frees it */
+int mace_sysmat_take_view(void* handle, int view, int64_t* row_ptr, int32_t* cols, double* lens);
+void mace_sysmat_free(void* handle);
+
+/* ---- device context */
+int mace_ctx_create(int device, void** ctx);
+void mace_ctx_destroy(void* ctx);
+int mace_ctx_stream(void* ctx, void** stream);
+int mace_sync(void* ctx);
+int mace_ctx_info(void* ctx, int64_t* info8);
+int mace_agent_info(void* ctx, int local, int64_t* info8);
+
+/* global CSR over all (view, channel) rows: row_ptr[n_views*n_ch + 1], cols/vals[nnz] */
+int mace_load_matrix(void* ctx, int n_side, int n_views, int n_ch, const int64_t* row_ptr, const int32_t* cols,
+                     const float* vals);
+/* kind 0 = quadratic-mrf, 1 = qggmrf */
+int mace_set_prior(void* ctx, int kind, double p, double q, double T, double sigma_x, double eps_reg);
+/* n_local agents, agent a owns views[sum(view_counts[:a]) ...]; schedule 0 = super-voxel, 1 = raster */
+int mace_setup_agents(void* ctx, int n_local, const int* view_counts, const int* views, int schedule, int sv_side,
+                      int colours, int n_threads);
+/* local < 0: every local agent */
+int mace_set_agent_params(void* ctx, int local, double beta_eff, double inv_sigma2, int clamp);
+/* global sinogram y and weights, n_views x n_ch float32; recomputes theta2 */
+int mace_load_data(void* ctx, const float* y, const float* lam);
+
+int mace_set_state(void* ctx, int local, const float* x);
+int mace_get_state(void* ctx, int local, float* x);
+int mace_get_error(void* ctx, int local, float* e);
+int mace_get_theta2(void* ctx, int local, float* th);
+int mace_refresh(void* ctx, int local);
+/* n_passes passes over pixels [s_begin, s_end) (s_end < 0: all; ranges need the raster schedule) */
+int mace_pass(void* ctx, int local, const float* v, int n_passes, int64_t s_begin, int64_t s_end, double* dsq);
+
+int mace_forward_project(void* ctx, const float* x, float* out);
+int mace_cost(void* ctx, const float* x, double beta, double* like, double* prior);
+
+/* ---- MACE outer loop */
+int mace_stack_init(void* ctx, const float* w0, int n_total);
+int mace_set_ref(void* ctx, const float* ref);
+int mace_states_from(void* ctx, int which);
+int mace_get_image(void* ctx, int which, float* out);
+int mace_set_image(void* ctx, int which, const float* img);
+int mace_get_stack(void* ctx, float* w);
+int mace_iterate(void* ctx, int iters, int iter0, double rho, int use_g, double tol, int n_total, int with_ref,
+                 float* ms_out);
+int mace_iterate_local(void* ctx, double rho, int use_g);
+int mace_comm_buffers(void* ctx, void** wsum, void** sums5);
+int mace_local_sum(void* ctx);
+int mace_mean_from_sum(void* ctx, int n_total);
+int mace_iterate_finish(void* ctx, int n_total, double tol, int iter);
+int mace_read_log(void* ctx, int n, double* log, int* done2);
+
+/* ---- host-only layout probes (no device needed; used by the CPU test suite).
+ * mace_agent_csc: the stacked agent CSC of icd.py:185-192; col_ptr[n+1] always, rows/vals if non-null.
+ * mace_sv_layout_probe: the super-voxel layout decoded back to (pixel, local row, value) triples;
+ * stats[6] = entries, max_band, max_col, n_sv, duplicates, decoded. */
+int mace_agent_csc(int n_side, int n_ch, int n_views, const int64_t* row_ptr, const int32_t* cols, const float* vals,
+                   int n_agent_views, const int* views, int64_t* col_ptr, uint32_t* rows, float* out_vals);
+int mace_sv_layout_probe(int n_side, int n_ch, int n_views, const int64_t* row_ptr, const int32_t* cols,
+                         const float* vals, int n_agent_views, const int* views, int svs, int64_t* stats,
+                         int32_t* pix_out, int32_t* row_out, float* val_out);
+
+int mace_host_alloc(size_t bytes, void** out);
+void mace_host_free(void* ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,752 @@
+// Device code for the MACE hot path on sm_100a.
+//
+//   K2  k_icd_sv / k_icd_raster   one partial-update ICD pass per agent
+//                                 (restates _sweep, pkg/src/macetomo/icd.py:67-139,
+//                                 with v = 2G(w)-w (mace.py:99-102) fused in front and
+//                                 the Mann step (mace.py:111-117) fused behind)
+//   K3  k_fp_agents / k_fp_rows   forward projection, e = y - A z (icd.py:200,210-211;
+//                                 geometry.py:261-270)
+//       k_like / k_prior_cost     costs (models.py:235-257)
+//   K4  k_consensus / k_norms /   average (mace.py:71-90), relnorm and divergence test
+//       k_finish                  (mace.py:309-318), log row
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+struct PriorC {
+    int kind;  // 0 quadratic-mrf, 1 qggmrf  (models.py:43-44)
+    int p_is_2;
+    float eps2;      // 2 * eps_reg
+    float inv_Tsx;   // 1 / (T sigma_x)
+    float inv_sxp;   // sigma_x^-p
+    float qp;        // q / p
+    float qmp;       // q - p
+    float pm1, pm2;  // p - 1, p - 2
+    float floor_;    // 1e-9 T sigma_x
+    float inv_sx2;   // 1 / sigma_x^2
+    double p, q, T, sx, eps;  // double copies for the cost kernels
+};
+
+struct AgentDev {
+    float2* el;        // [R] {e, lambda}: error sinogram and weights, interleaved
+    float* y;          // [R]
+    float* z;          // [n] agent state X_i
+    float* w;          // [n] stack component w_i
+    float* th;         // [n] theta2 data term, sum a^2 lambda (icd.py:193-195)
+    float* vt;         // [n] explicit proximal target (plain passes)
+    const int* views;  // [V] global view index of local view j
+    // super-voxel layout
+    const int2* band;   // [n_sv * V]
+    const int* bsize;   // [n_sv]
+    const int2* pix;    // [n_sv * S * S]
+    const float* val;
+    const uint16_t* idx;
+    // raster layout
+    const int2* rpix;   // [n]
+    const uint32_t* ridx;
+    const float* rval;
+    int R, V, n_sv_side;
+    float beta_eff, inv_s2;
+    int clamp;
+};
+
+struct PassParams {
+    const AgentDev* agents;
+    PriorC pr;
+    int n_side, S, mode;  // mode 0: v from vt; 1: MACE (v = 2 g - w, Mann epilogue)
+    const float* g;       // consensus image G(w) or G_H(w)
+    float rho;
+    const uint32_t* queue;
+    int n_items;
+    unsigned* head;
+    double* part;  // [n_items * 4]: sum alpha^2, sum (w'-w)^2, sum w'^2, sum w^2
+    int band_cap;
+    const int* done;
+    long s_begin, s_end;  // raster passes: pixel range [s_begin, s_end) (icd.py:222-246)
+};
+
+__constant__ int c_dr[8] = {-1, -1, -1, 0, 0, 1, 1, 1};  // models.py:50
+__constant__ int c_dc[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+__constant__ float c_nw[8];  // raw weight / (4 + 2 sqrt 2), models.py:51-52,107
+
+// ---- qGGMRF potential derivatives in fp32 (icd.py:45-64)
+__device__ __forceinline__ float pow_pos(float x, float e) { return exp2f(e * log2f(x)); }
+
+__device__ __forceinline__ float qg_influence(float d, const PriorC& P)
+{
+    const float ad = fabsf(d);
+    if (ad == 0.0f) return 0.0f;
+    const float um = pow_pos(ad * P.inv_Tsx, P.qmp);
+    const float base = P.p_is_2 ? ad : pow_pos(ad, P.pm1);
+    const float opu = 1.0f + um;
+    const float val = (base * P.inv_sxp) * um * (P.qp + um) / (opu * opu);
+    return d > 0.0f ? val : -val;
+}
+
+__device__ __forceinline__ float qg_coef(float d, const PriorC& P)
+{
+    float ad = fabsf(d);
+    if (ad <= P.floor_) {
+        if (P.p_is_2) return P.inv_sx2;
+        ad = P.floor_;
+    }
+    const float um = pow_pos(ad * P.inv_Tsx, P.qmp);
+    const float base = P.p_is_2 ? 1.0f : pow_pos(ad, P.pm2);
+    const float opu = 1.0f + um;
+    return (base * P.inv_sxp) * um * (P.qp + um) / (opu * opu);
+}
+
+__device__ __forceinline__ float warp_sum(float v)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+// Neighbour term of one lane (lanes 0..7 own neighbour k = lane; models.py:50-52 order).
+__device__ __forceinline__ void prior_lane(int lane, float zs, float zr, bool valid, const PriorC& P,
+                                           float& g, float& c)
+{
+    g = 0.f;
+    c = 0.f;
+    if (lane < 8 && valid) {
+        const float wk = c_nw[lane];
+        if (P.kind == 0) {
+            g = wk * (zs - zr);
+            c = wk;
+        } else {
+            const float d = zs - zr;
+            g = wk * qg_influence(d, P);
+            c = wk * qg_coef(d, P);
+        }
+    }
+}
+
+// 1-D surrogate solve (icd.py:128-134); returns false where the reference `continue`s.
+__device__ __forceinline__ bool pixel_step(float t, float g, float c, float zs, float v, float th, float beta,
+                                           float inv_s2, int clamp, const PriorC& P, float& alpha)
+{
+    float gp = 0.f, cp = 0.f;
+    if (beta > 0.f) {
+        if (P.kind == 0) {
+            gp = beta * (g + P.eps2 * zs);
+            cp = beta * (c + P.eps2);
+        } else {
+            gp = beta * g;
+            cp = beta * c;
+        }
+    }
+    const float num = t - gp - inv_s2 * (zs - v);
+    const float den = th + cp + inv_s2;
+    if (!(den > 0.f)) return false;
+    alpha = num / den;
+    if (clamp && zs + alpha < 0.f) alpha = -zs;
+    return true;
+}
+
+// ===========================================================================
+// K2 super-voxel pass.  One warp owns one (agent, super-voxel) work item at a
+// time, taken from a global queue in colour-class order, so concurrently
+// active tiles are spread across the image.  The tile's error-sinogram band
+// (one channel window per view) is staged in shared memory; the tile's pixels
+// are then updated sequentially in tile-raster order against the staged band
+// (Gauss-Seidel inside the tile), and the band's net change is folded back
+// into global e with red.add at the end (tiles of the same agent that run
+// concurrently see each other one tile late: the bounded-staleness schedule
+// of DESIGN.md §4).  Column entries are streamed with 128-bit loads D pixels
+// ahead of use.
+// ===========================================================================
+template <int NV, int D>
+__global__ void __launch_bounds__(128) k_icd_sv(PassParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    if (P.done && *P.done) return;
+    const int lane = threadIdx.x & 31;
+    const int S = P.S, SS = S * S, S2 = S + 2, T2 = S2 * S2, T2p = (T2 + 3) & ~3;
+    const int cap = P.band_cap;  // multiple of 4
+    const size_t per_warp = (size_t)12 * cap + 4 * T2p + 16 * SS;
+    unsigned char* base = smem + (threadIdx.x >> 5) * per_warp;
+    float2* sel = reinterpret_cast<float2*>(base);
+    float* se0 = reinterpret_cast<float*>(base + 8 * (size_t)cap);
+    float* zt = se0 + cap;
+    float* svv = zt + T2p;
+    float* sth = svv + SS;
+    int2* spe = reinterpret_cast<int2*>(sth + SS);
+    const int n = P.n_side;
+    const PriorC& PR = P.pr;
+
+    for (;;) {
+        unsigned item = 0;
+        if (lane == 0) item = atomicAdd(P.head, 1u);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= (unsigned)P.n_items) break;
+        const uint32_t code = __ldg(P.queue + item);
+        const AgentDev& A = P.agents[code >> 24];
+        const int sv = (int)(code & 0xffffffu);
+        float2* __restrict__ el = A.el;
+        float* __restrict__ z = A.z;
+        float* __restrict__ w = A.w;
+        const int V = A.V;
+        const int r0 = (sv / A.n_sv_side) * S, c0 = (sv % A.n_sv_side) * S;
+        const float beta = A.beta_eff, inv_s2 = A.inv_s2;
+        const int clamp = A.clamp;
+
+        // -- stage the band: half a warp per view
+        const int2* bt = A.band + (size_t)sv * V;
+        for (int j = lane >> 4; j < V; j += 2) {
+            const int2 b = __ldg(bt + j);
+            const int cnt = b.y & 0xffff, pos = b.y >> 16;
+            for (int c = lane & 15; c < cnt; c += 16) {
+                const float2 x = __ldcg(el + b.x + c);
+                sel[pos + c] = x;
+                se0[pos + c] = x.x;
+            }
+        }
+        // -- state tile with a one-pixel halo, targets, theta2, column table
+        for (int i = lane; i < T2; i += 32) {
+            const int rr = r0 - 1 + i / S2, cc = c0 - 1 + i % S2;
+            zt[i] = (rr >= 0 && rr < n && cc >= 0 && cc < n) ? __ldcg(z + (size_t)rr * n + cc) : 0.f;
+        }
+        for (int i = lane; i < SS; i += 32) {
+            const int rr = r0 + i / S, cc = c0 + i % S;
+            spe[i] = __ldg(A.pix + (size_t)sv * SS + i);
+            if (rr < n && cc < n) {
+                const size_t s = (size_t)rr * n + cc;
+                sth[i] = A.th[s];
+                svv[i] = P.mode ? 2.f * P.g[s] - w[s] : A.vt[s];
+            }
+        }
+        __syncwarp();
+
+        // -- sequential pixel loop, columns prefetched D pixels ahead
+        const float* __restrict__ av = A.val;
+        const uint16_t* __restrict__ ai = A.idx;
+        float4 rv[D][NV];
+        uint2 ri[D][NV];
+        auto fetch = [&](int k, float4 (&v4)[NV], uint2 (&i4)[NV]) {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                v4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                i4[j] = make_uint2(0u, 0u);
+            }
+            if (k < SS) {
+                const int2 pe = spe[k];
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                    const int e0 = 4 * (lane + 32 * j);
+                    if (e0 < pe.y) {
+                        v4[j] = __ldcs(reinterpret_cast<const float4*>(av + pe.x + e0));
+                        i4[j] = __ldcs(reinterpret_cast<const uint2*>(ai + pe.x + e0));
+                    }
+                }
+            }
+        };
+#pragma unroll
+        for (int u = 0; u < D; ++u) fetch(u, rv[u], ri[u]);
+        double dsq = 0.0;
+        for (int kb = 0; kb < SS; kb += D) {
+#pragma unroll
+            for (int u = 0; u < D; ++u) {
+                const int k = kb + u;
+                if (k < SS) {
+                    const int lr = k / S, lc = k % S;
+                    if (r0 + lr < n && c0 + lc < n) {
+                        const int len = spe[k].y;
+                        const int ci = (lr + 1) * S2 + (lc + 1);
+                        const float zs = zt[ci];
+                        float t = 0.f;
+#pragma unroll
+                        for (int j = 0; j < NV; ++j) {
+                            const int e0 = 4 * (lane + 32 * j);
+                            const float vv[4] = {rv[u][j].x, rv[u][j].y, rv[u][j].z, rv[u][j].w};
+                            const uint32_t ii[4] = {ri[u][j].x & 0xffffu, ri[u][j].x >> 16, ri[u][j].y & 0xffffu,
+                                                    ri[u][j].y >> 16};
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                if (e0 + q < len) {
+                                    const float2 x = sel[ii[q]];
+                                    t = fmaf(vv[q] * x.y, x.x, t);
+                                }
+                        }
+                        float g, c;
+                        {
+                            const int kk = lane & 7;
+                            const int gr = r0 + lr + c_dr[kk], gc = c0 + lc + c_dc[kk];
+                            const bool valid = gr >= 0 && gr < n && gc >= 0 && gc < n;
+                            const float zr = zt[(lr + 1 + c_dr[kk]) * S2 + (lc + 1 + c_dc[kk])];
+                            prior_lane(lane, zs, zr, valid && beta > 0.f, PR, g, c);
+                        }
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) {
+                            t += __shfl_xor_sync(FULL, t, o);
+                            g += __shfl_xor_sync(FULL, g, o);
+                            c += __shfl_xor_sync(FULL, c, o);
+                        }
+                        float alpha;
+                        if (pixel_step(t, g, c, zs, svv[k], sth[k], beta, inv_s2, clamp, PR, alpha)) {
+                            if (lane == 0) {
+                                zt[ci] = zs + alpha;
+                                dsq += (double)alpha * alpha;
+                            }
+#pragma unroll
+                            for (int j = 0; j < NV; ++j) {
+                                const int e0 = 4 * (lane + 32 * j);
+                                const float vv[4] = {rv[u][j].x, rv[u][j].y, rv[u][j].z, rv[u][j].w};
+                                const uint32_t ii[4] = {ri[u][j].x & 0xffffu, ri[u][j].x >> 16,
+                                                        ri[u][j].y & 0xffffu, ri[u][j].y >> 16};
+#pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    if (e0 + q < len) sel[ii[q]].x -= alpha * vv[q];
+                            }
+                        }
+                        __syncwarp();
+                    }
+                }
+                fetch(k + D, rv[u], ri[u]);
+            }
+        }
+        __syncwarp();
+
+        // -- fold the band's change back into global e
+        for (int j = lane >> 4; j < V; j += 2) {
+            const int2 b = __ldg(bt + j);
+            const int cnt = b.y & 0xffff, pos = b.y >> 16;
+            for (int c = lane & 15; c < cnt; c += 16) {
+                const float d = sel[pos + c].x - se0[pos + c];
+                if (d != 0.f) atomicAdd(&el[b.x + c].x, d);
+            }
+        }
+        // -- write the tile back; fused Mann step and norm partials
+        double dw2 = 0.0, wn2 = 0.0, wo2 = 0.0;
+        for (int i = lane; i < SS; i += 32) {
+            const int rr = r0 + i / S, cc = c0 + i % S;
+            if (rr < n && cc < n) {
+                const size_t s = (size_t)rr * n + cc;
+                const float zn = zt[(i / S + 1) * S2 + (i % S + 1)];
+                __stcg(z + s, zn);
+                if (P.mode) {
+                    const float wo = w[s];
+                    const float wn = P.rho * (2.f * zn - svv[i]) + (1.f - P.rho) * wo;
+                    w[s] = wn;
+                    const double dd = (double)wn - (double)wo;
+                    dw2 += dd * dd;
+                    wn2 += (double)wn * wn;
+                    wo2 += (double)wo * wo;
+                }
+            }
+        }
+        dw2 = warp_sum_d(dw2);
+        wn2 = warp_sum_d(wn2);
+        wo2 = warp_sum_d(wo2);
+        if (lane == 0) {
+            double* o = P.part + (size_t)item * 4;
+            o[0] = dsq;
+            o[1] = dw2;
+            o[2] = wn2;
+            o[3] = wo2;
+        }
+        __syncwarp();
+    }
+}
+
+// ===========================================================================
+// K2 raster pass: the reference's exact visiting order (pixels 0..n-1), one
+// warp per agent, e and z in global memory.  This is the per-pass parity mode
+// (it reproduces partial_update_prox pass by pass, to fp32 rounding).
+// ===========================================================================
+template <int NV>
+__global__ void __launch_bounds__(32) k_icd_raster(PassParams P, int agent_base)
+{
+    if (P.done && *P.done) return;
+    const int lane = threadIdx.x & 31;
+    const int item = blockIdx.x;
+    const AgentDev& A = P.agents[agent_base + item];
+    const int n = P.n_side;
+    const PriorC& PR = P.pr;
+    float2* el = A.el;
+    float* z = A.z;
+    const float beta = A.beta_eff, inv_s2 = A.inv_s2;
+    double dsq = 0.0;
+    const size_t N = (size_t)n * n;
+    for (size_t s = (size_t)P.s_begin; s < (size_t)P.s_end && s < N; ++s) {
+        const int2 pe = A.rpix[s];
+        const int r = (int)(s / n), col = (int)(s % n);
+        const float zs = __ldcg(z + s);
+        float vv4[NV][4];
+        uint32_t ii4[NV][4];
+        float t = 0.f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const int e0 = 4 * (lane + 32 * j);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                vv4[j][q] = 0.f;
+                ii4[j][q] = 0;
+            }
+            if (e0 < pe.y) {
+                const float4 v4 = *reinterpret_cast<const float4*>(A.rval + pe.x + e0);
+                const uint4 i4 = *reinterpret_cast<const uint4*>(A.ridx + pe.x + e0);
+                vv4[j][0] = v4.x; vv4[j][1] = v4.y; vv4[j][2] = v4.z; vv4[j][3] = v4.w;
+                ii4[j][0] = i4.x; ii4[j][1] = i4.y; ii4[j][2] = i4.z; ii4[j][3] = i4.w;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (e0 + q < pe.y) {
+                    const float2 x = __ldcg(el + ii4[j][q]);
+                    t = fmaf(vv4[j][q] * x.y, x.x, t);
+                }
+        }
+        float g, c;
+        {
+            const int kk = lane & 7;
+            const int gr = r + c_dr[kk], gc = col + c_dc[kk];
+            const bool valid = gr >= 0 && gr < n && gc >= 0 && gc < n;
+            const float zr = valid ? __ldcg(z + (size_t)gr * n + gc) : 0.f;
+            prior_lane(lane, zs, zr, valid && beta > 0.f, PR, g, c);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            t += __shfl_xor_sync(FULL, t, o);
+            g += __shfl_xor_sync(FULL, g, o);
+            c += __shfl_xor_sync(FULL, c, o);
+        }
+        const float v = P.mode ? 2.f * P.g[s] - A.w[s] : A.vt[s];
+        float alpha;
+        if (pixel_step(t, g, c, zs, v, A.th[s], beta, inv_s2, A.clamp, PR, alpha)) {
+            if (lane == 0) {
+                __stcg(z + s, zs + alpha);
+                dsq += (double)alpha * alpha;
+            }
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                const int e0 = 4 * (lane + 32 * j);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (e0 + q < pe.y) {
+                        float* ep = &el[ii4[j][q]].x;
+                        __stcg(ep, __ldcg(ep) - alpha * vv4[j][q]);
+                    }
+            }
+        }
+        __syncwarp();
+    }
+    // fused Mann step (mace.py:307) over the whole image
+    double dw2 = 0.0, wn2 = 0.0, wo2 = 0.0;
+    if (P.mode) {
+        for (size_t s = lane; s < N; s += 32) {
+            const float zn = __ldcg(z + s);
+            const float wo = A.w[s];
+            const float v = 2.f * P.g[s] - wo;
+            const float wn = P.rho * (2.f * zn - v) + (1.f - P.rho) * wo;
+            A.w[s] = wn;
+            const double dd = (double)wn - (double)wo;
+            dw2 += dd * dd;
+            wn2 += (double)wn * wn;
+            wo2 += (double)wo * wo;
+        }
+    }
+    dw2 = warp_sum_d(dw2);
+    wn2 = warp_sum_d(wn2);
+    wo2 = warp_sum_d(wo2);
+    if (lane == 0) {
+        double* o = P.part + (size_t)item * 4;
+        o[0] = dsq;
+        o[1] = dw2;
+        o[2] = wn2;
+        o[3] = wo2;
+    }
+}
+
+// ===========================================================================
+// K3: forward projection.  One warp per sinogram row over the global CSR
+// (fixed reduction order -> deterministic).  Agent refresh writes
+// e = y - A_i z into the agent's interleaved {e, lambda} array.
+// ===========================================================================
+struct FPParams {
+    const int64_t* rp;
+    const int* cols;
+    const float* vals;
+    int n_ch;
+};
+
+__global__ void k_fp_agents(FPParams F, const AgentDev* agents, const int* row_base, int n_agents,
+                            int total_rows, const int* done)
+{
+    if (done && *done) return;
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int wr = gw; wr < total_rows; wr += nw) {
+        int a = 0;
+        while (a + 1 < n_agents && row_base[a + 1] <= wr) ++a;
+        const AgentDev& A = agents[a];
+        const int r = wr - row_base[a];
+        const int j = r / F.n_ch, ch = r % F.n_ch;
+        const int64_t g = (int64_t)A.views[j] * F.n_ch + ch;
+        float acc = 0.f;
+        for (int64_t k = F.rp[g] + lane; k < F.rp[g + 1]; k += 32) acc = fmaf(F.vals[k], __ldcg(A.z + F.cols[k]), acc);
+        acc = warp_sum(acc);
+        if (lane == 0) A.el[r].x = A.y[r] - acc;
+    }
+}
+
+// out[g] = (A x)[g] for all rows; optional weighted residual partials 0.5 lambda (y - Ax)^2
+__global__ void k_fp_rows(FPParams F, int n_rows, const float* x, float* out, const float* y, const float* lam,
+                          double* part)
+{
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    double loc = 0.0;
+    for (int g = gw; g < n_rows; g += nw) {
+        float acc = 0.f;
+        for (int64_t k = F.rp[g] + lane; k < F.rp[g + 1]; k += 32) acc = fmaf(F.vals[k], x[F.cols[k]], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) {
+            if (out) out[g] = acc;
+            if (part) {
+                const double r = (double)y[g] - (double)acc;
+                loc += 0.5 * (double)lam[g] * r * r;
+            }
+        }
+    }
+    if (part) {
+        __shared__ double sh[32];
+        if (lane == 0) sh[threadIdx.x >> 5] = loc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sh[i];
+            part[blockIdx.x] = s;
+        }
+    }
+}
+
+// beta * h(x), pairs s < r only (models.py:111-118,248-257), fp64 arithmetic
+__device__ __forceinline__ double qg_potential_d(double d, const PriorC& P)
+{
+    const double ad = fabs(d);
+    const double u = ad / (P.T * P.sx);
+    if (!(u > 0.0)) return 0.0;
+    const double um = pow(u, P.q - P.p);
+    return (pow(ad, P.p) / (P.p * pow(P.sx, P.p))) * (um / (1.0 + um));
+}
+
+__global__ void k_prior_cost(const float* x, int n_side, PriorC P, double* part)
+{
+    const size_t N = (size_t)n_side * n_side;
+    double loc = 0.0;
+    for (size_t s = blockIdx.x * (size_t)blockDim.x + threadIdx.x; s < N; s += (size_t)gridDim.x * blockDim.x) {
+        const int r = (int)(s / n_side), c = (int)(s % n_side);
+        const double xs = x[s];
+        for (int k = 4; k < 8; ++k) {  // offsets (0,1), (1,-1), (1,0), (1,1): exactly the r > s partners
+            const int rr = r + c_dr[k], cc = c + c_dc[k];
+            if (rr < 0 || rr >= n_side || cc < 0 || cc >= n_side) continue;
+            const double d = xs - (double)x[(size_t)rr * n_side + cc];
+            const double wk = (double)c_nw[k];
+            loc += P.kind == 0 ? 0.5 * wk * d * d : wk * qg_potential_d(d, P);
+        }
+        if (P.kind == 0) loc += P.eps * xs * xs;
+    }
+    __shared__ double sh[1024];
+    sh[threadIdx.x] = loc;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+// ===========================================================================
+// theta2 = sum_rows a^2 lambda per pixel (icd.py:193-195), deterministic
+// ===========================================================================
+__global__ void k_theta2_raster(const AgentDev* agents, int n_agents, int n)
+{
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const long total = (long)n_agents * n;
+    for (long it = gw; it < total; it += nw) {
+        const AgentDev& A = agents[it / n];
+        const int s = (int)(it % n);
+        const int2 pe = A.rpix[s];
+        float acc = 0.f;
+        for (int k = lane; k < pe.y; k += 32) {
+            const float a = A.rval[pe.x + k];
+            acc = fmaf(a * a, A.el[A.ridx[pe.x + k]].y, acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) A.th[s] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(128) k_theta2_sv(const AgentDev* agents, int n_items, const uint32_t* queue,
+                                                   int n_side, int S, int cap)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* lamb = reinterpret_cast<float*>(smem) + (threadIdx.x >> 5) * (size_t)cap;
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const int SS = S * S;
+    for (int item = gw; item < n_items; item += nw) {
+        const uint32_t code = queue[item];
+        const AgentDev& A = agents[code >> 24];
+        const int sv = (int)(code & 0xffffffu);
+        const int r0 = (sv / A.n_sv_side) * S, c0 = (sv % A.n_sv_side) * S;
+        const int2* bt = A.band + (size_t)sv * A.V;
+        for (int j = lane >> 4; j < A.V; j += 2) {
+            const int2 b = bt[j];
+            const int cnt = b.y & 0xffff, pos = b.y >> 16;
+            for (int c = lane & 15; c < cnt; c += 16) lamb[pos + c] = A.el[b.x + c].y;
+        }
+        __syncwarp();
+        for (int k = 0; k < SS; ++k) {
+            const int rr = r0 + k / S, cc = c0 + k % S;
+            if (rr >= n_side || cc >= n_side) continue;
+            const int2 pe = A.pix[(size_t)sv * SS + k];
+            float acc = 0.f;
+            for (int e = lane; e < pe.y; e += 32) {
+                const float a = A.val[pe.x + e];
+                acc = fmaf(a * a, lamb[A.idx[pe.x + e]], acc);
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) A.th[(size_t)rr * n_side + cc] = acc;
+        }
+        __syncwarp();
+    }
+}
+
+// agent rows <- global y / lambda (local row r = j n_ch + c, icd.py:187-188)
+__global__ void k_gather_data(const AgentDev* agents, const int* row_base, int n_agents, int total_rows, int n_ch,
+                              const float* y, const float* lam)
+{
+    for (int wr = blockIdx.x * blockDim.x + threadIdx.x; wr < total_rows; wr += gridDim.x * blockDim.x) {
+        int a = 0;
+        while (a + 1 < n_agents && row_base[a + 1] <= wr) ++a;
+        const AgentDev& A = agents[a];
+        const int r = wr - row_base[a];
+        const int64_t g = (int64_t)A.views[r / n_ch] * n_ch + r % n_ch;
+        A.y[r] = y[g];
+        A.el[r].y = lam[g];
+    }
+}
+
+// ===========================================================================
+// K4: consensus average in the reference's fixed pairwise-tree order
+// (mace.py:71-90), optionally the local partial sum for multi-rank runs.
+// ===========================================================================
+__global__ void k_consensus(const float* W, int n_local, size_t n, float scale, float* out, const float* ref,
+                            double* ref_part, const int* done)
+{
+    if (done && *done) return;
+    double loc = 0.0;
+    for (size_t s = blockIdx.x * (size_t)blockDim.x + threadIdx.x; s < n; s += (size_t)gridDim.x * blockDim.x) {
+        float acc[64];
+        for (int i = 0; i < n_local; ++i) acc[i] = W[(size_t)i * n + s];
+        int m = n_local;
+        while (m > 1) {
+            const int half = m / 2;
+            for (int i = 0; i < half; ++i) acc[i] += acc[half + i];
+            if (m % 2) {
+                acc[half] = acc[2 * half];
+                m = half + 1;
+            } else {
+                m = half;
+            }
+        }
+        const float v = acc[0] / scale;
+        out[s] = v;
+        if (ref) {
+            const double d = (double)v - (double)ref[s];
+            loc += d * d;
+        }
+    }
+    if (ref_part) {
+        __shared__ double sh[256];
+        sh[threadIdx.x] = loc;
+        __syncthreads();
+        for (int o = blockDim.x / 2; o; o >>= 1) {
+            if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) ref_part[blockIdx.x] = sh[0];
+    }
+}
+
+// fixed-order reduction of the per-item partials -> out4 (and nrmse^2 partials -> out4[4])
+__global__ void k_norms(const double* part, int n_items, const double* ref_part, int n_ref, double* out5,
+                        const int* done)
+{
+    if (done && *done) return;
+    __shared__ double sh[4][256];
+    __shared__ double shr[256];
+    double a[4] = {0, 0, 0, 0}, r = 0.0;
+    for (int i = threadIdx.x; i < n_items; i += blockDim.x)
+        for (int k = 0; k < 4; ++k) a[k] += part[(size_t)i * 4 + k];
+    if (ref_part)
+        for (int i = threadIdx.x; i < n_ref; i += blockDim.x) r += ref_part[i];
+    for (int k = 0; k < 4; ++k) sh[k][threadIdx.x] = a[k];
+    shr[threadIdx.x] = r;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            for (int k = 0; k < 4; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + o];
+            shr[threadIdx.x] += shr[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 4; ++k) out5[k] = sh[k][0];
+        out5[4] = shr[0];
+    }
+}
+
+// relnorm, divergence and stop test (mace.py:309-318,337-339); log row [relnorm, |w'|, sum a^2, nrmse^2]
+__global__ void k_finish(const double* sums5, double ref_norm2, double tol, int iter, double* log, int* done,
+                         unsigned* head)
+{
+    if (*done) return;
+    const double dw2 = sums5[1], wn2 = sums5[2], wo2 = sums5[3];
+    const double nn = sqrt(wn2);
+    const double rel = sqrt(dw2) / fmax(sqrt(wo2), 1e-300);
+    double* L = log + (size_t)iter * 4;
+    L[0] = rel;
+    L[1] = nn;
+    L[2] = sums5[0];
+    L[3] = ref_norm2 > 0.0 ? sqrt(sums5[4] / ref_norm2) : -1.0;
+    if (!isfinite(nn)) {
+        done[0] = 2;
+        done[1] = iter + 1;
+    } else if (rel < tol) {
+        done[0] = 1;
+        done[1] = iter + 1;
+    }
+    *head = 0u;
+}
+
+__global__ void k_reset_head(unsigned* head) { *head = 0u; }
+
+__global__ void k_fill(float* p, size_t n, float v)
+{
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__global__ void k_broadcast_state(const AgentDev* agents, int n_agents, const float* x, size_t n)
+{
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n * n_agents; i += (size_t)gridDim.x * blockDim.x)
+        agents[i / n].z[i % n] = x[i % n];
+}
+
+}  // namespace mace

@@ -1,0 +1,1007 @@
+// libmace_b200: device context, launches and the C ABI (include/mace_b200.h).
+//
+// One context = one GPU, the full-data operator (global CSR for K3), one
+// sinogram, and the agents this rank owns (view subsets, geometry.py:161-174).
+// All device memory is owned here; host pointers are borrowed for the call.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "internal.h"
+#include "kernels.cuh"
+#include "mace_b200.h"
+
+namespace mace {
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+#define CK(x)                                                                                              \
+    do {                                                                                                   \
+        cudaError_t e_ = (x);                                                                              \
+        if (e_ != cudaSuccess)                                                                             \
+            throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_) + " (" + __FILE__ + ":" +      \
+                            std::to_string(__LINE__) + ")");                                               \
+    } while (0)
+
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count)
+    {
+        free();
+        n = count;
+        if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void free()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DBuf() { free(); }
+};
+
+struct AgentMem {
+    std::vector<int> views;
+    DBuf<int> d_views;
+    DBuf<int2> band, pix, rpix;
+    DBuf<int> bsize;
+    DBuf<float> val, rval;
+    DBuf<uint16_t> idx;
+    DBuf<uint32_t> ridx;
+    int R = 0, n_sv_side = 0, n_sv = 0, max_band = 0, max_col = 0;
+    int64_t entries = 0, nnz = 0, duplicates = 0;
+    DBuf<uint32_t> queue;  // this agent alone, colour order
+    float beta_eff = 0.f, inv_s2 = 0.f;
+    int clamp = 0;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = true;
+    int n_side = 0, n_views = 0, n_ch = 0;
+    size_t n = 0;
+    DBuf<int64_t> rp;
+    DBuf<int> cols;
+    DBuf<float> vals;
+    int64_t nnz = 0;
+    DBuf<float> y, lam;
+    PriorC prior{};
+    // agents
+    int n_local = 0, schedule = 0, S = 8, NV = 1;
+    std::vector<std::unique_ptr<AgentMem>> am;
+    std::vector<AgentDev> h_agents;
+    DBuf<AgentDev> d_agents;
+    DBuf<int> row_base;
+    int total_rows = 0;
+    DBuf<float2> EL;
+    DBuf<float> Y, Z, W, TH, VT;
+    DBuf<uint32_t> queue;
+    int n_items = 0;
+    DBuf<double> part;
+    DBuf<unsigned> head;
+    DBuf<int> done;
+    DBuf<double> sums5, log;
+    int log_cap = 0;
+    DBuf<float> wbar, g, ref, wsum;
+    DBuf<double> refpart;
+    double ref_norm2 = 0.0;
+    int band_cap = 0;
+    size_t sv_smem = 0;
+    int sv_grid = 0;
+    int passes = 0;
+    int num_sms = 148;
+    // timing of the last iterate call
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+static const int kRefBlocks = 256;
+
+static void upload_prior_consts()
+{
+    const double raw[8] = {1 / std::sqrt(2.0), 1.0, 1 / std::sqrt(2.0), 1.0, 1.0, 1 / std::sqrt(2.0), 1.0,
+                           1 / std::sqrt(2.0)};
+    const double norm = 4.0 + 2.0 * std::sqrt(2.0);
+    float w[8];
+    for (int k = 0; k < 8; ++k) w[k] = (float)(raw[k] / norm);
+    CK(cudaMemcpyToSymbol(c_nw, w, sizeof(w)));
+}
+
+static void sync(Ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
+
+// ------------------------------------------------------------------ K2 launch helpers
+template <int NV>
+static void launch_sv(Ctx* c, const PassParams& P, int items)
+{
+    auto kern = k_icd_sv<NV, 4>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sv_smem));
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, c->sv_smem));
+    if (nb < 1) throw std::runtime_error("super-voxel kernel does not fit on an SM (band too large)");
+    long grid = (long)nb * c->num_sms;
+    if (const char* e = std::getenv("MACE_SV_MAX_WARPS")) {
+        long mw = std::atol(e);
+        if (mw > 0) grid = std::min(grid, std::max(1L, mw / 4));
+    }
+    grid = std::min<long>(grid, (items + 3) / 4);
+    c->sv_grid = (int)grid;
+    kern<<<(int)grid, 128, c->sv_smem, c->stream>>>(P);
+    CK(cudaGetLastError());
+}
+
+template <int NV>
+static void launch_raster(Ctx* c, const PassParams& P, int n_agents, int agent_base)
+{
+    k_icd_raster<NV><<<n_agents, 32, 0, c->stream>>>(P, agent_base);
+    CK(cudaGetLastError());
+}
+
+static PassParams base_params(Ctx* c)
+{
+    PassParams P{};
+    P.agents = c->d_agents.p;
+    P.pr = c->prior;
+    P.n_side = c->n_side;
+    P.S = c->S;
+    P.band_cap = c->band_cap;
+    P.head = c->head.p;
+    P.part = c->part.p;
+    P.done = c->done.p;
+    return P;
+}
+
+// One pass of every agent in [a0, a0 + na) (or all local agents if na == n_local via the combined queue).
+static void run_pass(Ctx* c, int mode, float rho, const float* gimg, int a0, int na, long s0 = 0, long s1 = -1)
+{
+    PassParams P = base_params(c);
+    P.mode = mode;
+    P.rho = rho;
+    P.g = gimg;
+    P.s_begin = s0;
+    P.s_end = s1 < 0 ? (long)c->n : s1;
+    if (c->schedule == 0 && (P.s_begin != 0 || P.s_end != (long)c->n))
+        throw std::runtime_error("pixel ranges need the raster schedule");
+    if (c->schedule == 1) {
+        switch (c->NV) {
+            case 1: launch_raster<1>(c, P, na, a0); break;
+            case 2: launch_raster<2>(c, P, na, a0); break;
+            default: launch_raster<4>(c, P, na, a0); break;
+        }
+        return;
+    }
+    CK(cudaMemsetAsync(c->head.p, 0, sizeof(unsigned), c->stream));
+    if (na == c->n_local) {
+        P.queue = c->queue.p;
+        P.n_items = c->n_items;
+    } else {
+        if (na != 1) throw std::runtime_error("run_pass: single agent or all agents");
+        P.queue = c->am[a0]->queue.p;
+        P.n_items = c->am[a0]->n_sv;
+    }
+    switch (c->NV) {
+        case 1: launch_sv<1>(c, P, P.n_items); break;
+        case 2: launch_sv<2>(c, P, P.n_items); break;
+        default: launch_sv<4>(c, P, P.n_items); break;
+    }
+}
+
+static void refresh(Ctx* c, int a0, int na)
+{
+    // e = y - A_i z for agents [a0, a0+na)
+    FPParams F{c->rp.p, c->cols.p, c->vals.p, c->n_ch};
+    if (na == c->n_local && a0 == 0) {
+        k_fp_agents<<<std::max(1, std::min(c->num_sms * 16, (c->total_rows + 7) / 8)), 256, 0, c->stream>>>(
+            F, c->d_agents.p, c->row_base.p, c->n_local, c->total_rows, c->done.p);
+    } else {
+        for (int i = 0; i < na; ++i) {
+            const int R = c->h_agents[a0 + i].R;
+            // one agent at a time: row_base[0] == 0, so the agent-local row is the warp's row index
+            k_fp_agents<<<std::max(1, std::min(c->num_sms * 16, (R + 7) / 8)), 256, 0, c->stream>>>(
+                F, c->d_agents.p + a0 + i, c->row_base.p, 1, R, c->done.p);
+        }
+    }
+    CK(cudaGetLastError());
+}
+
+static void compute_theta2(Ctx* c)
+{
+    if (c->schedule == 1) {
+        k_theta2_raster<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_agents.p, c->n_local, (int)c->n);
+    } else {
+        const size_t smem = (size_t)4 * c->band_cap * 4;
+        CK(cudaFuncSetAttribute(k_theta2_sv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_theta2_sv<<<std::max(1, std::min(c->num_sms * 4, (c->n_items + 3) / 4)), 128, smem, c->stream>>>(
+            c->d_agents.p, c->n_items, c->queue.p, c->n_side, c->S, c->band_cap);
+    }
+    CK(cudaGetLastError());
+}
+
+static void consensus(Ctx* c, float scale, float* out, bool with_ref)
+{
+    const int blocks = kRefBlocks;
+    k_consensus<<<blocks, 256, 0, c->stream>>>(c->W.p, c->n_local, c->n, scale, out, with_ref ? c->ref.p : nullptr,
+                                                with_ref ? c->refpart.p : nullptr, c->done.p);
+    CK(cudaGetLastError());
+}
+
+static void ensure_log(Ctx* c, int n)
+{
+    if (n > c->log_cap) {
+        DBuf<double> nl;
+        nl.alloc((size_t)n * 4);
+        if (c->log_cap) CK(cudaMemcpyAsync(nl.p, c->log.p, sizeof(double) * 4 * c->log_cap, cudaMemcpyDeviceToDevice, c->stream));
+        std::swap(c->log.p, nl.p);
+        std::swap(c->log.n, nl.n);
+        c->log_cap = n;
+    }
+}
+
+}  // namespace mace
+
+using namespace mace;
+
+#define API_BEGIN try {
+#define API_END                                   \
+    }                                             \
+    catch (const std::exception& ex)              \
+    {                                             \
+        set_error(ex.what());                     \
+        return -1;                                \
+    }                                             \
+    return 0;
+
+static Ctx* C(void* p)
+{
+    if (!p) throw std::runtime_error("null context");
+    Ctx* c = static_cast<Ctx*>(p);
+    CK(cudaSetDevice(c->device));
+    return c;
+}
+
+extern "C" {
+
+const char* mace_last_error(void) { return g_err.c_str(); }
+int mace_abi_version(void) { return MACE_ABI_VERSION; }
+
+// ------------------------------------------------------------------ tracer
+int mace_sysmat_trace(int n_side, double pixel_pitch, int n_views, int n_channels, const double* ux,
+                      const double* uy, const double* ex, const double* ey, const double* offsets, int n_threads,
+                      void** handle)
+{
+    API_BEGIN
+    if (n_side < 1 || n_views < 1 || n_channels < 1 || !(pixel_pitch > 0)) throw std::runtime_error("bad geometry");
+    *handle = sysmat_trace(n_side, pixel_pitch, n_views, n_channels, ux, uy, ex, ey, offsets, n_threads);
+    API_END
+}
+
+int64_t mace_sysmat_view_nnz(void* handle, int view)
+{
+    SysMat* s = static_cast<SysMat*>(handle);
+    if (!s || view < 0 || view >= s->n_views) return -1;
+    return (int64_t)s->views[view].cols.size();
+}
+
+int mace_sysmat_take_view(void* handle, int view, int64_t* row_ptr, int32_t* cols, double* lens)
+{
+    API_BEGIN
+    SysMat* s = static_cast<SysMat*>(handle);
+    if (!s || view < 0 || view >= s->n_views) throw std::runtime_error("bad view");
+    SysMatView& V = s->views[view];
+    std::memcpy(row_ptr, V.row_ptr.data(), V.row_ptr.size() * sizeof(int64_t));
+    std::memcpy(cols, V.cols.data(), V.cols.size() * sizeof(int32_t));
+    std::memcpy(lens, V.lens.data(), V.lens.size() * sizeof(double));
+    SysMatView().row_ptr.swap(V.row_ptr);
+    std::vector<int32_t>().swap(V.cols);
+    std::vector<double>().swap(V.lens);
+    API_END
+}
+
+void mace_sysmat_free(void* handle) { delete static_cast<SysMat*>(handle); }
+
+// ------------------------------------------------------------------ context
+int mace_ctx_create(int device, void** out)
+{
+    API_BEGIN
+    auto c = std::make_unique<Ctx>();
+    c->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    c->head.alloc(1);
+    c->done.alloc(2);
+    c->sums5.alloc(5);
+    CK(cudaMemset(c->head.p, 0, sizeof(unsigned)));
+    CK(cudaMemset(c->done.p, 0, 2 * sizeof(int)));
+    upload_prior_consts();
+    *out = c.release();
+    API_END
+}
+
+void mace_ctx_destroy(void* p)
+{
+    if (!p) return;
+    Ctx* c = static_cast<Ctx*>(p);
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    cudaEventDestroy(c->ev0);
+    cudaEventDestroy(c->ev1);
+    delete c;
+}
+
+int mace_ctx_stream(void* p, void** stream)
+{
+    API_BEGIN
+    *stream = (void*)C(p)->stream;
+    API_END
+}
+
+int mace_sync(void* p)
+{
+    API_BEGIN
+    sync(C(p));
+    API_END
+}
+
+int mace_load_matrix(void* p, int n_side, int n_views, int n_ch, const int64_t* row_ptr, const int32_t* cols,
+                     const float* vals)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    const int64_t rows = (int64_t)n_views * n_ch;
+    c->n_side = n_side;
+    c->n_views = n_views;
+    c->n_ch = n_ch;
+    c->n = (size_t)n_side * n_side;
+    c->nnz = row_ptr[rows];
+    c->rp.alloc(rows + 1);
+    c->cols.alloc(c->nnz);
+    c->vals.alloc(c->nnz);
+    CK(cudaMemcpy(c->rp.p, row_ptr, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->cols.p, cols, sizeof(int32_t) * c->nnz, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->vals.p, vals, sizeof(float) * c->nnz, cudaMemcpyHostToDevice));
+    c->y.alloc(rows);
+    c->lam.alloc(rows);
+    c->wbar.alloc(c->n);
+    c->g.alloc(c->n);
+    c->ref.alloc(c->n);
+    c->wsum.alloc(c->n);
+    c->refpart.alloc(kRefBlocks);
+    API_END
+}
+
+int mace_set_prior(void* p, int kind, double p_, double q, double T, double sx, double eps)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    PriorC& P = c->prior;
+    P.kind = kind;
+    P.p_is_2 = (p_ == 2.0);
+    P.eps2 = (float)(2.0 * eps);
+    P.inv_Tsx = (float)(1.0 / (T * sx));
+    P.inv_sxp = (float)(1.0 / std::pow(sx, p_));
+    P.qp = (float)(q / p_);
+    P.qmp = (float)(q - p_);
+    P.pm1 = (float)(p_ - 1.0);
+    P.pm2 = (float)(p_ - 2.0);
+    P.floor_ = (float)(1e-9 * T * sx);
+    P.inv_sx2 = (float)(1.0 / (sx * sx));
+    P.p = p_;
+    P.q = q;
+    P.T = T;
+    P.sx = sx;
+    P.eps = eps;
+    API_END
+}
+
+int mace_setup_agents(void* p, int n_local, const int* view_counts, const int* views, int schedule, int svs,
+                      int colours, int n_threads)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (!c->nnz && !c->rp.p) throw std::runtime_error("load the system matrix first");
+    if (n_local < 1 || n_local > 64) throw std::runtime_error("1..64 agents per context");
+    if (schedule == 0 && (svs < 2 || (svs & 1))) throw std::runtime_error("super-voxel side must be even and >= 2");
+    c->n_local = n_local;
+    c->schedule = schedule;
+    c->S = schedule == 0 ? svs : c->n_side;
+    c->am.clear();
+    int off = 0;
+    for (int a = 0; a < n_local; ++a) {
+        auto m = std::make_unique<AgentMem>();
+        m->views.assign(views + off, views + off + view_counts[a]);
+        off += view_counts[a];
+        for (int v : m->views)
+            if (v < 0 || v >= c->n_views) throw std::runtime_error("view index out of range");
+        m->R = (int)m->views.size() * c->n_ch;
+        c->am.push_back(std::move(m));
+    }
+    // host layout build (CSR download is avoided: we keep a host copy only transiently)
+    const int64_t rows = (int64_t)c->n_views * c->n_ch;
+    std::vector<int64_t> h_rp(rows + 1);
+    std::vector<int32_t> h_cols(c->nnz);
+    std::vector<float> h_vals(c->nnz);
+    CK(cudaMemcpy(h_rp.data(), c->rp.p, sizeof(int64_t) * (rows + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h_cols.data(), c->cols.p, sizeof(int32_t) * c->nnz, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h_vals.data(), c->vals.p, sizeof(float) * c->nnz, cudaMemcpyDeviceToHost));
+    if (n_threads <= 0) n_threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    std::vector<std::exception_ptr> errs(n_local);
+    std::vector<RasterLayout> rl(n_local);
+    std::vector<SVLayout> sl(n_local);
+    {
+        std::atomic<int> next(0);
+        auto work = [&]() {
+            for (;;) {
+                int a = next.fetch_add(1);
+                if (a >= n_local) break;
+                try {
+                    AgentCSC csc;
+                    build_agent_csc(c->n_side, c->n_ch, h_rp.data(), h_cols.data(), h_vals.data(), c->am[a]->views, csc);
+                    c->am[a]->nnz = csc.col_ptr.back();
+                    if (schedule == 1) build_raster_layout(csc, (int)c->n, rl[a]);
+                    else build_sv_layout(csc, c->n_side, c->n_ch, (int)c->am[a]->views.size(), svs, sl[a]);
+                } catch (...) {
+                    errs[a] = std::current_exception();
+                }
+            }
+        };
+        std::vector<std::thread> th;
+        for (int t = 0; t < std::min(n_threads, n_local); ++t) th.emplace_back(work);
+        for (auto& t : th) t.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+    }
+    // device buffers
+    c->total_rows = 0;
+    std::vector<int> rb(n_local + 1, 0);
+    for (int a = 0; a < n_local; ++a) rb[a + 1] = rb[a] + c->am[a]->R;
+    c->total_rows = rb[n_local];
+    c->row_base.alloc(n_local + 1);
+    CK(cudaMemcpy(c->row_base.p, rb.data(), sizeof(int) * (n_local + 1), cudaMemcpyHostToDevice));
+    c->EL.alloc(c->total_rows);
+    c->Y.alloc(c->total_rows);
+    c->Z.alloc((size_t)n_local * c->n);
+    c->W.alloc((size_t)n_local * c->n);
+    c->TH.alloc((size_t)n_local * c->n);
+    c->VT.alloc((size_t)n_local * c->n);
+    CK(cudaMemset(c->Z.p, 0, sizeof(float) * n_local * c->n));
+    CK(cudaMemset(c->W.p, 0, sizeof(float) * n_local * c->n));
+    CK(cudaMemset(c->EL.p, 0, sizeof(float2) * c->total_rows));
+    int max_col = 0, max_band = 0, n_sv_side = 1;
+    c->h_agents.assign(n_local, AgentDev{});
+    for (int a = 0; a < n_local; ++a) {
+        AgentMem& m = *c->am[a];
+        m.d_views.alloc(m.views.size());
+        CK(cudaMemcpy(m.d_views.p, m.views.data(), sizeof(int) * m.views.size(), cudaMemcpyHostToDevice));
+        AgentDev& A = c->h_agents[a];
+        A.el = c->EL.p + rb[a];
+        A.y = c->Y.p + rb[a];
+        A.z = c->Z.p + (size_t)a * c->n;
+        A.w = c->W.p + (size_t)a * c->n;
+        A.th = c->TH.p + (size_t)a * c->n;
+        A.vt = c->VT.p + (size_t)a * c->n;
+        A.views = m.d_views.p;
+        A.R = m.R;
+        A.V = (int)m.views.size();
+        if (schedule == 1) {
+            RasterLayout& L = rl[a];
+            m.rpix.alloc(L.pix.size());
+            m.ridx.alloc(L.idx.size());
+            m.rval.alloc(L.val.size());
+            CK(cudaMemcpy(m.rpix.p, L.pix.data(), sizeof(int2) * L.pix.size(), cudaMemcpyHostToDevice));
+            if (L.idx.size()) {
+                CK(cudaMemcpy(m.ridx.p, L.idx.data(), sizeof(uint32_t) * L.idx.size(), cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(m.rval.p, L.val.data(), sizeof(float) * L.val.size(), cudaMemcpyHostToDevice));
+            }
+            m.entries = (int64_t)L.idx.size();
+            m.max_col = L.max_col;
+            A.rpix = m.rpix.p;
+            A.ridx = m.ridx.p;
+            A.rval = m.rval.p;
+            A.n_sv_side = 1;
+            m.n_sv = 1;
+        } else {
+            SVLayout& L = sl[a];
+            m.band.alloc(L.band.size());
+            m.bsize.alloc(L.bsize.size());
+            m.pix.alloc(L.pix.size());
+            m.val.alloc(L.val.size());
+            m.idx.alloc(L.idx.size());
+            CK(cudaMemcpy(m.band.p, L.band.data(), sizeof(int2) * L.band.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(m.bsize.p, L.bsize.data(), sizeof(int) * L.bsize.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(m.pix.p, L.pix.data(), sizeof(int2) * L.pix.size(), cudaMemcpyHostToDevice));
+            if (L.val.size()) {
+                CK(cudaMemcpy(m.val.p, L.val.data(), sizeof(float) * L.val.size(), cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(m.idx.p, L.idx.data(), sizeof(uint16_t) * L.idx.size(), cudaMemcpyHostToDevice));
+            }
+            m.entries = (int64_t)L.val.size();
+            m.max_col = L.max_col;
+            m.max_band = L.max_band;
+            m.n_sv = L.n_sv;
+            m.n_sv_side = L.n_sv_side;
+            m.duplicates = L.duplicates;
+            A.band = m.band.p;
+            A.bsize = m.bsize.p;
+            A.pix = m.pix.p;
+            A.val = m.val.p;
+            A.idx = m.idx.p;
+            A.n_sv_side = L.n_sv_side;
+            n_sv_side = L.n_sv_side;
+            std::vector<uint32_t> q1 = build_queue(1, L.n_sv_side, colours);
+            for (auto& v : q1) v |= ((uint32_t)a << 24);
+            m.queue.alloc(q1.size());
+            CK(cudaMemcpy(m.queue.p, q1.data(), sizeof(uint32_t) * q1.size(), cudaMemcpyHostToDevice));
+        }
+        max_col = std::max(max_col, m.max_col);
+        max_band = std::max(max_band, m.max_band);
+    }
+    c->NV = max_col <= 128 ? 1 : (max_col <= 256 ? 2 : 4);
+    if (max_col > 512) throw std::runtime_error("column longer than 512 entries");
+    c->band_cap = (max_band + 3) & ~3;
+    if (schedule == 0) {
+        std::vector<uint32_t> q = build_queue(n_local, n_sv_side, colours);
+        c->queue.alloc(q.size());
+        CK(cudaMemcpy(c->queue.p, q.data(), sizeof(uint32_t) * q.size(), cudaMemcpyHostToDevice));
+        c->n_items = (int)q.size();
+        const int S = c->S, T2p = ((S + 2) * (S + 2) + 3) & ~3;
+        c->sv_smem = (size_t)4 * (12 * (size_t)c->band_cap + 4 * T2p + 16 * S * S);
+        if (c->sv_smem > 227 * 1024) throw std::runtime_error("super-voxel band does not fit in shared memory");
+    } else {
+        c->n_items = n_local;
+    }
+    c->part.alloc((size_t)std::max(c->n_items, n_local) * 4);
+    c->d_agents.alloc(n_local);
+    for (int a = 0; a < n_local; ++a) {
+        c->h_agents[a].beta_eff = c->am[a]->beta_eff;
+        c->h_agents[a].inv_s2 = c->am[a]->inv_s2;
+        c->h_agents[a].clamp = c->am[a]->clamp;
+    }
+    CK(cudaMemcpy(c->d_agents.p, c->h_agents.data(), sizeof(AgentDev) * n_local, cudaMemcpyHostToDevice));
+    c->passes = 0;
+    API_END
+}
+
+int mace_agent_info(void* p, int local, int64_t* info /* [8] */)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (local < 0 || local >= c->n_local) throw std::runtime_error("bad agent");
+    AgentMem& m = *c->am[local];
+    info[0] = m.nnz;
+    info[1] = m.entries;
+    info[2] = m.R;
+    info[3] = m.max_col;
+    info[4] = m.max_band;
+    info[5] = m.n_sv;
+    info[6] = m.duplicates;
+    info[7] = c->band_cap;
+    API_END
+}
+
+int mace_ctx_info(void* p, int64_t* info /* [8] */)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    info[0] = c->nnz;
+    info[1] = c->n_items;
+    info[2] = c->NV;
+    info[3] = (int64_t)c->sv_smem;
+    info[4] = c->sv_grid;
+    info[5] = c->num_sms;
+    info[6] = c->passes;
+    info[7] = c->S;
+    API_END
+}
+
+int mace_set_agent_params(void* p, int local, double beta_eff, double inv_sigma2, int clamp)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    int a0 = local < 0 ? 0 : local, a1 = local < 0 ? c->n_local : local + 1;
+    for (int a = a0; a < a1; ++a) {
+        c->am[a]->beta_eff = (float)beta_eff;
+        c->am[a]->inv_s2 = (float)inv_sigma2;
+        c->am[a]->clamp = clamp;
+        c->h_agents[a].beta_eff = (float)beta_eff;
+        c->h_agents[a].inv_s2 = (float)inv_sigma2;
+        c->h_agents[a].clamp = clamp;
+    }
+    CK(cudaMemcpyAsync(c->d_agents.p, c->h_agents.data(), sizeof(AgentDev) * c->n_local, cudaMemcpyHostToDevice,
+                       c->stream));
+    sync(c);
+    API_END
+}
+
+int mace_load_data(void* p, const float* y, const float* lam)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    const size_t rows = (size_t)c->n_views * c->n_ch;
+    CK(cudaMemcpyAsync(c->y.p, y, sizeof(float) * rows, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->lam.p, lam, sizeof(float) * rows, cudaMemcpyHostToDevice, c->stream));
+    if (c->n_local) {
+        k_gather_data<<<c->num_sms * 4, 256, 0, c->stream>>>(c->d_agents.p, c->row_base.p, c->n_local, c->total_rows,
+                                                              c->n_ch, c->y.p, c->lam.p);
+        CK(cudaGetLastError());
+        compute_theta2(c);
+    }
+    API_END
+}
+
+int mace_set_state(void* p, int local, const float* x)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    int a0 = local < 0 ? 0 : local, na = local < 0 ? c->n_local : 1;
+    for (int a = a0; a < a0 + na; ++a)
+        CK(cudaMemcpyAsync(c->h_agents[a].z, x, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->done.p, 0, 2 * sizeof(int), c->stream));
+    refresh(c, a0, na);
+    sync(c);
+    API_END
+}
+
+int mace_get_state(void* p, int local, float* x)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    CK(cudaMemcpyAsync(x, c->h_agents.at(local).z, sizeof(float) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    API_END
+}
+
+int mace_get_error(void* p, int local, float* e)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    const AgentDev& A = c->h_agents.at(local);
+    CK(cudaMemcpy2DAsync(e, sizeof(float), A.el, sizeof(float2), sizeof(float), A.R, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    API_END
+}
+
+int mace_get_theta2(void* p, int local, float* th)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    CK(cudaMemcpyAsync(th, c->h_agents.at(local).th, sizeof(float) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    API_END
+}
+
+int mace_refresh(void* p, int local)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    CK(cudaMemsetAsync(c->done.p, 0, 2 * sizeof(int), c->stream));
+    if (local < 0) refresh(c, 0, c->n_local);
+    else refresh(c, local, 1);
+    sync(c);
+    API_END
+}
+
+// Plain partial-update passes toward an explicit target v (icd.py:272-283); dsq[k] = sum alpha^2 of pass k.
+int mace_pass(void* p, int local, const float* v, int n_passes, int64_t s_begin, int64_t s_end, double* dsq)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (local < 0 || local >= c->n_local) throw std::runtime_error("bad agent");
+    CK(cudaMemcpyAsync(c->h_agents[local].vt, v, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->done.p, 0, 2 * sizeof(int), c->stream));
+    std::vector<double> part;
+    for (int k = 0; k < n_passes; ++k) {
+        run_pass(c, 0, 0.f, nullptr, local, 1, s_begin, s_end);
+        if (dsq) {
+            const int items = c->schedule == 1 ? 1 : c->am[local]->n_sv;
+            part.resize((size_t)items * 4);
+            CK(cudaMemcpyAsync(part.data(), c->part.p, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, c->stream));
+            sync(c);
+            double s = 0;
+            for (int i = 0; i < items; ++i) s += part[(size_t)i * 4];
+            dsq[k] = s;
+        }
+    }
+    sync(c);
+    API_END
+}
+
+// Forward projection of an image: out (n_views x n_ch) = A x  (geometry.py:261-270)
+int mace_forward_project(void* p, const float* x, float* out)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    const int rows = c->n_views * c->n_ch;
+    DBuf<float> dx, dout;
+    dx.alloc(c->n);
+    dout.alloc(rows);
+    CK(cudaMemcpyAsync(dx.p, x, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream));
+    FPParams F{c->rp.p, c->cols.p, c->vals.p, c->n_ch};
+    k_fp_rows<<<std::max(1, std::min(c->num_sms * 16, (rows + 7) / 8)), 256, 0, c->stream>>>(F, rows, dx.p, dout.p,
+                                                                                             nullptr, nullptr, nullptr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, dout.p, sizeof(float) * rows, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    API_END
+}
+
+// f(x) = 1/2 sum lambda (y - Ax)^2 + beta h(x)  (models.py:235-278), fp64 accumulation
+int mace_cost(void* p, const float* x, double beta, double* like, double* prior)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    const int rows = c->n_views * c->n_ch;
+    DBuf<float> dx;
+    dx.alloc(c->n);
+    CK(cudaMemcpyAsync(dx.p, x, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream));
+    const int b1 = std::max(1, std::min(c->num_sms * 8, (rows + 7) / 8)), b2 = c->num_sms * 2;
+    DBuf<double> pp;
+    pp.alloc(b1 + b2);
+    FPParams F{c->rp.p, c->cols.p, c->vals.p, c->n_ch};
+    k_fp_rows<<<b1, 256, 0, c->stream>>>(F, rows, dx.p, nullptr, c->y.p, c->lam.p, pp.p);
+    k_prior_cost<<<b2, 1024, 0, c->stream>>>(dx.p, c->n_side, c->prior, pp.p + b1);
+    CK(cudaGetLastError());
+    std::vector<double> h(b1 + b2);
+    CK(cudaMemcpyAsync(h.data(), pp.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    double L = 0, P = 0;
+    for (int i = 0; i < b1; ++i) L += h[i];
+    for (int i = 0; i < b2; ++i) P += h[b1 + i];
+    *like = L;
+    *prior = beta * P;
+    API_END
+}
+
+// ------------------------------------------------------------------ MACE outer loop (mace.py:276-365)
+int mace_stack_init(void* p, const float* w0, int n_total)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (w0) CK(cudaMemcpyAsync(c->W.p, w0, sizeof(float) * c->n * c->n_local, cudaMemcpyHostToDevice, c->stream));
+    else CK(cudaMemsetAsync(c->W.p, 0, sizeof(float) * c->n * c->n_local, c->stream));
+    CK(cudaMemsetAsync(c->done.p, 0, 2 * sizeof(int), c->stream));
+    c->passes = 0;
+    if (n_total > 0) consensus(c, (float)n_total, c->wbar.p, false);  // single rank: wbar = average(w)
+    sync(c);
+    API_END
+}
+
+int mace_set_ref(void* p, const float* ref)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (!ref) {
+        c->ref_norm2 = 0.0;
+        return 0;
+    }
+    double s = 0;
+    for (size_t i = 0; i < c->n; ++i) s += (double)ref[i] * ref[i];
+    c->ref_norm2 = s;
+    CK(cudaMemcpyAsync(c->ref.p, ref, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream));
+    sync(c);
+    API_END
+}
+
+// which: 0 -> wbar, 1 -> g (denoised average); X_i = image for all local agents, then e refreshed
+int mace_states_from(void* p, int which)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    k_broadcast_state<<<c->num_sms * 4, 256, 0, c->stream>>>(c->d_agents.p, c->n_local, which ? c->g.p : c->wbar.p, c->n);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(c->done.p, 0, 2 * sizeof(int), c->stream));
+    refresh(c, 0, c->n_local);
+    sync(c);
+    API_END
+}
+
+int mace_get_image(void* p, int which, float* out)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    CK(cudaMemcpyAsync(out, which ? c->g.p : c->wbar.p, sizeof(float) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    API_END
+}
+
+int mace_set_image(void* p, int which, const float* img)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    CK(cudaMemcpyAsync(which ? c->g.p : c->wbar.p, img, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream));
+    sync(c);
+    API_END
+}
+
+int mace_get_stack(void* p, float* w)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    CK(cudaMemcpyAsync(w, c->W.p, sizeof(float) * c->n * c->n_local, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    API_END
+}
+
+// Single-rank device loop: iters x [K2 pass of all agents -> K4 average/norms -> stop test];
+// use_g: v = 2 g - w with g set by the caller (PnP), else v = 2 wbar - w.  No host sync inside.
+int mace_iterate(void* p, int iters, int iter0, double rho, int use_g, double tol, int n_total, int with_ref,
+                 float* ms_out)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    ensure_log(c, iter0 + iters);
+    CK(cudaEventRecord(c->ev0, c->stream));
+    for (int k = 0; k < iters; ++k) {
+        run_pass(c, 1, (float)rho, use_g ? c->g.p : c->wbar.p, 0, c->n_local);
+        c->passes++;
+        consensus(c, (float)n_total, c->wbar.p, with_ref && !use_g);
+        k_norms<<<1, 256, 0, c->stream>>>(c->part.p, c->n_items, with_ref && !use_g ? c->refpart.p : nullptr,
+                                          kRefBlocks, c->sums5.p, c->done.p);
+        k_finish<<<1, 1, 0, c->stream>>>(c->sums5.p, with_ref && !use_g ? c->ref_norm2 : 0.0, tol, iter0 + k,
+                                         c->log.p, c->done.p, c->head.p);
+        if (c->passes % 50 == 0) refresh(c, 0, c->n_local);  // icd.py:29,280-282
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(c->ev1, c->stream));
+    if (ms_out) {
+        CK(cudaEventSynchronize(c->ev1));
+        CK(cudaEventElapsedTime(ms_out, c->ev0, c->ev1));
+    }
+    API_END
+}
+
+// Multi-rank phase 1: K2 for the local agents, then the local tree sum (into wsum) and the
+// norm partial sums (into sums5).  The caller all-reduces both, then calls mace_iterate_finish.
+int mace_iterate_local(void* p, double rho, int use_g)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    run_pass(c, 1, (float)rho, use_g ? c->g.p : c->wbar.p, 0, c->n_local);
+    c->passes++;
+    consensus(c, 1.0f, c->wsum.p, false);
+    k_norms<<<1, 256, 0, c->stream>>>(c->part.p, c->n_items, nullptr, 0, c->sums5.p, c->done.p);
+    CK(cudaGetLastError());
+    API_END
+}
+
+int mace_comm_buffers(void* p, void** wsum, void** sums5)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    *wsum = c->wsum.p;
+    *sums5 = c->sums5.p;
+    API_END
+}
+
+int mace_local_sum(void* p)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    consensus(c, 1.0f, c->wsum.p, false);
+    API_END
+}
+
+int mace_mean_from_sum(void* p, int n_total)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    // wbar = wsum / N: a one-agent "tree" over the reduced sum
+    k_consensus<<<kRefBlocks, 256, 0, c->stream>>>(c->wsum.p, 1, c->n, (float)n_total, c->wbar.p, nullptr, nullptr,
+                                                   nullptr);
+    CK(cudaGetLastError());
+    API_END
+}
+
+int mace_iterate_finish(void* p, int n_total, double tol, int iter)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    ensure_log(c, iter + 1);
+    k_consensus<<<kRefBlocks, 256, 0, c->stream>>>(c->wsum.p, 1, c->n, (float)n_total, c->wbar.p, nullptr, nullptr,
+                                                   c->done.p);
+    k_finish<<<1, 1, 0, c->stream>>>(c->sums5.p, 0.0, tol, iter, c->log.p, c->done.p, c->head.p);
+    if (c->passes % 50 == 0) refresh(c, 0, c->n_local);
+    CK(cudaGetLastError());
+    API_END
+}
+
+int mace_read_log(void* p, int n, double* log, int* done2)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (n > 0) CK(cudaMemcpyAsync(log, c->log.p, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(done2, c->done.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    API_END
+}
+
+// ------------------------------------------------------------------ host-only layout probes (no GPU needed)
+// Stacked agent CSC (icd.py:185-192).  col_ptr[n+1] always written; rows/vals if non-null.
+int mace_agent_csc(int n_side, int n_ch, int n_views, const int64_t* row_ptr, const int32_t* cols, const float* vals,
+                   int n_agent_views, const int* views, int64_t* col_ptr, uint32_t* rows, float* out_vals)
+{
+    API_BEGIN
+    std::vector<int> vv(views, views + n_agent_views);
+    for (int v : vv)
+        if (v < 0 || v >= n_views) throw std::runtime_error("view index out of range");
+    AgentCSC csc;
+    build_agent_csc(n_side, n_ch, row_ptr, cols, vals, vv, csc);
+    std::memcpy(col_ptr, csc.col_ptr.data(), sizeof(int64_t) * csc.col_ptr.size());
+    if (rows) std::memcpy(rows, csc.row.data(), sizeof(uint32_t) * csc.row.size());
+    if (out_vals) std::memcpy(out_vals, csc.val.data(), sizeof(float) * csc.val.size());
+    API_END
+}
+
+// Super-voxel layout decoded back to (pixel, local row, value) per stored entry (pads skipped).
+// stats: [entries, max_band, max_col, n_sv, duplicates, decoded]; decoded arrays may be null.
+int mace_sv_layout_probe(int n_side, int n_ch, int n_views, const int64_t* row_ptr, const int32_t* cols,
+                         const float* vals, int n_agent_views, const int* views, int svs, int64_t* stats,
+                         int32_t* pix_out, int32_t* row_out, float* val_out)
+{
+    API_BEGIN
+    std::vector<int> vv(views, views + n_agent_views);
+    for (int v : vv)
+        if (v < 0 || v >= n_views) throw std::runtime_error("view index out of range");
+    AgentCSC csc;
+    build_agent_csc(n_side, n_ch, row_ptr, cols, vals, vv, csc);
+    SVLayout L;
+    build_sv_layout(csc, n_side, n_ch, n_agent_views, svs, L);
+    int64_t k = 0;
+    const int S = L.svs;
+    for (int sv = 0; sv < L.n_sv; ++sv) {
+        const int r0 = (sv / L.n_sv_side) * S, c0 = (sv % L.n_sv_side) * S;
+        const int2_t* bt = &L.band[(size_t)sv * L.views];
+        for (int q = 0; q < S * S; ++q) {
+            const int2_t pe = L.pix[(size_t)sv * S * S + q];
+            for (int e = 0; e < pe.y; ++e) {
+                const int li = L.idx[pe.x + e];
+                int j = 0;
+                while (!(bt[j].y & 0xffff) || li >= (bt[j].y >> 16) + (bt[j].y & 0xffff) || li < (bt[j].y >> 16)) ++j;
+                if (pix_out) {
+                    pix_out[k] = (r0 + q / S) * n_side + (c0 + q % S);
+                    row_out[k] = bt[j].x + (li - (bt[j].y >> 16));
+                    val_out[k] = L.val[pe.x + e];
+                }
+                ++k;
+            }
+        }
+    }
+    stats[0] = (int64_t)L.val.size();
+    stats[1] = L.max_band;
+    stats[2] = L.max_col;
+    stats[3] = L.n_sv;
+    stats[4] = L.duplicates;
+    stats[5] = k;
+    API_END
+}
+
+// pinned host memory for the end-to-end path
+int mace_host_alloc(size_t bytes, void** out)
+{
+    API_BEGIN
+    CK(cudaHostAlloc(out, bytes, cudaHostAllocDefault));
+    API_END
+}
+void mace_host_free(void* ptr)
+{
+    if (ptr) cudaFreeHost(ptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+"""Seeded synthetic workload for the benchmark configurations (BASELINE.json:configs).
+
+The reference ships only fixed phantoms and a Gaussian noise model
+(/root/reference/pkg/src/macetomo/sim.py:58-120); BASELINE asks for seeded
+random ellipses and Poisson counts, so this module defines that recipe.  The
+same arrays feed the CPU oracle and the GPU path (decisions recorded in
+DESIGN.md §3):
+
+* field of view fixed at 128 mm; pixel pitch = channel pitch = 128 / n_side mm;
+* phantom = 0.02 mm^-1 disk (radius 0.9 x half-FOV) + K ellipses with values
+  U[0.005, 0.05] mm^-1 painted in draw order, 2x2 supersampled;
+* counts ~ Poisson(I0 exp(-A x)) clamped >= 1; y = -log(counts / I0); lambda = counts.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+FOV_MM = 128.0
+
+# BASELINE.json:configs -> (n_side, n_views, n_channels, n_agents, iterations, I0, n_ellipses, slices)
+CONFIGS = {
+    0: dict(n_side=128, n_views=180, n_channels=185, n_agents=4, iters=30, I0=1e4, n_ellipses=10, slices=1),
+    1: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=40, I0=1e4, n_ellipses=10, slices=1),
+    2: dict(n_side=1024, n_views=1440, n_channels=1450, n_agents=16, iters=50, I0=5e3, n_ellipses=40, slices=1),
+    3: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=40, I0=1e4, n_ellipses=10, slices=1),
+    4: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=30, I0=1e4, n_ellipses=10, slices=64),
+}
+
+
+def pitch_for(n_side: int, config: int | None = None) -> float:
+    """Pixel = channel pitch.  Config 0 is 1 mm by BASELINE; the rest keep the 128 mm FOV."""
+    return FOV_MM / n_side
+
+
+def ellipse_phantom(n_side: int, pitch: float, n_ellipses: int = 10, seed: int = 0,
+                    disk_value: float = 0.02, value_range=(0.005, 0.05)) -> np.ndarray:
+    """Flat (n_side*n_side,) float64 attenuation image in mm^-1, row 0 at the top."""
+    rng = np.random.default_rng(seed)
+    half = 0.5 * n_side * pitch
+    R = 0.9 * half
+    # 2x2 supersampled pixel sample points
+    sub = (np.arange(2 * n_side) + 0.5) * (pitch / 2.0)
+    xs = sub - half
+    ys = half - sub
+    X, Y = np.meshgrid(xs, ys)
+    img = np.where(X * X + Y * Y <= R * R, disk_value, 0.0)
+    for _ in range(n_ellipses):
+        r = 0.6 * R * np.sqrt(rng.random())
+        phi = 2.0 * np.pi * rng.random()
+        cx, cy = r * np.cos(phi), r * np.sin(phi)
+        a = R * rng.uniform(0.05, 0.25)
+        b = R * rng.uniform(0.05, 0.25)
+        ang = np.pi * rng.random()
+        val = rng.uniform(*value_range)
+        c, s = np.cos(ang), np.sin(ang)
+        dx, dy = X - cx, Y - cy
+        u = (c * dx + s * dy) / a
+        v = (-s * dx + c * dy) / b
+        img = np.where(u * u + v * v <= 1.0, val, img)
+    img = img.reshape(n_side, 2, n_side, 2).mean(axis=(1, 3))
+    return np.ascontiguousarray(img.ravel())
+
+
+def poisson_sinogram(proj: np.ndarray, I0: float, seed: int = 1):
+    """counts ~ Poisson(I0 exp(-proj)), clamped >= 1; returns (y, weights=counts)."""
+    rng = np.random.default_rng(seed)
+    counts = rng.poisson(I0 * np.exp(-np.asarray(proj, np.float64))).astype(np.float64)
+    np.maximum(counts, 1.0, out=counts)
+    y = -np.log(counts / I0)
+    return y, counts

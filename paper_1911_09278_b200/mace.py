@@ -1,0 +1,475 @@
+"""Consensus-equilibrium outer loop on the GPU (mirrors /root/reference/pkg/src/macetomo/mace.py).
+
+``mace_solve`` / ``mace_pnp_solve`` keep the reference signatures, config
+validation, error behaviour and result types.  One MACE iteration
+
+    v = (2G - I) w ;  X_i <- one ICD pass toward prox_{f_i}(v_i) ;  w <- rho (2X - v) + (1 - rho) w
+
+runs as kernel K2 (all local agents at once, v and the Mann step fused in)
+followed by K4 (fixed-order average + norms + stop test), with no host
+synchronisation between iterations.  With several ranks (one process per
+GPU, ``torch.distributed``), agent i lives on rank i mod world and the only
+exchange per iteration is one all-reduce of the local stack sum (+4 scalars).
+
+The small stacked-state helpers (``average``, ``reflect_G``, ``mann_step`` ...)
+are the reference's host algebra, kept for API compatibility; the solver
+never calls them.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .denoisers import DenoiserSpec, make_denoiser
+from .engine import DEFAULT_COLOURS, DEFAULT_SV, plan_for
+from .geometry import partition_views
+from .icd import AgentWorkspace, ConvergenceError, prox_solve
+
+__all__ = ["MaceConfig", "MaceResult", "ConvergenceLog", "ResidualReport", "WorkerPool", "new_stack", "average",
+           "consensus_G", "reflect_G", "consensus_GH", "mann_step", "mace_solve", "mace_pnp_solve",
+           "equilibrium_residuals", "EquitCounter", "nrmse"]
+
+CONVENTIONAL = "conventional"
+PNP = "pnp"
+
+
+# --------------------------------------------------------------------------- host algebra (mace.py:57-117)
+
+def new_stack(n_subsets: int, n: int) -> np.ndarray:
+    if n_subsets < 1 or n < 1:
+        raise ValueError("stack dimensions must be >= 1")
+    return np.zeros((n_subsets, n))
+
+
+def _check_stack(stack) -> np.ndarray:
+    stack = np.asarray(stack, dtype=np.float64)
+    if stack.ndim != 2 or stack.shape[0] < 1:
+        raise ValueError("a stacked state must be a (N, n) array with N >= 1")
+    return stack
+
+
+def average(stack) -> np.ndarray:
+    """Balanced pairwise-tree mean in fixed order (the order K4 uses on the device)."""
+    stack = _check_stack(stack)
+    acc = stack.copy()
+    m = acc.shape[0]
+    while m > 1:
+        half = m // 2
+        acc[:half] += acc[half:2 * half]
+        if m % 2:
+            acc[half] = acc[2 * half]
+            m = half + 1
+        else:
+            m = half
+    return acc[0] / stack.shape[0]
+
+
+def consensus_G(stack) -> np.ndarray:
+    stack = _check_stack(stack)
+    return np.broadcast_to(average(stack), stack.shape).copy()
+
+
+def reflect_G(stack) -> np.ndarray:
+    stack = _check_stack(stack)
+    return 2.0 * average(stack)[None, :] - stack
+
+
+def consensus_GH(stack, denoiser) -> np.ndarray:
+    stack = _check_stack(stack)
+    return np.broadcast_to(denoiser(average(stack)), stack.shape).copy()
+
+
+def mann_step(w, Tw, rho: float) -> np.ndarray:
+    w = np.asarray(w, dtype=np.float64)
+    Tw = np.asarray(Tw, dtype=np.float64)
+    if w.shape != Tw.shape:
+        raise ValueError("w and Tw must have identical shapes")
+    return rho * Tw + (1.0 - rho) * w
+
+
+def nrmse(x, x_ref) -> float:
+    """||x - x_ref|| / ||x_ref|| (oracle.py:341-351 of the reference)."""
+    x = np.asarray(x, dtype=np.float64)
+    x_ref = np.asarray(x_ref, dtype=np.float64)
+    if x.shape != x_ref.shape:
+        raise ValueError("shapes must match")
+    scale = float(np.linalg.norm(x_ref))
+    if scale == 0.0:
+        raise ValueError("reference norm is zero")
+    return float(np.linalg.norm(x - x_ref)) / scale
+
+
+@dataclass
+class EquitCounter:
+    """One equit = one pass over the ROI by every one of the N agents (oracle.py:354-374)."""
+
+    roi_voxels: int
+    n_subsets: int
+    updates: int = 0
+
+    def __post_init__(self):
+        if self.roi_voxels <= 0:
+            raise ValueError("roi_voxels must be > 0")
+        if self.n_subsets < 1:
+            raise ValueError("n_subsets must be >= 1")
+
+    def add_updates(self, count: int) -> None:
+        if count < 0:
+            raise ValueError("update count must be nonnegative")
+        self.updates += count
+
+    def equits(self) -> float:
+        return self.updates / (self.roi_voxels * self.n_subsets)
+
+
+# --------------------------------------------------------------------------- config / bookkeeping
+
+@dataclass(frozen=True)
+class MaceConfig:
+    """Outer-loop configuration (mace.py:124-163) plus the GPU schedule knobs:
+    ``schedule`` "sv" (parallel super-voxel passes) or "raster" (reference order),
+    ``sv_side`` / ``colours`` (tile side and colour-class stride of the SV queue)."""
+
+    n_subsets: int
+    rho: float = 0.8
+    sigma: float = 1.0
+    mode: str = CONVENTIONAL
+    beta: float | None = None
+    denoiser: DenoiserSpec | None = None
+    max_outer: int = 1000
+    tol: float = 1e-7
+    equit_accounting: bool = True
+    residuals: str = "final"
+    clamp_nonneg: bool = False
+    schedule: str = "sv"
+    sv_side: int = DEFAULT_SV
+    colours: int = DEFAULT_COLOURS
+    device: int = 0
+
+    def __post_init__(self):
+        if self.n_subsets < 1:
+            raise ValueError("n_subsets must be >= 1")
+        if not 0.0 < self.rho < 1.0:
+            raise ValueError("rho must lie in (0, 1)")
+        if self.sigma <= 0.0:
+            raise ValueError("sigma must be > 0")
+        if self.mode not in (CONVENTIONAL, PNP):
+            raise ValueError(f"mode must be '{CONVENTIONAL}' or '{PNP}'")
+        if self.mode == PNP and self.denoiser is None:
+            raise ValueError("pnp mode requires a denoiser spec")
+        if self.max_outer < 1:
+            raise ValueError("max_outer must be >= 1")
+        if self.tol <= 0.0:
+            raise ValueError("tol must be > 0")
+        if self.residuals not in ("final", "none"):
+            raise ValueError("residuals must be 'final' or 'none'")
+        if self.schedule not in ("sv", "raster"):
+            raise ValueError("schedule must be 'sv' or 'raster'")
+
+
+class ConvergenceLog:
+    """Per-iteration rows, CSV-serialisable (mace.py:166-201)."""
+
+    COLUMNS = ("iter", "equits", "mann_update_relnorm", "r_F", "r_u", "nrmse_vs_ref", "wall_seconds")
+
+    def __init__(self, pnp: bool = False):
+        self.pnp = pnp
+        self.rows: list[dict] = []
+
+    def append(self, **kw) -> None:
+        self.rows.append(kw)
+
+    def header(self) -> tuple:
+        cols = list(self.COLUMNS)
+        if self.pnp:
+            cols[4] = "r_H"
+        return tuple(cols)
+
+    def write_csv(self, path) -> None:
+        import csv
+
+        def fmt(v):
+            return "" if v is None else repr(float(v))
+
+        with open(path, "w", newline="") as fh:
+            wr = csv.writer(fh)
+            wr.writerow(self.header())
+            for r in self.rows:
+                wr.writerow([r.get("iter"), fmt(r.get("equits")), fmt(r.get("relnorm")), fmt(r.get("r_F")),
+                             fmt(r.get("r_u")), fmt(r.get("nrmse")), fmt(r.get("wall"))])
+
+
+@dataclass
+class ResidualReport:
+    mode: str
+    r_F: float
+    r_u: float
+    per_agent: list = field(default_factory=list)
+
+
+@dataclass
+class MaceResult:
+    image: np.ndarray
+    stack: np.ndarray
+    log: ConvergenceLog
+    iterations: int
+    converged: bool
+    equits: float | None = None
+    residuals: ResidualReport | None = None
+    device_ms: float | None = None  # device time of the iteration loop (CUDA events)
+
+
+class WorkerPool:
+    """Accepted for API compatibility (mace.py:229-254).  On the GPU every local
+    agent runs concurrently inside one kernel, so the worker count is unused and
+    results never depend on it."""
+
+    def __init__(self, workers: int | None = None):
+        self.workers = workers
+
+    def map(self, fn, items):
+        return [fn(i) for i in items]
+
+    def close(self) -> None:
+        pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+# --------------------------------------------------------------------------- distributed plumbing
+
+class _Comm:
+    """Rank layout + all-reduce of the per-iteration consensus buffers (torch.distributed)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def allreduce(self, *tensors):
+        for t in tensors:
+            self.dist.all_reduce(t, group=self.group)
+
+    def allgather_stack(self, local_rows: dict, N: int, n: int) -> np.ndarray:
+        objs = [None] * self.world
+        self.dist.all_gather_object(objs, local_rows, group=self.group)
+        out = np.zeros((N, n))
+        for d in objs:
+            for i, row in d.items():
+                out[i] = row
+        return out
+
+
+def _resolve_comm(comm):
+    if comm is None or comm is False:
+        return None
+    if comm is True:
+        import torch.distributed as dist
+
+        if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+            return None
+        return _Comm()
+    return comm
+
+
+# --------------------------------------------------------------------------- the driver (mace.py:276-365)
+
+def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=None, backend=None):
+    n = problem.geom.n_pixels
+    N = config.n_subsets
+    subsets = partition_views(problem.geom.n_views, N)
+    comm = _resolve_comm(comm)
+    rank, world = (comm.rank, comm.world) if comm else (0, 1)
+    local = [i for i in range(N) if i % world == rank]
+    pnp = denoiser is not None
+    if pnp:
+        sigma, beta = np.sqrt(N) * config.sigma, 0.0  # mace.py:263-265
+    else:
+        sigma = config.sigma
+        beta = problem.prior.beta if config.beta is None else config.beta
+    views = [subsets[i].view_indices for i in local]
+    if backend is None:
+        plan = plan_for(problem.matrices, views, schedule=config.schedule, sv=config.sv_side,
+                        colours=config.colours, device=config.device)
+    else:
+        plan = backend(problem, views)
+    plan.load_data(problem.y, problem.weights)
+    plan.set_prior(problem.prior)
+    plan.set_agent_params(-1, beta / N, 1.0 / (sigma * sigma), config.clamp_nonneg)
+
+    if w0 is not None:
+        w0 = _check_stack(w0)
+        if w0.shape != (N, n):
+            raise ValueError(f"w0 must have shape ({N}, {n})")
+        w_local = np.ascontiguousarray(w0[local], np.float32)
+    else:
+        w_local = None
+    if comm is None:
+        plan.stack_init(w_local, N)
+    else:
+        plan.stack_init(w_local, 0)
+        plan.local_sum()
+        comm.allreduce(*plan.comm_arrays()[:1])
+        plan.mean_from_sum(N)
+    device_g = pnp and getattr(denoiser, "device_apply", None) is not None
+    if pnp:
+        _apply_denoiser(plan, denoiser)
+        plan.states_from(1)  # X0 = H(average(w0)), mace.py:286
+    else:
+        plan.states_from(0)  # X0 = average(w0)
+    ref32 = None if ref_image is None else np.ascontiguousarray(ref_image, np.float32)
+    ref_norm = None if ref_image is None else float(np.linalg.norm(np.asarray(ref_image, np.float64)))
+    if ref_image is not None and ref_norm == 0.0:
+        raise ValueError("reference norm is zero")
+    plan.set_ref(ref32 if (not pnp and comm is None) else None)
+
+    log = ConvergenceLog(pnp=pnp)
+    counter = EquitCounter(n, N) if config.equit_accounting else None
+    t0 = time.perf_counter()
+    device_ms = 0.0
+    rows = []  # (relnorm, nrmse, wall)
+    done = (0, 0)
+    it = 0
+    host_loop = comm is not None or (pnp and not device_g)
+    if not host_loop:
+        chunk = config.max_outer
+        while it < config.max_outer and done[0] == 0:
+            k = min(chunk, config.max_outer - it)
+            if pnp:  # device denoiser: one iteration per call, H applied on the device in between
+                k = 1
+            ms = plan.iterate(k, it, config.rho, pnp, config.tol, N, ref32 is not None)
+            device_ms += ms
+            if pnp:
+                _apply_denoiser(plan, denoiser)
+            it += k
+            lg, done = plan.read_log(it)
+            wall = time.perf_counter() - t0
+            lim = it if done[0] == 0 else (done[1] if done[0] == 1 else done[1] - 1)
+            for j in range(len(rows), lim):
+                nr = None
+                if ref_image is not None:
+                    nr = lg[j, 3] if not pnp else nrmse(plan.get_image(1), ref_image)
+                rows.append((lg[j, 0], nr, wall * (j + 1) / it))
+    else:
+        for k in range(config.max_outer):
+            plan.iterate_local(config.rho, pnp)
+            if comm is not None:
+                comm.allreduce(*plan.comm_arrays())
+            plan.iterate_finish(N, config.tol, k)
+            if pnp:
+                _apply_denoiser(plan, denoiser)
+            lg, done = plan.read_log(k + 1)
+            it = k + 1
+            est = None
+            if ref_image is not None:
+                est = nrmse(plan.get_image(1 if pnp else 0), ref_image)
+            if done[0] == 2:
+                break
+            rows.append((lg[k, 0], est, time.perf_counter() - t0))
+            if done[0] == 1:
+                break
+    if done[0] == 2:
+        raise ConvergenceError(
+            f"MACE diverged at iteration {done[1]}: the partial-update map is expansive for this sigma "
+            "(reduce sigma)", last_iterate=None, log=_fill_log(log, rows, counter, N, n))
+    iterations = len(rows)
+    converged = done[0] == 1
+    _fill_log(log, rows, counter, N, n)
+    image = plan.get_image(1 if pnp else 0).astype(np.float64)
+    w_loc = plan.get_stack().reshape(len(local), n).astype(np.float64)
+    if comm is None:
+        stack = w_loc
+    else:
+        stack = comm.allgather_stack({i: w_loc[j] for j, i in enumerate(local)}, N, n)
+    result = MaceResult(image=image, stack=stack, log=log, iterations=iterations, converged=converged,
+                        equits=None if counter is None else counter.equits(), device_ms=device_ms)
+    if config.residuals == "final":
+        result.residuals = equilibrium_residuals(problem, config, stack, denoiser=denoiser)
+        if log.rows:
+            log.rows[-1]["r_F"] = result.residuals.r_F
+            log.rows[-1]["r_u"] = result.residuals.r_u
+    if not converged:
+        raise ConvergenceError(f"MACE: Mann update relnorm did not reach {config.tol:g} in {config.max_outer} "
+                               "iterations", last_iterate=result, log=log)
+    return result
+
+
+def _fill_log(log, rows, counter, N, n):
+    log.rows.clear()
+    if counter is not None:
+        counter.updates = 0
+    for j, (rel, nr, wall) in enumerate(rows):
+        if counter is not None:
+            counter.add_updates(N * n)
+        log.append(iter=j + 1, equits=None if counter is None else counter.equits(), relnorm=float(rel), r_F=None,
+                   r_u=None, nrmse=None if nr is None else float(nr), wall=wall)
+    return log
+
+
+def _apply_denoiser(plan, denoiser):
+    dev = getattr(denoiser, "device_apply", None)
+    if dev is not None:
+        dev(plan)  # reads wbar, writes g on the device
+        return
+    wbar = plan.get_image(0).astype(np.float64)
+    h = np.asarray(denoiser(wbar), dtype=np.float64)
+    if h.shape != wbar.shape:
+        raise ValueError("denoiser must map a length-n image to a length-n image")
+    plan.set_image(1, h)
+
+
+def mace_solve(problem, config: MaceConfig, pool: WorkerPool | None = None, ref_image=None, w0=None,
+               comm=None) -> MaceResult:
+    """Partial-update MACE with the conventional prior (mace.py:368-382).  Converges to
+    the MAP image of the full-data objective; returns the component average."""
+    if config.mode != CONVENTIONAL:
+        raise ValueError("mace_solve requires mode='conventional'")
+    return _run_outer(problem, config, pool, ref_image, w0, denoiser=None, comm=comm)
+
+
+def mace_pnp_solve(problem, config: MaceConfig, pool: WorkerPool | None = None, ref_image=None, w0=None,
+                   denoiser=None, comm=None) -> MaceResult:
+    """MACE with a PnP denoiser prior (mace.py:385-404): agents carry only data terms at
+    sqrt(N) sigma; H acts once per iteration on the average; returns H(mean w)."""
+    if config.mode != PNP:
+        raise ValueError("mace_pnp_solve requires mode='pnp'")
+    if denoiser is None:
+        denoiser = make_denoiser(config.denoiser, problem.geom.n_side)
+    return _run_outer(problem, config, pool, ref_image, w0, denoiser=denoiser, comm=comm)
+
+
+def equilibrium_residuals(problem, config: MaceConfig, w, prox_tol: float = 1e-9, denoiser=None) -> ResidualReport:
+    """Equilibrium check of a stacked state (mace.py:407-454), proximal maps solved on the GPU."""
+    w = _check_stack(w)
+    subsets = partition_views(problem.geom.n_views, config.n_subsets)
+    w_bar = average(w)
+    if config.mode == PNP:
+        if denoiser is None:
+            denoiser = make_denoiser(config.denoiser, problem.geom.n_side)
+        x_hat = np.asarray(denoiser(w_bar), np.float64)
+        sigma, beta = np.sqrt(config.n_subsets) * config.sigma, 0.0
+        seconds = x_hat - w
+        aux = float(np.linalg.norm(np.asarray(denoiser(x_hat + (w_bar - x_hat))) - x_hat))
+    else:
+        x_hat = w_bar
+        sigma, beta = config.sigma, config.beta
+        seconds = x_hat - w
+        aux = float(np.linalg.norm(seconds.sum(axis=0)))
+    scale = max(float(np.linalg.norm(x_hat)), 1e-300)
+    per_agent = []
+    for i, sub in enumerate(subsets):
+        ws = AgentWorkspace(problem, sub, config.n_subsets, sigma=sigma, beta=beta, state=x_hat,
+                            device=config.device)
+        fi = prox_solve(ws, x_hat + seconds[i], tol=prox_tol)
+        per_agent.append(float(np.linalg.norm(fi - x_hat)) / scale)
+    return ResidualReport(mode=config.mode, r_F=max(per_agent), r_u=aux / scale, per_agent=per_agent)
