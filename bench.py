@@ -1,0 +1,355 @@
+"""Benchmark: MACE voxel-updates/s on BASELINE config 1 (512^2, 720 views x 725 channels,
+N = 8 view-interleaved agents, rho = 0.8, 40 iterations, qGGMRF), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+A step is one full MACE solve of the config's iteration budget on the seeded
+synthetic scan (gen.make_scan).  ``value`` = total voxel updates (N agents x n
+pixels x iterations x steps, all ranks) / max-over-ranks device time, inputs
+resident in HBM.  ``e2e`` = the same metric through the public API
+(mace_solve on host numpy arrays: H2D of y / weights, D2H of image + stack
+inside the timed region).  The per-iteration A stream (1.4 GB) exceeds the
+126 MB L2, so no L2 flush is needed between steps.
+
+``--impl reference`` times the CPU oracle (oracle/, the restatement of the
+reference's numba hot loop, all host threads) on a bounded sample of the same
+workload and prints the same metric with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MACE voxel-updates/s"
+UNIT = "voxel-updates/s"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        self.f.flush()
+        rows = []
+        try:
+            for line in open(self.f.name):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def algorithmic_bytes_per_pass(plan, n_agents_local) -> tuple[int, dict]:
+    """B_upd = 8 c + 16 + 12 R_i / n per voxel update; per K2 launch that is
+    8 nnz (A: f32 value + i32 row) + 16 n N (z r/w, v, theta2) + 12 sum R_i (e r/w, lambda)."""
+    nnz = 0
+    ent = 0
+    R = 0
+    for a in range(n_agents_local):
+        info = plan.agent_info(a)
+        nnz += info["nnz"]
+        ent += info["entries"]
+        R += info["R"]
+    n = plan.n
+    alg = 8 * nnz + 16 * n * n_agents_local + 12 * R
+    layout = 6 * ent + 16 * n * n_agents_local + 12 * R  # bytes the super-voxel layout actually streams
+    return alg, {"nnz": nnz, "layout_entries": ent, "rows": R, "layout_bytes": layout,
+                 "c_mean": nnz / (n * n_agents_local)}
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    import paper_1911_09278_b200 as mb
+    from paper_1911_09278_b200 import gen
+    from paper_1911_09278_b200.engine import plan_for
+
+    cfg = gen.CONFIGS[args.config]
+    N, iters = cfg["n_agents"], args.iters or cfg["iters"]
+    t0 = time.time()
+    geom, mats, phantom, y, lam = gen.make_scan(args.config)
+    t_scan = time.time() - t0
+    prior = mb.PriorParams("qggmrf", beta=cfg["beta"], p=2.0, q=1.2, T=1.0, sigma_x=0.01)
+    prob = mb.ReconProblem(geom, mats, y, lam, prior)
+    mcfg = mb.MaceConfig(n_subsets=N, rho=0.8, sigma=cfg["sigma"], max_outer=iters, tol=1e-300,
+                         residuals="none", schedule=args.schedule, sv_side=args.sv, device=local)
+    comm = True if world > 1 else None
+    subsets = mb.partition_views(geom.n_views, N)
+    local_agents = [i for i in range(N) if i % world == rank]
+    t0 = time.time()
+    plan = plan_for(mats, [subsets[i].view_indices for i in local_agents], schedule=args.schedule, sv=args.sv,
+                    device=local)
+    t_plan = time.time() - t0
+    n = geom.n_pixels
+    stream = torch.cuda.ExternalStream(plan_stream(plan), device=f"cuda:{local}")
+
+    def solve_device():
+        """one step with inputs resident: stack init, X0 = average(w0), refresh e, `iters` iterations"""
+        plan.stack_init(None, N if world == 1 else 0)
+        if world > 1:
+            plan.local_sum()
+            mb.mace._resolve_comm(True).allreduce(*plan.comm_arrays()[:1])
+            plan.mean_from_sum(N)
+        plan.states_from(0)
+        if world == 1:
+            plan.iterate(iters, 0, 0.8, False, 1e-300, N, False)
+        else:
+            c = mb.mace._resolve_comm(True)
+            for k in range(iters):
+                plan.iterate_local(0.8, False)
+                c.allreduce(*plan.comm_arrays())
+                plan.iterate_finish(N, 1e-300, k)
+
+    # resident inputs
+    plan.load_data(y, lam)
+    plan.set_prior(prior)
+    plan.set_agent_params(-1, prior.beta / N, 1.0 / cfg["sigma"] ** 2, False)
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        solve_device()
+    plan.k2_timing(True)
+    barrier()
+    with ClockSampler(local) as clk:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            solve_device()
+        ev1.record(stream)
+        barrier()
+    k2_ms, k2_launches = plan.k2_timing(False)
+    ms = ev0.elapsed_time(ev1)
+    lg, done = plan.read_log(iters)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    updates = N * n * iters * args.steps
+    value = updates / (ms / 1e3)
+
+    # ---- end to end through the public API (host numpy in, host numpy out)
+    for _ in range(1):
+        _solve_api(mb, prob, mcfg, comm)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = _solve_api(mb, prob, mcfg, comm)
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = updates / e2e_s
+    h2d = 2 * geom.n_views * geom.n_channels * 4
+    d2h = (n + N * n) * 4
+
+    alg, lay = algorithmic_bytes_per_pass(plan, len(local_agents))
+    pk = peaks()
+    k2_avg_ms = k2_ms / max(k2_launches, 1)
+    achieved = alg / (k2_avg_ms / 1e3) / 1e9
+    clocks = clk.summary()
+    launches_per_step = 3 + 4 * iters + (iters // 50)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak"
+        if False else "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded ellipse phantom, "
+        "Poisson counts; gen.make_scan)",
+        "config": {"workload": f"BASELINE config {args.config}: {geom.n_side}^2, {geom.n_views} views x "
+                   f"{geom.n_channels} ch, N={N} agents, {iters} iterations, rho=0.8, qGGMRF beta={cfg['beta']}, "
+                   f"sigma={cfg['sigma']}", "schedule": args.schedule, "sv_side": args.sv,
+                   "parallelism": f"agents {N} over {world} GPU(s)", "l2": "inputs > L2 (A stream 1.4 GB/iter)",
+                   "final_relnorm": float(lg[-1, 0]) if len(lg) else None},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "note": "mace_solve() on host float64 y/weights; includes H2D, solve, D2H image+stack"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+                     "frac": achieved / pk.get("hbm_gbs"), "traffic": None, "kernel": "k_icd_sv (K2)",
+                     "bytes_per_launch": alg, "layout_bytes_per_launch": lay["layout_bytes"],
+                     "k2_avg_ms": k2_avg_ms, "k2_share": k2_ms / ms, "c_mean": lay["c_mean"],
+                     "peak_source": "MEASURED_PEAKS.json" if not pk.get("_fallback") else "fallback"},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+        "setup_s": {"scan": t_scan, "plan": t_plan},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args.config, mats, y, lam, sample_iters=args.cpu_iters)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def plan_stream(plan):
+    import ctypes
+
+    s = ctypes.c_void_p()
+    plan.call("mace_ctx_stream", ctypes.byref(s))
+    return s.value
+
+
+def _solve_api(mb, prob, cfg, comm):
+    try:
+        return mb.mace_solve(prob, cfg, comm=comm)
+    except mb.ConvergenceError as err:
+        return err.last_iterate
+
+
+def cpu_baseline(config, mats, y, lam, sample_iters=2, threads=None):
+    """CPU oracle (restated reference hot loop, float64) on a bounded sample: `sample_iters`
+    MACE iterations of the same workload, agents mapped over min(N, cores) threads."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    from paper_1911_09278_b200 import gen
+
+    cfg = gen.CONFIGS[config]
+    N = cfg["n_agents"]
+    cores = os.cpu_count() or 1
+    threads = threads or min(N, cores)
+    ns = int(np.sqrt(mats[0].n_pixels))
+    prior = O.Prior("qggmrf", cfg["beta"], 2.0, 1.2, 1.0, 0.01)
+    agents = O.build_agents(mats, y, lam, N, cfg["sigma"], prior, ns)
+    O.mace_run(agents, 1, 0.8, workers=threads)  # warm-up
+    t0 = time.perf_counter()
+    run = O.mace_run(agents, sample_iters, 0.8, workers=threads)
+    dt = time.perf_counter() - t0
+    n = ns * ns
+    return {"value": N * n * len(run.relnorms) / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{sample_iters} MACE iterations of config {config} (N={N} agents, {n} px), "
+                      f"oracle/sweep.c float64 raster ICD, {threads} threads; host has {cores} cores",
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1911_09278_b200 import gen
+
+    cfg = gen.CONFIGS[args.config]
+    geom, mats, phantom, y, lam = gen.make_scan(args.config)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    N = cfg["n_agents"]
+    cores = os.cpu_count() or 1
+    threads = min(N, cores)
+    prior = O.Prior("qggmrf", cfg["beta"], 2.0, 1.2, 1.0, 0.01)
+    agents = O.build_agents(mats, y, lam, N, cfg["sigma"], prior, geom.n_side)
+    per_step = max(1, args.cpu_iters)
+    for _ in range(args.warmup):
+        O.mace_run(agents, 1, 0.8, workers=threads)
+    t0 = time.perf_counter()
+    done = 0
+    for _ in range(args.steps):
+        run = O.mace_run(agents, per_step, 0.8, workers=threads)
+        done += len(run.relnorms)
+    dt = time.perf_counter() - t0
+    n = geom.n_pixels
+    value = N * n * done / dt
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen.make_scan)",
+            "impl": "reference",
+            "config": {"workload": f"BASELINE config {args.config}: {geom.n_side}^2, {geom.n_views} views x "
+                       f"{geom.n_channels} ch, N={N} agents; each step = {per_step} MACE iteration(s) (bounded "
+                       "sample of the 40-iteration solve)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{per_step} MACE iteration(s) per step, oracle/sweep.c float64, "
+                                       f"{threads} threads of {cores}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--iters", type=int, default=0)
+    ap.add_argument("--schedule", default="sv", choices=["sv", "raster"])
+    ap.add_argument("--sv", type=int, default=8)
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

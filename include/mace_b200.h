@@ -72,6 +72,9 @@ int mace_set_prior(void* ctx, int kind, double p, double q, double T, double sig
 /* n_local agents, agent a owns views[sum(view_counts[:a]) ...]; schedule 0 = super-voxel, 1 = raster */
 int mace_setup_agents(void* ctx, int n_local, const int* view_counts, const int* views, int schedule, int sv_side,
                       int colours, int n_threads);
+/* super-voxel schedule: at most `concurrency` x (tiles in the pass) tiles in flight (>= 1 per agent);
+ * max_warps > 0 caps the number of resident warps */
+int mace_set_schedule(void* ctx, double concurrency, int64_t max_warps);
 /* local < 0: every local agent */
 int mace_set_agent_params(void* ctx, int local, double beta_eff, double inv_sigma2, int clamp);
 /* global sinogram y and weights, n_views x n_ch float32; recomputes theta2 */
@@ -103,6 +106,8 @@ int mace_local_sum(void* ctx);
 int mace_mean_from_sum(void* ctx, int n_total);
 int mace_iterate_finish(void* ctx, int n_total, double tol, int iter);
 int mace_read_log(void* ctx, int n, double* log, int* done2);
+/* per-launch CUDA-event timing of K2 on the context stream (enable=1 start, 0 stop + read) */
+int mace_k2_timing(void* ctx, int enable, double* total_ms, int64_t* launches);
 
 /* ---- host-only layout probes (no device needed; used by the CPU test suite).
  * mace_agent_csc: the stacked agent CSC of icd.py:185-192; col_ptr[n+1] always, rows/vals if non-null.

@@ -38,6 +38,7 @@ _SIGS = {
     "mace_load_matrix": (c_int, [P, c_int, c_int, c_int, P, P, P]),
     "mace_set_prior": (c_int, [P, c_int, c_double, c_double, c_double, c_double, c_double]),
     "mace_setup_agents": (c_int, [P, c_int, P, P, c_int, c_int, c_int, c_int]),
+    "mace_set_schedule": (c_int, [P, c_double, c_int64]),
     "mace_set_agent_params": (c_int, [P, c_int, c_double, c_double, c_int]),
     "mace_load_data": (c_int, [P, P, P]),
     "mace_set_state": (c_int, [P, c_int, P]),
@@ -61,6 +62,7 @@ _SIGS = {
     "mace_mean_from_sum": (c_int, [P, c_int]),
     "mace_iterate_finish": (c_int, [P, c_int, c_double, c_int]),
     "mace_read_log": (c_int, [P, c_int, P, P]),
+    "mace_k2_timing": (c_int, [P, c_int, P, P]),
     "mace_agent_csc": (c_int, [c_int, c_int, c_int, P, P, P, c_int, P, P, P, P]),
     "mace_sv_layout_probe": (c_int, [c_int, c_int, c_int, P, P, P, c_int, P, c_int, P, P, P, P]),
     "mace_host_alloc": (c_int, [c_size_t, ctypes.POINTER(c_void_p)]),

@@ -558,7 +558,7 @@ __global__ void k_prior_cost(const float* x, int n_side, PriorC P, double* part)
         }
         if (P.kind == 0) loc += P.eps * xs * xs;
     }
-    __shared__ double sh[1024];
+    __shared__ double sh[256];
     sh[threadIdx.x] = loc;
     __syncthreads();
     for (int o = blockDim.x / 2; o; o >>= 1) {

@@ -104,12 +104,46 @@ struct Ctx {
     double ref_norm2 = 0.0;
     int band_cap = 0;
     size_t sv_smem = 0;
-    int sv_grid = 0;
+    int sv_grid = 0, sv_warps = 0;
+    double sv_frac = 1.0 / 16.0;  // max fraction of an agent's tiles in flight
+    long sv_max_warps = 0;        // optional hard cap (0: none)
     int passes = 0;
     int num_sms = 148;
     // timing of the last iterate call
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // optional per-launch timing of K2 (bench roofline): event pairs on the launch stream
+    bool time_k2 = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k2ev;
+    size_t k2_used = 0;
+    ~Ctx()
+    {
+        for (auto& e : k2ev) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+    }
 };
+
+static cudaEvent_t k2_begin(Ctx* c)
+{
+    if (!c->time_k2) return nullptr;
+    if (c->k2_used == c->k2ev.size()) {
+        std::pair<cudaEvent_t, cudaEvent_t> e;
+        CK(cudaEventCreate(&e.first));
+        CK(cudaEventCreate(&e.second));
+        c->k2ev.push_back(e);
+    }
+    auto& e = c->k2ev[c->k2_used];
+    CK(cudaEventRecord(e.first, c->stream));
+    return e.second;
+}
+
+static void k2_end(Ctx* c, cudaEvent_t second)
+{
+    if (!second) return;
+    CK(cudaEventRecord(second, c->stream));
+    c->k2_used++;
+}
 
 static const int kRefBlocks = 256;
 
@@ -127,21 +161,26 @@ static void sync(Ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
 
 // ------------------------------------------------------------------ K2 launch helpers
 template <int NV>
-static void launch_sv(Ctx* c, const PassParams& P, int items)
+static void launch_sv(Ctx* c, const PassParams& P, int items, int agents_in_queue)
 {
     auto kern = k_icd_sv<NV, 4>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sv_smem));
     int nb = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, c->sv_smem));
     if (nb < 1) throw std::runtime_error("super-voxel kernel does not fit on an SM (band too large)");
-    long grid = (long)nb * c->num_sms;
-    if (const char* e = std::getenv("MACE_SV_MAX_WARPS")) {
-        long mw = std::atol(e);
-        if (mw > 0) grid = std::min(grid, std::max(1L, mw / 4));
-    }
-    grid = std::min<long>(grid, (items + 3) / 4);
+    // Concurrency bound: at most a fraction `sv_frac` of an agent's tiles are in flight at once
+    // (bounded staleness), never fewer than one tile per agent, never more than
+    // the resident warps of the whole GPU.
+    long warps = (long)nb * 4 * c->num_sms;
+    long cap = (long)std::floor(c->sv_frac * (double)items);
+    cap = std::max<long>(cap, agents_in_queue);
+    if (c->sv_max_warps > 0) cap = std::min<long>(cap, c->sv_max_warps);
+    warps = std::max(1L, std::min(warps, cap));
+    const int threads = warps >= 4 ? 128 : (int)warps * 32;
+    const long grid = warps >= 4 ? warps / 4 : 1;
     c->sv_grid = (int)grid;
-    kern<<<(int)grid, 128, c->sv_smem, c->stream>>>(P);
+    c->sv_warps = (int)(grid * threads / 32);
+    kern<<<(int)grid, threads, c->sv_smem, c->stream>>>(P);
     CK(cudaGetLastError());
 }
 
@@ -178,14 +217,17 @@ static void run_pass(Ctx* c, int mode, float rho, const float* gimg, int a0, int
     if (c->schedule == 0 && (P.s_begin != 0 || P.s_end != (long)c->n))
         throw std::runtime_error("pixel ranges need the raster schedule");
     if (c->schedule == 1) {
+        cudaEvent_t ev = k2_begin(c);
         switch (c->NV) {
             case 1: launch_raster<1>(c, P, na, a0); break;
             case 2: launch_raster<2>(c, P, na, a0); break;
             default: launch_raster<4>(c, P, na, a0); break;
         }
+        k2_end(c, ev);
         return;
     }
     CK(cudaMemsetAsync(c->head.p, 0, sizeof(unsigned), c->stream));
+    cudaEvent_t ev = k2_begin(c);
     if (na == c->n_local) {
         P.queue = c->queue.p;
         P.n_items = c->n_items;
@@ -195,10 +237,11 @@ static void run_pass(Ctx* c, int mode, float rho, const float* gimg, int a0, int
         P.n_items = c->am[a0]->n_sv;
     }
     switch (c->NV) {
-        case 1: launch_sv<1>(c, P, P.n_items); break;
-        case 2: launch_sv<2>(c, P, P.n_items); break;
-        default: launch_sv<4>(c, P, P.n_items); break;
+        case 1: launch_sv<1>(c, P, P.n_items, na); break;
+        case 2: launch_sv<2>(c, P, P.n_items, na); break;
+        default: launch_sv<4>(c, P, P.n_items, na); break;
     }
+    k2_end(c, ev);
 }
 
 static void refresh(Ctx* c, int a0, int na)
@@ -604,10 +647,20 @@ int mace_ctx_info(void* p, int64_t* info /* [8] */)
     info[1] = c->n_items;
     info[2] = c->NV;
     info[3] = (int64_t)c->sv_smem;
-    info[4] = c->sv_grid;
+    info[4] = c->sv_warps;
     info[5] = c->num_sms;
     info[6] = c->passes;
     info[7] = c->S;
+    API_END
+}
+
+int mace_set_schedule(void* p, double concurrency, int64_t max_warps)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (!(concurrency > 0.0) || concurrency > 1.0) throw std::runtime_error("concurrency must be in (0, 1]");
+    c->sv_frac = concurrency;
+    c->sv_max_warps = (long)max_warps;
     API_END
 }
 
@@ -756,7 +809,7 @@ int mace_cost(void* p, const float* x, double beta, double* like, double* prior)
     pp.alloc(b1 + b2);
     FPParams F{c->rp.p, c->cols.p, c->vals.p, c->n_ch};
     k_fp_rows<<<b1, 256, 0, c->stream>>>(F, rows, dx.p, nullptr, c->y.p, c->lam.p, pp.p);
-    k_prior_cost<<<b2, 1024, 0, c->stream>>>(dx.p, c->n_side, c->prior, pp.p + b1);
+    k_prior_cost<<<b2, 256, 0, c->stream>>>(dx.p, c->n_side, c->prior, pp.p + b1);
     CK(cudaGetLastError());
     std::vector<double> h(b1 + b2);
     CK(cudaMemcpyAsync(h.data(), pp.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c->stream));
@@ -989,6 +1042,31 @@ int mace_sv_layout_probe(int n_side, int n_ch, int n_views, const int64_t* row_p
     stats[3] = L.n_sv;
     stats[4] = L.duplicates;
     stats[5] = k;
+    API_END
+}
+
+// K2 launch timing: enable=1 starts a fresh record; enable=0 stops and returns the summed
+// device time (ms) and the number of K2 launches recorded since.
+int mace_k2_timing(void* p, int enable, double* total_ms, int64_t* launches)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (enable) {
+        c->time_k2 = true;
+        c->k2_used = 0;
+    } else {
+        sync(c);
+        double s = 0.0;
+        for (size_t i = 0; i < c->k2_used; ++i) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, c->k2ev[i].first, c->k2ev[i].second));
+            s += ms;
+        }
+        if (total_ms) *total_ms = s;
+        if (launches) *launches = (int64_t)c->k2_used;
+        c->time_k2 = false;
+        c->k2_used = 0;
+    }
     API_END
 }
 

@@ -24,6 +24,7 @@ from .geometry import global_csr
 SCHEDULES = {"sv": 0, "raster": 1}
 DEFAULT_SV = int(os.environ.get("MACE_SV", "8"))
 DEFAULT_COLOURS = int(os.environ.get("MACE_COLOURS", "4"))
+DEFAULT_CONCURRENCY = float(os.environ.get("MACE_SV_CONCURRENCY", str(1.0 / 16.0)))
 
 
 def _n_side_of(matrices) -> int:
@@ -153,6 +154,7 @@ class AgentPlan(_Context):
         self.call("mace_setup_agents", len(self.agent_views), N.ptr(counts), N.ptr(flat), SCHEDULES[schedule],
                   int(sv_eff), int(colours), 0)
         self.n_local = len(self.agent_views)
+        self.set_schedule(DEFAULT_CONCURRENCY, int(os.environ.get("MACE_SV_MAX_WARPS", "0")))
 
     def agent_info(self, a):
         buf = np.zeros(8, np.int64)
@@ -161,8 +163,27 @@ class AgentPlan(_Context):
                         buf.tolist()))
 
     def load_data(self, y, weights):
-        y32, w32 = N.f32(y), N.f32(weights)
-        self.call("mace_load_data", N.ptr(y32), N.ptr(w32))
+        """y / weights (n_views x n_ch, any float dtype) -> pinned float32 staging -> device."""
+        rows = self.n_views * self.n_ch
+        if getattr(self, "_pin", None) is None:
+            p = ctypes.c_void_p()
+            N.check(self.L.mace_host_alloc(2 * rows * 4, ctypes.byref(p)), "host_alloc")
+            self._pin = p
+            self._pin_arr = np.ctypeslib.as_array((ctypes.c_float * (2 * rows)).from_address(p.value))
+        np.copyto(self._pin_arr[:rows], np.asarray(y).reshape(-1), casting="same_kind")
+        np.copyto(self._pin_arr[rows:], np.asarray(weights).reshape(-1), casting="same_kind")
+        self.call("mace_load_data", ctypes.c_void_p(self._pin.value), ctypes.c_void_p(self._pin.value + rows * 4))
+
+    def close(self):
+        if getattr(self, "_pin", None) is not None:
+            if getattr(self, "h", None):
+                self.L.mace_sync(self.h)
+            self.L.mace_host_free(self._pin)
+            self._pin = None
+        super().close()
+
+    def set_schedule(self, concurrency=DEFAULT_CONCURRENCY, max_warps=0):
+        self.call("mace_set_schedule", float(concurrency), int(max_warps))
 
     def set_agent_params(self, local, beta_eff, inv_sigma2, clamp=False):
         self.call("mace_set_agent_params", int(local), float(beta_eff), float(inv_sigma2), int(bool(clamp)))
@@ -229,6 +250,11 @@ class AgentPlan(_Context):
         self.call("mace_iterate", int(iters), int(iter0), float(rho), int(bool(use_g)), float(tol), int(n_total),
                   int(bool(with_ref)), ctypes.byref(ms))
         return float(ms.value)
+
+    def k2_timing(self, enable: bool):
+        ms, n = ctypes.c_double(0.0), ctypes.c_int64(0)
+        self.call("mace_k2_timing", int(bool(enable)), ctypes.byref(ms), ctypes.byref(n))
+        return ms.value, n.value
 
     def iterate_local(self, rho, use_g):
         self.call("mace_iterate_local", float(rho), int(bool(use_g)))

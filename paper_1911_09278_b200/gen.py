@@ -19,12 +19,19 @@ import numpy as np
 FOV_MM = 128.0
 
 # BASELINE.json:configs -> (n_side, n_views, n_channels, n_agents, iterations, I0, n_ellipses, slices)
+# beta is the reference-convention qGGMRF strength (p=2, q=1.2, T=1, sigma_x=0.01); sigma is the
+# agents' proximal parameter.  BASELINE leaves both open; values and probes in DESIGN.md §3.
 CONFIGS = {
-    0: dict(n_side=128, n_views=180, n_channels=185, n_agents=4, iters=30, I0=1e4, n_ellipses=10, slices=1),
-    1: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=40, I0=1e4, n_ellipses=10, slices=1),
-    2: dict(n_side=1024, n_views=1440, n_channels=1450, n_agents=16, iters=50, I0=5e3, n_ellipses=40, slices=1),
-    3: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=40, I0=1e4, n_ellipses=10, slices=1),
-    4: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=30, I0=1e4, n_ellipses=10, slices=64),
+    0: dict(n_side=128, n_views=180, n_channels=185, n_agents=4, iters=30, I0=1e4, n_ellipses=10, slices=1,
+            beta=100.0, sigma=3e-4),
+    1: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=40, I0=1e4, n_ellipses=10, slices=1,
+            beta=25.0, sigma=3.5e-4),
+    2: dict(n_side=1024, n_views=1440, n_channels=1450, n_agents=16, iters=50, I0=5e3, n_ellipses=40, slices=1,
+            beta=4.0, sigma=3.5e-4),
+    3: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=40, I0=1e4, n_ellipses=10, slices=1,
+            beta=25.0, sigma=3.5e-4),
+    4: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=30, I0=1e4, n_ellipses=10, slices=64,
+            beta=25.0, sigma=3.5e-4),
 }
 
 
@@ -60,6 +67,34 @@ def ellipse_phantom(n_side: int, pitch: float, n_ellipses: int = 10, seed: int =
         img = np.where(u * u + v * v <= 1.0, val, img)
     img = img.reshape(n_side, 2, n_side, 2).mean(axis=(1, 3))
     return np.ascontiguousarray(img.ravel())
+
+
+def host_forward_project(matrices, x) -> np.ndarray:
+    """Float64 host projection used only to synthesise data (identical for every arm)."""
+    import scipy.sparse as sp
+
+    x = np.asarray(x, np.float64)
+    out = np.empty((len(matrices), matrices[0].n_channels))
+    for k, m in enumerate(matrices):
+        A = sp.csr_matrix((m.lens, m.cols, m.row_ptr), shape=(m.n_channels, m.n_pixels))
+        out[k] = A @ x
+    return out
+
+
+def make_scan(config: int = 1, seed: int = 0, slice_index: int = 0, matrices=None):
+    """(geometry, matrices, phantom, y, weights) for BASELINE config `config` (seeded)."""
+    from .geometry import Geometry, build_system_matrix
+
+    c = CONFIGS[config]
+    ns = c["n_side"]
+    pitch = 1.0 if config == 0 else pitch_for(ns)
+    geom = Geometry(ns, pitch, c["n_views"], c["n_channels"], pitch)
+    if matrices is None:
+        matrices = build_system_matrix(geom)
+    s = seed + 1000 * slice_index
+    phantom = ellipse_phantom(ns, pitch, c["n_ellipses"], seed=s)
+    y, lam = poisson_sinogram(host_forward_project(matrices, phantom), c["I0"], seed=s + 1)
+    return geom, matrices, phantom, y, lam
 
 
 def poisson_sinogram(proj: np.ndarray, I0: float, seed: int = 1):
