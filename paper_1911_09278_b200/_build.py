@@ -23,8 +23,7 @@ FLAGS = [
 
 
 def _inputs():
-    out = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
-    out += [os.path.join(CSRC, h) for h in HEADERS if os.path.exists(os.path.join(CSRC, h))]
+    out = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".cpp", ".h"))]
     out.append(os.path.join(ROOT, "include", "mace_b200.h"))
     return out
 

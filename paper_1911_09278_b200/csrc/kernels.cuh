@@ -64,7 +64,8 @@ struct PassParams {
     int n_items;
     unsigned* head;
     double* part;  // [n_items * 4]: sum alpha^2, sum (w'-w)^2, sum w'^2, sum w^2
-    int band_cap;
+    int band_cap, view_cap;
+    int stage_tma;  // 1: stage bands with TMA bulk copies; 0: LDGSTS (cp.async.cg)
     const int* done;
     long s_begin, s_end;  // raster passes: pixel range [s_begin, s_end) (icd.py:222-246)
 };
@@ -154,210 +155,7 @@ __device__ __forceinline__ bool pixel_step(float t, float g, float c, float zs, 
     return true;
 }
 
-// ===========================================================================
-// K2 super-voxel pass.  One warp owns one (agent, super-voxel) work item at a
-// time, taken from a global queue in colour-class order, so concurrently
-// active tiles are spread across the image.  The tile's error-sinogram band
-// (one channel window per view) is staged in shared memory; the tile's pixels
-// are then updated sequentially in tile-raster order against the staged band
-// (Gauss-Seidel inside the tile), and the band's net change is folded back
-// into global e with red.add at the end (tiles of the same agent that run
-// concurrently see each other one tile late: the bounded-staleness schedule
-// of DESIGN.md §4).  Column entries are streamed with 128-bit loads D pixels
-// ahead of use.
-// ===========================================================================
-template <int NV, int D>
-__global__ void __launch_bounds__(128) k_icd_sv(PassParams P)
-{
-    extern __shared__ __align__(16) unsigned char smem[];
-    if (P.done && *P.done) return;
-    const int lane = threadIdx.x & 31;
-    const int S = P.S, SS = S * S, S2 = S + 2, T2 = S2 * S2, T2p = (T2 + 3) & ~3;
-    const int cap = P.band_cap;  // multiple of 4
-    const size_t per_warp = (size_t)12 * cap + 4 * T2p + 16 * SS;
-    unsigned char* base = smem + (threadIdx.x >> 5) * per_warp;
-    float2* sel = reinterpret_cast<float2*>(base);
-    float* se0 = reinterpret_cast<float*>(base + 8 * (size_t)cap);
-    float* zt = se0 + cap;
-    float* svv = zt + T2p;
-    float* sth = svv + SS;
-    int2* spe = reinterpret_cast<int2*>(sth + SS);
-    const int n = P.n_side;
-    const PriorC& PR = P.pr;
-
-    for (;;) {
-        unsigned item = 0;
-        if (lane == 0) item = atomicAdd(P.head, 1u);
-        item = __shfl_sync(FULL, item, 0);
-        if (item >= (unsigned)P.n_items) break;
-        const uint32_t code = __ldg(P.queue + item);
-        const AgentDev& A = P.agents[code >> 24];
-        const int sv = (int)(code & 0xffffffu);
-        float2* __restrict__ el = A.el;
-        float* __restrict__ z = A.z;
-        float* __restrict__ w = A.w;
-        const int V = A.V;
-        const int r0 = (sv / A.n_sv_side) * S, c0 = (sv % A.n_sv_side) * S;
-        const float beta = A.beta_eff, inv_s2 = A.inv_s2;
-        const int clamp = A.clamp;
-
-        // -- stage the band: half a warp per view
-        const int2* bt = A.band + (size_t)sv * V;
-        for (int j = lane >> 4; j < V; j += 2) {
-            const int2 b = __ldg(bt + j);
-            const int cnt = b.y & 0xffff, pos = b.y >> 16;
-            for (int c = lane & 15; c < cnt; c += 16) {
-                const float2 x = __ldcg(el + b.x + c);
-                sel[pos + c] = x;
-                se0[pos + c] = x.x;
-            }
-        }
-        // -- state tile with a one-pixel halo, targets, theta2, column table
-        for (int i = lane; i < T2; i += 32) {
-            const int rr = r0 - 1 + i / S2, cc = c0 - 1 + i % S2;
-            zt[i] = (rr >= 0 && rr < n && cc >= 0 && cc < n) ? __ldcg(z + (size_t)rr * n + cc) : 0.f;
-        }
-        for (int i = lane; i < SS; i += 32) {
-            const int rr = r0 + i / S, cc = c0 + i % S;
-            spe[i] = __ldg(A.pix + (size_t)sv * SS + i);
-            if (rr < n && cc < n) {
-                const size_t s = (size_t)rr * n + cc;
-                sth[i] = A.th[s];
-                svv[i] = P.mode ? 2.f * P.g[s] - w[s] : A.vt[s];
-            }
-        }
-        __syncwarp();
-
-        // -- sequential pixel loop, columns prefetched D pixels ahead
-        const float* __restrict__ av = A.val;
-        const uint16_t* __restrict__ ai = A.idx;
-        float4 rv[D][NV];
-        uint2 ri[D][NV];
-        auto fetch = [&](int k, float4 (&v4)[NV], uint2 (&i4)[NV]) {
-#pragma unroll
-            for (int j = 0; j < NV; ++j) {
-                v4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-                i4[j] = make_uint2(0u, 0u);
-            }
-            if (k < SS) {
-                const int2 pe = spe[k];
-#pragma unroll
-                for (int j = 0; j < NV; ++j) {
-                    const int e0 = 4 * (lane + 32 * j);
-                    if (e0 < pe.y) {
-                        v4[j] = __ldcs(reinterpret_cast<const float4*>(av + pe.x + e0));
-                        i4[j] = __ldcs(reinterpret_cast<const uint2*>(ai + pe.x + e0));
-                    }
-                }
-            }
-        };
-#pragma unroll
-        for (int u = 0; u < D; ++u) fetch(u, rv[u], ri[u]);
-        double dsq = 0.0;
-        for (int kb = 0; kb < SS; kb += D) {
-#pragma unroll
-            for (int u = 0; u < D; ++u) {
-                const int k = kb + u;
-                if (k < SS) {
-                    const int lr = k / S, lc = k % S;
-                    if (r0 + lr < n && c0 + lc < n) {
-                        const int len = spe[k].y;
-                        const int ci = (lr + 1) * S2 + (lc + 1);
-                        const float zs = zt[ci];
-                        float t = 0.f;
-#pragma unroll
-                        for (int j = 0; j < NV; ++j) {
-                            const int e0 = 4 * (lane + 32 * j);
-                            const float vv[4] = {rv[u][j].x, rv[u][j].y, rv[u][j].z, rv[u][j].w};
-                            const uint32_t ii[4] = {ri[u][j].x & 0xffffu, ri[u][j].x >> 16, ri[u][j].y & 0xffffu,
-                                                    ri[u][j].y >> 16};
-#pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                if (e0 + q < len) {
-                                    const float2 x = sel[ii[q]];
-                                    t = fmaf(vv[q] * x.y, x.x, t);
-                                }
-                        }
-                        float g, c;
-                        {
-                            const int kk = lane & 7;
-                            const int gr = r0 + lr + c_dr[kk], gc = c0 + lc + c_dc[kk];
-                            const bool valid = gr >= 0 && gr < n && gc >= 0 && gc < n;
-                            const float zr = zt[(lr + 1 + c_dr[kk]) * S2 + (lc + 1 + c_dc[kk])];
-                            prior_lane(lane, zs, zr, valid && beta > 0.f, PR, g, c);
-                        }
-#pragma unroll
-                        for (int o = 16; o; o >>= 1) {
-                            t += __shfl_xor_sync(FULL, t, o);
-                            g += __shfl_xor_sync(FULL, g, o);
-                            c += __shfl_xor_sync(FULL, c, o);
-                        }
-                        float alpha;
-                        if (pixel_step(t, g, c, zs, svv[k], sth[k], beta, inv_s2, clamp, PR, alpha)) {
-                            if (lane == 0) {
-                                zt[ci] = zs + alpha;
-                                dsq += (double)alpha * alpha;
-                            }
-#pragma unroll
-                            for (int j = 0; j < NV; ++j) {
-                                const int e0 = 4 * (lane + 32 * j);
-                                const float vv[4] = {rv[u][j].x, rv[u][j].y, rv[u][j].z, rv[u][j].w};
-                                const uint32_t ii[4] = {ri[u][j].x & 0xffffu, ri[u][j].x >> 16,
-                                                        ri[u][j].y & 0xffffu, ri[u][j].y >> 16};
-#pragma unroll
-                                for (int q = 0; q < 4; ++q)
-                                    if (e0 + q < len) sel[ii[q]].x -= alpha * vv[q];
-                            }
-                        }
-                        __syncwarp();
-                    }
-                }
-                fetch(k + D, rv[u], ri[u]);
-            }
-        }
-        __syncwarp();
-
-        // -- fold the band's change back into global e
-        for (int j = lane >> 4; j < V; j += 2) {
-            const int2 b = __ldg(bt + j);
-            const int cnt = b.y & 0xffff, pos = b.y >> 16;
-            for (int c = lane & 15; c < cnt; c += 16) {
-                const float d = sel[pos + c].x - se0[pos + c];
-                if (d != 0.f) atomicAdd(&el[b.x + c].x, d);
-            }
-        }
-        // -- write the tile back; fused Mann step and norm partials
-        double dw2 = 0.0, wn2 = 0.0, wo2 = 0.0;
-        for (int i = lane; i < SS; i += 32) {
-            const int rr = r0 + i / S, cc = c0 + i % S;
-            if (rr < n && cc < n) {
-                const size_t s = (size_t)rr * n + cc;
-                const float zn = zt[(i / S + 1) * S2 + (i % S + 1)];
-                __stcg(z + s, zn);
-                if (P.mode) {
-                    const float wo = w[s];
-                    const float wn = P.rho * (2.f * zn - svv[i]) + (1.f - P.rho) * wo;
-                    w[s] = wn;
-                    const double dd = (double)wn - (double)wo;
-                    dw2 += dd * dd;
-                    wn2 += (double)wn * wn;
-                    wo2 += (double)wo * wo;
-                }
-            }
-        }
-        dw2 = warp_sum_d(dw2);
-        wn2 = warp_sum_d(wn2);
-        wo2 = warp_sum_d(wo2);
-        if (lane == 0) {
-            double* o = P.part + (size_t)item * 4;
-            o[0] = dsq;
-            o[1] = dw2;
-            o[2] = wn2;
-            o[3] = wo2;
-        }
-        __syncwarp();
-    }
-}
+// K2 super-voxel pass: see k_sv.cuh.
 
 // ===========================================================================
 // K2 raster pass: the reference's exact visiting order (pixels 0..n-1), one
@@ -491,6 +289,7 @@ __global__ void k_fp_agents(FPParams F, const AgentDev* agents, const int* row_b
         while (a + 1 < n_agents && row_base[a + 1] <= wr) ++a;
         const AgentDev& A = agents[a];
         const int r = wr - row_base[a];
+        if (r >= A.R) continue;  // alignment padding between agents
         const int j = r / F.n_ch, ch = r % F.n_ch;
         const int64_t g = (int64_t)A.views[j] * F.n_ch + ch;
         float acc = 0.f;
@@ -611,13 +410,14 @@ __global__ void __launch_bounds__(128) k_theta2_sv(const AgentDev* agents, int n
             const int cnt = b.y & 0xffff, pos = b.y >> 16;
             for (int c = lane & 15; c < cnt; c += 16) lamb[pos + c] = A.el[b.x + c].y;
         }
+        if (lane == 0) lamb[A.bsize[sv]] = 0.f;  // dummy row referenced by pad slots (value 0)
         __syncwarp();
         for (int k = 0; k < SS; ++k) {
             const int rr = r0 + k / S, cc = c0 + k % S;
             if (rr >= n_side || cc >= n_side) continue;
             const int2 pe = A.pix[(size_t)sv * SS + k];
             float acc = 0.f;
-            for (int e = lane; e < pe.y; e += 32) {
+            for (int e = lane; e < ((pe.y + 7) & ~7); e += 32) {
                 const float a = A.val[pe.x + e];
                 acc = fmaf(a * a, lamb[A.idx[pe.x + e]], acc);
             }
@@ -637,6 +437,7 @@ __global__ void k_gather_data(const AgentDev* agents, const int* row_base, int n
         while (a + 1 < n_agents && row_base[a + 1] <= wr) ++a;
         const AgentDev& A = agents[a];
         const int r = wr - row_base[a];
+        if (r >= A.R) continue;
         const int64_t g = (int64_t)A.views[r / n_ch] * n_ch + r % n_ch;
         A.y[r] = y[g];
         A.el[r].y = lam[g];

@@ -46,6 +46,7 @@ void build_agent_csc(int n_side, int n_ch, const int64_t* row_ptr, const int32_t
 }
 
 static inline int64_t pad4(int64_t x) { return (x + 3) & ~int64_t(3); }
+static inline int64_t pad8(int64_t x) { return (x + 7) & ~int64_t(7); }
 
 void build_raster_layout(const AgentCSC& csc, int n, RasterLayout& out)
 {
@@ -109,14 +110,21 @@ void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SV
                 hi[j] = std::max(hi[j], ch);
             }
             out.max_col = std::max<int>(out.max_col, (int)L);
-            ent += pad4(L);
+            ent += pad8(L);
         }
         int pos = 0;
         for (int j = 0; j < V; ++j) {
-            const int cnt = hi[j] >= 0 ? hi[j] - lo[j] + 1 : 0;
-            out.band[(size_t)sv * V + j] = {(int32_t)(j * n_ch + (cnt ? lo[j] : 0)), (int32_t)((pos << 16) | cnt)};
+            // window of local rows, widened to 16-byte ({e, lambda} float2 pairs) alignment so the
+            // kernel can stage it with one bulk (TMA) copy per view; pads are never referenced
+            int start = 0, cnt = 0;
+            if (hi[j] >= 0) {
+                start = (j * n_ch + lo[j]) & ~1;
+                const int end = ((j * n_ch + hi[j]) | 1) + 1;
+                cnt = end - start;
+            }
+            out.band[(size_t)sv * V + j] = {(int32_t)start, (int32_t)((pos << 16) | cnt)};
             pos += cnt;
-            if (pos > 65535) throw std::runtime_error("super-voxel band exceeds 65535 rows; use a smaller tile");
+            if (pos > 65534) throw std::runtime_error("super-voxel band exceeds 65534 rows; use a smaller tile");
         }
         out.bsize[sv] = pos;
         out.max_band = std::max(out.max_band, pos);
@@ -126,11 +134,20 @@ void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SV
     if (total >= (int64_t)1 << 31) throw std::runtime_error("super-voxel layout exceeds 2^31 entries per agent");
     out.idx.assign(total, 0);
     out.val.assign(total, 0.0f);
-    // pass 2: entries, SV-major, pixels in tile-raster order, band-local indices
+    // pass 2: entries, SV-major, pixels in tile-raster order, band-local indices.
+    // Within a column, entries are stored in groups of 128 (16 lanes x 8 slots); inside
+    // a group of Lg entries (L8 = ceil(Lg/8)) slot 8l+q holds entry l + q*L8, so lane l's
+    // two 128-bit value loads and one 128-bit index load bring entries l, l+L8, ...,
+    // l+7L8: at every step the half-warp touches consecutive entries (consecutive
+    // views' windows -> spread shared-memory banks).  Columns are padded to 8 slots.
+    // Pads carry value 0 and the tile's dummy band row B (never a real row).
     int64_t pos = 0;
+    std::vector<uint16_t> ci;
+    std::vector<float> cv;
     for (int sv = 0; sv < out.n_sv; ++sv) {
         const int r0 = (sv / out.n_sv_side) * S, c0 = (sv % out.n_sv_side) * S;
         const int2_t* bt = &out.band[(size_t)sv * V];
+        const uint16_t dummy = (uint16_t)out.bsize[sv];
         for (int k = 0; k < S * S; ++k) {
             const int r = r0 + k / S, c = c0 + k % S;
             if (r >= n_side || c >= n_side) {
@@ -138,25 +155,35 @@ void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SV
                 continue;
             }
             const int64_t s = (int64_t)r * n_side + c;
-            int64_t L = 0;
+            ci.clear();
+            cv.clear();
             uint32_t prev = UINT32_MAX;
             for (int64_t q = csc.col_ptr[s]; q < csc.col_ptr[s + 1]; ++q) {
                 const uint32_t row = csc.row[q];
                 if (row == prev) {  // merge duplicate entry (sum of lengths)
-                    out.val[pos + L - 1] += csc.val[q];
+                    cv.back() += csc.val[q];
                     out.duplicates++;
                     continue;
                 }
                 prev = row;
                 const int j = (int)(row / n_ch), ch = (int)(row % n_ch);
                 const int2_t b = bt[j];
-                const int lo_j = b.x - j * n_ch;
-                out.idx[pos + L] = (uint16_t)((b.y >> 16) + (ch - lo_j));
-                out.val[pos + L] = csc.val[q];
-                ++L;
+                ci.push_back((uint16_t)((b.y >> 16) + (j * n_ch + ch - b.x)));
+                cv.push_back(csc.val[q]);
+            }
+            const int L = (int)ci.size();
+            for (int g0 = 0; g0 < std::max(L, 1); g0 += 128) {
+                const int Lg = std::min(128, L - g0), L8 = (std::max(Lg, 0) + 7) / 8;
+                for (int l = 0; l < L8; ++l)
+                    for (int q = 0; q < 8; ++q) {
+                        const int e = l + q * L8;
+                        const int64_t slot = pos + g0 + 8 * l + q;
+                        out.idx[slot] = e < Lg ? ci[g0 + e] : dummy;
+                        out.val[slot] = e < Lg ? cv[g0 + e] : 0.0f;
+                    }
             }
             out.pix[(size_t)sv * S * S + k] = {(int32_t)pos, (int32_t)L};
-            pos += pad4(L);
+            pos += pad8(L);
         }
     }
 }

@@ -19,6 +19,7 @@
 
 #include "internal.h"
 #include "kernels.cuh"
+#include "k_sv.cuh"
 #include "mace_b200.h"
 
 namespace mace {
@@ -102,11 +103,13 @@ struct Ctx {
     DBuf<float> wbar, g, ref, wsum;
     DBuf<double> refpart;
     double ref_norm2 = 0.0;
-    int band_cap = 0;
+    int band_cap = 0, view_cap = 0;
     size_t sv_smem = 0;
     int sv_grid = 0, sv_warps = 0;
     double sv_frac = 1.0 / 16.0;  // max fraction of an agent's tiles in flight
     long sv_max_warps = 0;        // optional hard cap (0: none)
+    int sv_depth = 4;             // column prefetch depth (steps ahead), 2 or 4
+    int stage_tma = 0;            // band staging: 0 LDGSTS (default), 1 TMA bulk copies
     int passes = 0;
     int num_sms = 148;
     // timing of the last iterate call
@@ -160,10 +163,10 @@ static void upload_prior_consts()
 static void sync(Ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
 
 // ------------------------------------------------------------------ K2 launch helpers
-template <int NV>
+template <int S, int D, bool P2>
 static void launch_sv(Ctx* c, const PassParams& P, int items, int agents_in_queue)
 {
-    auto kern = k_icd_sv<NV, 4>;
+    auto kern = k_icd_sv<S, D, P2>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sv_smem));
     int nb = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, c->sv_smem));
@@ -191,6 +194,20 @@ static void launch_raster(Ctx* c, const PassParams& P, int n_agents, int agent_b
     CK(cudaGetLastError());
 }
 
+template <int D, bool P2>
+static void dispatch_sv(Ctx* c, const PassParams& P, int na)
+{
+    switch (c->S) {
+        case 2: launch_sv<2, D, P2>(c, P, P.n_items, na); break;
+        case 4: launch_sv<4, D, P2>(c, P, P.n_items, na); break;
+        case 6: launch_sv<6, D, P2>(c, P, P.n_items, na); break;
+        case 8: launch_sv<8, D, P2>(c, P, P.n_items, na); break;
+        case 12: launch_sv<12, D, P2>(c, P, P.n_items, na); break;
+        case 16: launch_sv<16, D, P2>(c, P, P.n_items, na); break;
+        default: throw std::runtime_error("super-voxel side must be one of 2, 4, 6, 8, 12, 16");
+    }
+}
+
 static PassParams base_params(Ctx* c)
 {
     PassParams P{};
@@ -199,6 +216,8 @@ static PassParams base_params(Ctx* c)
     P.n_side = c->n_side;
     P.S = c->S;
     P.band_cap = c->band_cap;
+    P.view_cap = c->view_cap;
+    P.stage_tma = c->stage_tma;
     P.head = c->head.p;
     P.part = c->part.p;
     P.done = c->done.p;
@@ -236,10 +255,13 @@ static void run_pass(Ctx* c, int mode, float rho, const float* gimg, int a0, int
         P.queue = c->am[a0]->queue.p;
         P.n_items = c->am[a0]->n_sv;
     }
-    switch (c->NV) {
-        case 1: launch_sv<1>(c, P, P.n_items, na); break;
-        case 2: launch_sv<2>(c, P, P.n_items, na); break;
-        default: launch_sv<4>(c, P, P.n_items, na); break;
+    const bool p2 = c->prior.kind == 0 || c->prior.p_is_2;
+    if (c->sv_depth <= 2) {
+        if (p2) dispatch_sv<2, true>(c, P, na);
+        else dispatch_sv<2, false>(c, P, na);
+    } else {
+        if (p2) dispatch_sv<4, true>(c, P, na);
+        else dispatch_sv<4, false>(c, P, na);
     }
     k2_end(c, ev);
 }
@@ -515,7 +537,8 @@ int mace_setup_agents(void* p, int n_local, const int* view_counts, const int* v
     // device buffers
     c->total_rows = 0;
     std::vector<int> rb(n_local + 1, 0);
-    for (int a = 0; a < n_local; ++a) rb[a + 1] = rb[a] + c->am[a]->R;
+    // each agent's {e, lambda} block starts on a 16-byte boundary (TMA bulk copies)
+    for (int a = 0; a < n_local; ++a) rb[a + 1] = rb[a] + ((c->am[a]->R + 1) & ~1);
     c->total_rows = rb[n_local];
     c->row_base.alloc(n_local + 1);
     CK(cudaMemcpy(c->row_base.p, rb.data(), sizeof(int) * (n_local + 1), cudaMemcpyHostToDevice));
@@ -598,14 +621,16 @@ int mace_setup_agents(void* p, int n_local, const int* view_counts, const int* v
     }
     c->NV = max_col <= 128 ? 1 : (max_col <= 256 ? 2 : 4);
     if (max_col > 512) throw std::runtime_error("column longer than 512 entries");
-    c->band_cap = (max_band + 3) & ~3;
+    c->band_cap = (max_band + 1 + 3) & ~3;  // + the dummy row that pad slots point at
     if (schedule == 0) {
         std::vector<uint32_t> q = build_queue(n_local, n_sv_side, colours);
         c->queue.alloc(q.size());
         CK(cudaMemcpy(c->queue.p, q.data(), sizeof(uint32_t) * q.size(), cudaMemcpyHostToDevice));
         c->n_items = (int)q.size();
-        const int S = c->S, T2p = ((S + 2) * (S + 2) + 3) & ~3;
-        c->sv_smem = (size_t)4 * (12 * (size_t)c->band_cap + 4 * T2p + 16 * S * S);
+        int vmax = 0;
+        for (int a = 0; a < n_local; ++a) vmax = std::max(vmax, (int)c->am[a]->views.size());
+        c->view_cap = (vmax + 1) & ~1;
+        c->sv_smem = 4 * sv_warp_bytes(c->S, c->band_cap, c->view_cap);
         if (c->sv_smem > 227 * 1024) throw std::runtime_error("super-voxel band does not fit in shared memory");
     } else {
         c->n_items = n_local;
@@ -661,6 +686,8 @@ int mace_set_schedule(void* p, double concurrency, int64_t max_warps)
     if (!(concurrency > 0.0) || concurrency > 1.0) throw std::runtime_error("concurrency must be in (0, 1]");
     c->sv_frac = concurrency;
     c->sv_max_warps = (long)max_warps;
+    if (const char* d = std::getenv("MACE_SV_DEPTH")) c->sv_depth = std::atoi(d) <= 2 ? 2 : 4;
+    if (const char* t = std::getenv("MACE_SV_STAGE")) c->stage_tma = std::string(t) == "tma";
     API_END
 }
 
@@ -1023,8 +1050,13 @@ int mace_sv_layout_probe(int n_side, int n_ch, int n_views, const int64_t* row_p
         const int2_t* bt = &L.band[(size_t)sv * L.views];
         for (int q = 0; q < S * S; ++q) {
             const int2_t pe = L.pix[(size_t)sv * S * S + q];
-            for (int e = 0; e < pe.y; ++e) {
+            const int B = L.bsize[sv];
+            for (int e = 0; e < ((pe.y + 7) & ~7); ++e) {
                 const int li = L.idx[pe.x + e];
+                if (li == B) {  // pad slot
+                    if (L.val[pe.x + e] != 0.0f) throw std::runtime_error("pad slot with a value");
+                    continue;
+                }
                 int j = 0;
                 while (!(bt[j].y & 0xffff) || li >= (bt[j].y >> 16) + (bt[j].y & 0xffff) || li < (bt[j].y >> 16)) ++j;
                 if (pix_out) {

@@ -22,6 +22,7 @@ from . import _native as N
 from .geometry import global_csr
 
 SCHEDULES = {"sv": 0, "raster": 1}
+SV_SIDES = (2, 4, 6, 8, 12, 16)  # tile sides compiled into k_icd_sv
 DEFAULT_SV = int(os.environ.get("MACE_SV", "8"))
 DEFAULT_COLOURS = int(os.environ.get("MACE_COLOURS", "4"))
 DEFAULT_CONCURRENCY = float(os.environ.get("MACE_SV_CONCURRENCY", str(1.0 / 16.0)))
@@ -149,8 +150,8 @@ class AgentPlan(_Context):
         flat = np.array([v for vs in self.agent_views for v in vs], np.int32)
         sv_eff = sv
         if schedule == "sv":
-            sv_eff = max(2, min(sv, self.n_side + (self.n_side & 1)))
-            sv_eff += sv_eff & 1
+            lim = min(sv, self.n_side + (self.n_side & 1))
+            sv_eff = max([s for s in SV_SIDES if s <= max(lim, 2)])
         self.call("mace_setup_agents", len(self.agent_views), N.ptr(counts), N.ptr(flat), SCHEDULES[schedule],
                   int(sv_eff), int(colours), 0)
         self.n_local = len(self.agent_views)
