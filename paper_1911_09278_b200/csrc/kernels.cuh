@@ -486,31 +486,41 @@ __global__ void k_consensus(const float* W, int n_local, size_t n, float scale, 
     }
 }
 
-// fixed-order reduction of the per-item partials -> out4 (and nrmse^2 partials -> out4[4])
-__global__ void k_norms(const double* part, int n_items, const double* ref_part, int n_ref, double* out5,
-                        const int* done)
+// Fixed-order reduction of the per-item partials -> out5[0..3] (and the nrmse^2 partials
+// -> out5[4]).  Each block folds a contiguous slice into scratch[5 * block]; the last
+// block to finish folds the block sums in block order, so the result is deterministic.
+__global__ void k_norms(const double* part, int n_items, const double* ref_part, int n_ref, double* scratch,
+                        double* out5, unsigned* counter, const int* done)
 {
     if (done && *done) return;
-    __shared__ double sh[4][256];
-    __shared__ double shr[256];
-    double a[4] = {0, 0, 0, 0}, r = 0.0;
-    for (int i = threadIdx.x; i < n_items; i += blockDim.x)
+    __shared__ double sh[5][256];
+    __shared__ bool last;
+    double a[5] = {0, 0, 0, 0, 0};
+    const int chunk = (n_items + gridDim.x - 1) / gridDim.x;
+    const int i0 = blockIdx.x * chunk, i1 = min(n_items, i0 + chunk);
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x)
         for (int k = 0; k < 4; ++k) a[k] += part[(size_t)i * 4 + k];
-    if (ref_part)
-        for (int i = threadIdx.x; i < n_ref; i += blockDim.x) r += ref_part[i];
-    for (int k = 0; k < 4; ++k) sh[k][threadIdx.x] = a[k];
-    shr[threadIdx.x] = r;
+    if (ref_part && blockIdx.x == 0)
+        for (int i = threadIdx.x; i < n_ref; i += blockDim.x) a[4] += ref_part[i];
+    for (int k = 0; k < 5; ++k) sh[k][threadIdx.x] = a[k];
     __syncthreads();
     for (int o = blockDim.x / 2; o; o >>= 1) {
-        if ((int)threadIdx.x < o) {
-            for (int k = 0; k < 4; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + o];
-            shr[threadIdx.x] += shr[threadIdx.x + o];
-        }
+        if ((int)threadIdx.x < o)
+            for (int k = 0; k < 5; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + o];
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        for (int k = 0; k < 4; ++k) out5[k] = sh[k][0];
-        out5[4] = shr[0];
+        for (int k = 0; k < 5; ++k) scratch[5 * blockIdx.x + k] = sh[k][0];
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        double s[5] = {0, 0, 0, 0, 0};
+        for (int b = 0; b < (int)gridDim.x; ++b)
+            for (int k = 0; k < 5; ++k) s[k] += __ldcg(scratch + 5 * b + k);
+        for (int k = 0; k < 5; ++k) out5[k] = s[k];
+        *counter = 0u;
     }
 }
 

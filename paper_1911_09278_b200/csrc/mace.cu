@@ -98,7 +98,8 @@ struct Ctx {
     DBuf<double> part;
     DBuf<unsigned> head;
     DBuf<int> done;
-    DBuf<double> sums5, log;
+    DBuf<double> sums5, log, norm_scratch;
+    DBuf<unsigned> norm_counter;
     int log_cap = 0;
     DBuf<float> wbar, g, ref, wsum;
     DBuf<double> refpart;
@@ -149,6 +150,7 @@ static void k2_end(Ctx* c, cudaEvent_t second)
 }
 
 static const int kRefBlocks = 256;
+static const int kNormBlocks = 64;
 
 static void upload_prior_consts()
 {
@@ -393,6 +395,9 @@ int mace_ctx_create(int device, void** out)
     c->head.alloc(1);
     c->done.alloc(2);
     c->sums5.alloc(5);
+    c->norm_scratch.alloc(5 * kNormBlocks);
+    c->norm_counter.alloc(1);
+    CK(cudaMemset(c->norm_counter.p, 0, sizeof(unsigned)));
     CK(cudaMemset(c->head.p, 0, sizeof(unsigned)));
     CK(cudaMemset(c->done.p, 0, 2 * sizeof(int)));
     upload_prior_consts();
@@ -932,8 +937,9 @@ int mace_iterate(void* p, int iters, int iter0, double rho, int use_g, double to
         run_pass(c, 1, (float)rho, use_g ? c->g.p : c->wbar.p, 0, c->n_local);
         c->passes++;
         consensus(c, (float)n_total, c->wbar.p, with_ref && !use_g);
-        k_norms<<<1, 256, 0, c->stream>>>(c->part.p, c->n_items, with_ref && !use_g ? c->refpart.p : nullptr,
-                                          kRefBlocks, c->sums5.p, c->done.p);
+        k_norms<<<kNormBlocks, 256, 0, c->stream>>>(c->part.p, c->n_items,
+                                                    with_ref && !use_g ? c->refpart.p : nullptr, kRefBlocks,
+                                                    c->norm_scratch.p, c->sums5.p, c->norm_counter.p, c->done.p);
         k_finish<<<1, 1, 0, c->stream>>>(c->sums5.p, with_ref && !use_g ? c->ref_norm2 : 0.0, tol, iter0 + k,
                                          c->log.p, c->done.p, c->head.p);
         if (c->passes % 50 == 0) refresh(c, 0, c->n_local);  // icd.py:29,280-282
@@ -956,7 +962,8 @@ int mace_iterate_local(void* p, double rho, int use_g)
     run_pass(c, 1, (float)rho, use_g ? c->g.p : c->wbar.p, 0, c->n_local);
     c->passes++;
     consensus(c, 1.0f, c->wsum.p, false);
-    k_norms<<<1, 256, 0, c->stream>>>(c->part.p, c->n_items, nullptr, 0, c->sums5.p, c->done.p);
+    k_norms<<<kNormBlocks, 256, 0, c->stream>>>(c->part.p, c->n_items, nullptr, 0, c->norm_scratch.p, c->sums5.p,
+                                                c->norm_counter.p, c->done.p);
     CK(cudaGetLastError());
     API_END
 }

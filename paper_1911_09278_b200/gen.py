@@ -23,7 +23,7 @@ FOV_MM = 128.0
 # agents' proximal parameter.  BASELINE leaves both open; values and probes in DESIGN.md §3.
 CONFIGS = {
     0: dict(n_side=128, n_views=180, n_channels=185, n_agents=4, iters=30, I0=1e4, n_ellipses=10, slices=1,
-            beta=100.0, sigma=3e-4),
+            beta=100.0, sigma=2.5e-4),
     1: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=40, I0=1e4, n_ellipses=10, slices=1,
             beta=25.0, sigma=3.5e-4),
     2: dict(n_side=1024, n_views=1440, n_channels=1450, n_agents=16, iters=50, I0=5e3, n_ellipses=40, slices=1,
