@@ -109,6 +109,16 @@ int mace_read_log(void* ctx, int n, double* log, int* done2);
 /* per-launch CUDA-event timing of K2 on the context stream (enable=1 start, 0 stop + read) */
 int mace_k2_timing(void* ctx, int enable, double* total_ms, int64_t* launches);
 
+/* ---- the reference's compiled plug point, _sweep (icd.py:67-139), verbatim arguments:
+ * z[n], v[n], e[n_rows], CSC col_ptr[n+1] / row_idx / a_val, lam[n_rows], curv_data[n],
+ * nbr_idx / nbr_w [n*8]; float64 arithmetic, raster order over [s_begin, s_end), on the GPU.
+ * Mutates z and e in place; *delta_sq = sum alpha^2 (the reference's return value). */
+int mace_sweep_f64(double* z, const double* v, double* e, const int64_t* col_ptr, const int64_t* row_idx,
+                   const double* a_val, const double* lam, const double* curv_data, const int64_t* nbr_idx,
+                   const double* nbr_w, double beta_eff, double eps_reg, double inv_sigma2, int quad_prior, double p,
+                   double q, double T, double sigma_x, int clamp, int64_t s_begin, int64_t s_end, int64_t n,
+                   int64_t n_rows, double* delta_sq);
+
 /* ---- host-only layout probes (no device needed; used by the CPU test suite).
  * mace_agent_csc: the stacked agent CSC of icd.py:185-192; col_ptr[n+1] always, rows/vals if non-null.
  * mace_sv_layout_probe: the super-voxel layout decoded back to (pixel, local row, value) triples;

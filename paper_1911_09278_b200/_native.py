@@ -63,6 +63,8 @@ _SIGS = {
     "mace_iterate_finish": (c_int, [P, c_int, c_double, c_int]),
     "mace_read_log": (c_int, [P, c_int, P, P]),
     "mace_k2_timing": (c_int, [P, c_int, P, P]),
+    "mace_sweep_f64": (c_int, [P] * 10 + [c_double, c_double, c_double, c_int, c_double, c_double, c_double,
+                                          c_double, c_int, c_int64, c_int64, c_int64, c_int64, P]),
     "mace_agent_csc": (c_int, [c_int, c_int, c_int, P, P, P, c_int, P, P, P, P]),
     "mace_sv_layout_probe": (c_int, [c_int, c_int, c_int, P, P, P, c_int, P, c_int, P, P, P, P]),
     "mace_host_alloc": (c_int, [c_size_t, ctypes.POINTER(c_void_p)]),

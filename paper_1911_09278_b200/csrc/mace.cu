@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -20,6 +21,7 @@
 #include "internal.h"
 #include "kernels.cuh"
 #include "k_sv.cuh"
+#include "k_sweep64.cuh"
 #include "mace_b200.h"
 
 namespace mace {
@@ -1016,6 +1018,114 @@ int mace_read_log(void* p, int n, double* log, int* done2)
     if (n > 0) CK(cudaMemcpyAsync(log, c->log.p, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(done2, c->done.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
+    API_END
+}
+
+// ------------------------------------------------------------------ reference plug point: _sweep (icd.py:67-139)
+namespace {
+struct SweepEntry {
+    const void *k_cp, *k_ri, *k_av, *k_ni, *k_nw;
+    int64_t n = 0, nnz = 0, rows = 0;
+    DBuf<int64_t> col_ptr, row_idx, nbr_idx;
+    DBuf<double> a_val, nbr_w, z, v, e, lam, curv, dsq;
+    uint64_t last_use = 0;
+};
+std::mutex g_sweep_mu;
+std::vector<std::unique_ptr<SweepEntry>> g_sweep;
+uint64_t g_sweep_clock = 0;
+}  // namespace
+
+// Same arguments as the reference's numba _sweep (+ sizes); host float64 arrays in and out.
+// The static operator (col_ptr, row_idx, a_val, neighbour tables) is cached on the device
+// per workspace (keyed by host pointers and sizes); state, target, error sinogram, weights
+// and theta2 move every call.
+int mace_sweep_f64(double* z, const double* v, double* e, const int64_t* col_ptr, const int64_t* row_idx,
+                   const double* a_val, const double* lam, const double* curv_data, const int64_t* nbr_idx,
+                   const double* nbr_w, double beta_eff, double eps_reg, double inv_sigma2, int quad_prior, double p,
+                   double q, double T, double sx, int clamp, int64_t s_begin, int64_t s_end, int64_t n,
+                   int64_t n_rows, double* delta_sq)
+{
+    API_BEGIN
+    std::lock_guard<std::mutex> lk(g_sweep_mu);
+    if (s_begin < 0 || s_end > n || s_begin > s_end) throw std::runtime_error("bad pixel range");
+    const int64_t nnz = col_ptr[n];
+    SweepEntry* E = nullptr;
+    for (auto& x : g_sweep)
+        if (x->k_cp == col_ptr && x->k_ri == row_idx && x->k_av == a_val && x->k_ni == nbr_idx && x->k_nw == nbr_w &&
+            x->n == n && x->nnz == nnz && x->rows == n_rows)
+            E = x.get();
+    if (!E) {
+        if (g_sweep.size() >= 64) {
+            auto it = std::min_element(g_sweep.begin(), g_sweep.end(),
+                                       [](const auto& a, const auto& b) { return a->last_use < b->last_use; });
+            g_sweep.erase(it);
+        }
+        auto x = std::make_unique<SweepEntry>();
+        x->k_cp = col_ptr;
+        x->k_ri = row_idx;
+        x->k_av = a_val;
+        x->k_ni = nbr_idx;
+        x->k_nw = nbr_w;
+        x->n = n;
+        x->nnz = nnz;
+        x->rows = n_rows;
+        x->col_ptr.alloc(n + 1);
+        x->row_idx.alloc(std::max<int64_t>(nnz, 1));
+        x->a_val.alloc(std::max<int64_t>(nnz, 1));
+        x->nbr_idx.alloc(8 * n);
+        x->nbr_w.alloc(8 * n);
+        CK(cudaMemcpy(x->col_ptr.p, col_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+        if (nnz) {
+            CK(cudaMemcpy(x->row_idx.p, row_idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(x->a_val.p, a_val, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+        }
+        CK(cudaMemcpy(x->nbr_idx.p, nbr_idx, sizeof(int64_t) * 8 * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(x->nbr_w.p, nbr_w, sizeof(double) * 8 * n, cudaMemcpyHostToDevice));
+        x->z.alloc(n);
+        x->v.alloc(n);
+        x->curv.alloc(n);
+        x->e.alloc(std::max<int64_t>(n_rows, 1));
+        x->lam.alloc(std::max<int64_t>(n_rows, 1));
+        x->dsq.alloc(1);
+        E = x.get();
+        g_sweep.push_back(std::move(x));
+    }
+    E->last_use = ++g_sweep_clock;
+    CK(cudaMemcpy(E->z.p, z, sizeof(double) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(E->v.p, v, sizeof(double) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(E->curv.p, curv_data, sizeof(double) * n, cudaMemcpyHostToDevice));
+    if (n_rows) {
+        CK(cudaMemcpy(E->e.p, e, sizeof(double) * n_rows, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(E->lam.p, lam, sizeof(double) * n_rows, cudaMemcpyHostToDevice));
+    }
+    Sweep64 P{};
+    P.z = E->z.p;
+    P.e = E->e.p;
+    P.dsq = E->dsq.p;
+    P.v = E->v.p;
+    P.a_val = E->a_val.p;
+    P.lam = E->lam.p;
+    P.curv = E->curv.p;
+    P.nbr_w = E->nbr_w.p;
+    P.col_ptr = E->col_ptr.p;
+    P.row_idx = E->row_idx.p;
+    P.nbr_idx = E->nbr_idx.p;
+    P.beta_eff = beta_eff;
+    P.eps_reg = eps_reg;
+    P.inv_sigma2 = inv_sigma2;
+    P.p = p;
+    P.q = q;
+    P.T = T;
+    P.sx = sx;
+    P.quad = quad_prior;
+    P.clamp = clamp;
+    P.s_begin = s_begin;
+    P.s_end = s_end;
+    k_sweep64<<<1, 32>>>(P);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(z, E->z.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    if (n_rows) CK(cudaMemcpy(e, E->e.p, sizeof(double) * n_rows, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(delta_sq, E->dsq.p, sizeof(double), cudaMemcpyDeviceToHost));
     API_END
 }
 

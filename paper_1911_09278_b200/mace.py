@@ -299,8 +299,10 @@ def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=
         beta = problem.prior.beta if config.beta is None else config.beta
     views = [subsets[i].view_indices for i in local]
     if backend is None:
-        plan = plan_for(problem.matrices, views, schedule=config.schedule, sv=config.sv_side,
-                        colours=config.colours, device=config.device)
+        # getattr: the reference's own MaceConfig (no GPU knobs) is accepted too
+        plan = plan_for(problem.matrices, views, schedule=getattr(config, "schedule", "sv"),
+                        sv=getattr(config, "sv_side", DEFAULT_SV), colours=getattr(config, "colours", DEFAULT_COLOURS),
+                        device=getattr(config, "device", 0))
     else:
         plan = backend(problem, views)
     plan.load_data(problem.y, problem.weights)
@@ -429,23 +431,27 @@ def _apply_denoiser(plan, denoiser):
 
 
 def mace_solve(problem, config: MaceConfig, pool: WorkerPool | None = None, ref_image=None, w0=None,
-               comm=None) -> MaceResult:
+               comm=None, _backend=None) -> MaceResult:
     """Partial-update MACE with the conventional prior (mace.py:368-382).  Converges to
-    the MAP image of the full-data objective; returns the component average."""
+    the MAP image of the full-data objective; returns the component average.
+
+    ``comm``: None (single process), True (use the initialised default torch.distributed
+    group: agent i on rank i mod world), or a communicator object.  ``_backend`` is a test
+    hook replacing the device plan (the CPU tests of the multi-rank logic use it)."""
     if config.mode != CONVENTIONAL:
         raise ValueError("mace_solve requires mode='conventional'")
-    return _run_outer(problem, config, pool, ref_image, w0, denoiser=None, comm=comm)
+    return _run_outer(problem, config, pool, ref_image, w0, denoiser=None, comm=comm, backend=_backend)
 
 
 def mace_pnp_solve(problem, config: MaceConfig, pool: WorkerPool | None = None, ref_image=None, w0=None,
-                   denoiser=None, comm=None) -> MaceResult:
+                   denoiser=None, comm=None, _backend=None) -> MaceResult:
     """MACE with a PnP denoiser prior (mace.py:385-404): agents carry only data terms at
     sqrt(N) sigma; H acts once per iteration on the average; returns H(mean w)."""
     if config.mode != PNP:
         raise ValueError("mace_pnp_solve requires mode='pnp'")
     if denoiser is None:
         denoiser = make_denoiser(config.denoiser, problem.geom.n_side)
-    return _run_outer(problem, config, pool, ref_image, w0, denoiser=denoiser, comm=comm)
+    return _run_outer(problem, config, pool, ref_image, w0, denoiser=denoiser, comm=comm, backend=_backend)
 
 
 def equilibrium_residuals(problem, config: MaceConfig, w, prox_tol: float = 1e-9, denoiser=None) -> ResidualReport:
@@ -469,7 +475,7 @@ def equilibrium_residuals(problem, config: MaceConfig, w, prox_tol: float = 1e-9
     per_agent = []
     for i, sub in enumerate(subsets):
         ws = AgentWorkspace(problem, sub, config.n_subsets, sigma=sigma, beta=beta, state=x_hat,
-                            device=config.device)
+                            device=getattr(config, "device", 0))
         fi = prox_solve(ws, x_hat + seconds[i], tol=prox_tol)
         per_agent.append(float(np.linalg.norm(fi - x_hat)) / scale)
     return ResidualReport(mode=config.mode, r_F=max(per_agent), r_u=aux / scale, per_agent=per_agent)
