@@ -106,6 +106,13 @@ int mace_local_sum(void* ctx);
 int mace_mean_from_sum(void* ctx, int n_total);
 int mace_iterate_finish(void* ctx, int n_total, double tol, int iter);
 int mace_read_log(void* ctx, int n, double* log, int* done2);
+/* ---- K5: the PnP denoiser agent (17-layer 3x3 conv net, 64 ch, ReLU, out = x - net(x),
+ * bf16 weights/activations, tcgen05 implicit GEMM); replaces the `denoiser` callable of
+ * mace_pnp_solve (mace.py:385-404) applied in consensus_GH (mace.py:105-108).
+ * weights: 17 layers in OIHW order (1x1x3x3... 64x64x3x3 ... 1x64x3x3), bf16 bits. */
+int mace_cnn_set_weights(void* ctx, const uint16_t* bf16, int layers, int channels);
+int mace_cnn_apply(void* ctx); /* g = H(wbar), on the device */
+int mace_cnn_run(void* ctx, const float* x, float* out, int h, int w, float* ms_out);
 /* per-launch CUDA-event timing of K2 on the context stream (enable=1 start, 0 stop + read) */
 int mace_k2_timing(void* ctx, int enable, double* total_ms, int64_t* launches);
 

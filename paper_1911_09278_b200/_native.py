@@ -63,6 +63,9 @@ _SIGS = {
     "mace_iterate_finish": (c_int, [P, c_int, c_double, c_int]),
     "mace_read_log": (c_int, [P, c_int, P, P]),
     "mace_k2_timing": (c_int, [P, c_int, P, P]),
+    "mace_cnn_set_weights": (c_int, [P, P, c_int, c_int]),
+    "mace_cnn_apply": (c_int, [P]),
+    "mace_cnn_run": (c_int, [P, P, P, c_int, c_int, P]),
     "mace_sweep_f64": (c_int, [P] * 10 + [c_double, c_double, c_double, c_int, c_double, c_double, c_double,
                                           c_double, c_int, c_int64, c_int64, c_int64, c_int64, P]),
     "mace_agent_csc": (c_int, [c_int, c_int, c_int, P, P, P, c_int, P, P, P, P]),

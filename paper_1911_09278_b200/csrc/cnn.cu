@@ -1,0 +1,409 @@
+// K5: the PnP denoiser H of MACE-PnP (mace.py:105-108, applied to the consensus average)
+// as a 17-layer bias-free 3x3 conv net, 64 channels, ReLU, out = x - net(x), bf16 weights
+// and bf16 activations between layers, fp32 accumulation (BASELINE config 3).
+//
+// Layers 2..16 (64 -> 64) run on the 5th-gen tensor cores: an implicit GEMM per output row
+// segment of 128 pixels, D[128 px x 64 oc] = sum over 9 taps and 4 K-steps of
+// A[128 px x 16 ic] * W[16 ic x 64 oc]  (tcgen05.mma.cta_group::1.kind::f16, M=128, N=64,
+// K=16, fp32 accumulators in TMEM).  A-operand rows come from a rolling window of
+// channel-blocked halo rows ([8 channel groups][130 px][8 ch] bf16) loaded by 4-D TMA
+// (out-of-image coordinates are zero-filled = the conv's zero padding); the tap shift dx is
+// just a 16-byte offset of the UMMA descriptor (SWIZZLE_NONE, K-major).  The 9 taps'
+// weights (72 KB) stay resident in shared memory.  Two TMEM accumulators let the epilogue
+// (tcgen05.ld -> ReLU -> bf16 -> NHWC store) of row y-1 overlap the MMAs of row y.
+// Layers 1 (1 -> 64) and 17 (64 -> 1, fused residual) are CUDA-core kernels.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cnn.cuh"
+
+namespace mace {
+
+namespace {
+
+constexpr int kC = 64;             // channels
+constexpr int kTileX = 128;        // output pixels per tile (one row segment)
+constexpr int kHaloX = kTileX + 2;  // 130
+constexpr int kSlots = 4;          // rolling window of halo rows
+constexpr int kSlotBytes = 8 * kHaloX * 16;         // 16,640
+constexpr int kWBytes = 9 * kC * kC * 2;            // 73,728
+constexpr int kSmem = kWBytes + kSlots * kSlotBytes + 1024;
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity)
+{
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(s_u32(b)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_row(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar)
+{
+    // 4-D box {8 ch, 130 px, 1 row, 8 groups} at (0, x, y, 0)
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(s_u32(dst)),
+        "l"(map), "r"(0), "r"(x), "r"(y), "r"(0), "r"(s_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     s_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(s_u32(bar))
+                 : "memory");
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_NONE, K-major (cute/arch/mma_sm100_desc.hpp layout):
+// start>>4 [0,14), LBO>>4 [16,30) (K-adjacent core matrices), SBO>>4 [32,46) (8-row groups),
+// version 1 at [46,48), layout type 0 at [61,64).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo)
+{
+    return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | (1ull << 46);
+}
+
+// instruction descriptor: D f32, A/B bf16, both K-major, N = 64, M = 128
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate)
+{
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s_u32(bar))
+                 : "memory");
+}
+
+#define LD16(base, r)                                                                                             \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, " \
+                 "[%16];"                                                                                         \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),          \
+                   "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),       \
+                   "=r"(r[14]), "=r"(r[15])                                                                       \
+                 : "r"(base))
+
+// One 64->64 conv layer (+ ReLU) over a [H][W][64] bf16 NHWC image.  Grid: one CTA per
+// (x-strip, row range); 128 threads = 4 warps (warp w reads TMEM lanes 32w..32w+31).
+__global__ void __launch_bounds__(128, 1) k_conv64_tc(const __grid_constant__ CUtensorMap amap,
+                                                      const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* out,
+                                                      int H, int W, int rows_per_cta)
+{
+    extern __shared__ __align__(1024) unsigned char sm[];
+    unsigned char* sw = sm;                     // weights: [tap 9][ic-group 8][oc 64][8 ic]
+    unsigned char* slots = sm + kWBytes;        // [slot 4][ic-group 8][130 px][8 ch]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + kSlots * kSlotBytes);
+    uint64_t* wbar = bars;                      // weights landed
+    uint64_t* sbar = bars + 1;                  // [4] halo row landed
+    uint64_t* mbar = bars + 5;                  // [2] accumulator ready
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int strips = (W + kTileX - 1) / kTileX;
+    const int strip = blockIdx.x % strips;
+    const int x0 = strip * kTileX;
+    const int y0 = (blockIdx.x / strips) * rows_per_cta;
+    const int y1 = min(H, y0 + rows_per_cta);
+    if (y0 >= H) return;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(s_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 8; ++i) mbar_init(bars + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    // row r of the image lives in slot (r - (y0 - 1)) % 4; its k-th load uses parity k & 1
+    auto slot_of = [&](int r) { return (r - (y0 - 1)) & (kSlots - 1); };
+    auto slot_par = [&](int r) { return (uint32_t)(((r - (y0 - 1)) >> 2) & 1); };
+    if (tid == 0) {
+        mbar_expect(wbar, kWBytes);
+        bulk_copy(sw, wts, kWBytes, wbar);
+        for (int r = y0 - 1; r <= min(y0 + 1, y1); ++r) {
+            mbar_expect(sbar + slot_of(r), kSlotBytes);
+            tma_row(slots + slot_of(r) * kSlotBytes, &amap, x0 - 1, r, sbar + slot_of(r));
+        }
+    }
+    mbar_wait(wbar, 0);
+
+    const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
+    for (int y = y0; y <= y1; ++y) {
+        const int t = y - y0;  // tile index within this CTA
+        if (y < y1 && tid == 0) {
+            // tile y reads rows y-1, y, y+1
+            for (int r = y - 1; r <= y + 1; ++r) mbar_wait(sbar + slot_of(r), slot_par(r));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t d = tmem + (uint32_t)((t & 1) * 64);
+            int k = 0;
+#pragma unroll 1
+            for (int dy = 0; dy < 3; ++dy) {
+                const uint32_t row_base = sl_base + slot_of(y - 1 + dy) * kSlotBytes;
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx) {
+                    const uint32_t wtap = sw_base + (dy * 3 + dx) * (kC * kC * 2);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j, ++k) {
+                        // A: 128 px starting at halo column dx; K-step j = ic groups 2j, 2j+1
+                        const uint64_t a = sdesc(row_base + dx * 16 + 2 * j * (kHaloX * 16), kHaloX * 16, 128);
+                        const uint64_t b = sdesc(wtap + 2 * j * (kC * 16), kC * 16, 128);
+                        umma(d, a, b, k > 0);
+                    }
+                }
+            }
+            umma_commit(mbar + (t & 1));
+            // refill: row y+2 goes into the slot of row y-2, last read by tile y-1
+            if (y + 2 <= y1) {
+                if (t >= 1) mbar_wait(mbar + ((t - 1) & 1), (uint32_t)(((t - 1) >> 1) & 1));
+                const int r = y + 2;
+                mbar_expect(sbar + slot_of(r), kSlotBytes);
+                tma_row(slots + slot_of(r) * kSlotBytes, &amap, x0 - 1, r, sbar + slot_of(r));
+            }
+        }
+        if (t >= 1) {  // epilogue of tile y-1
+            const int te = t - 1, ye = y - 1;
+            mbar_wait(mbar + (te & 1), (uint32_t)((te >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((te & 1) * 64);
+            uint32_t r[64];
+            LD16(base + 0, (r + 0));
+            LD16(base + 16, (r + 16));
+            LD16(base + 32, (r + 32));
+            LD16(base + 48, (r + 48));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const int px = x0 + tid;
+            if (px < W) {
+                uint4* dst = reinterpret_cast<uint4*>(out + ((size_t)ye * W + px) * kC);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const float lo = fmaxf(__uint_as_float(r[8 * q + 2 * h]), 0.f);
+                        const float hi = fmaxf(__uint_as_float(r[8 * q + 2 * h + 1]), 0.f);
+                        const __nv_bfloat162 v2 = __floats2bfloat162_rn(lo, hi);
+                        pk[h] = *reinterpret_cast<const uint32_t*>(&v2);
+                    }
+                    dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+}
+
+// layer 1: x (fp32, rounded to bf16) -> 64 ch, ReLU, bf16 NHWC.  w1: [9 taps][64 oc] fp32 (bf16 values)
+__global__ void k_conv_first(const float* __restrict__ x, const float* __restrict__ w1, __nv_bfloat16* out, int H,
+                             int W)
+{
+    __shared__ float ws[9 * kC];
+    for (int i = threadIdx.x; i < 9 * kC; i += blockDim.x) ws[i] = w1[i];
+    __syncthreads();
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= H * W) return;
+    const int yy = p / W, xx = p % W;
+    float in[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+        const int sy = yy + t / 3 - 1, sx = xx + t % 3 - 1;
+        in[t] = (sy >= 0 && sy < H && sx >= 0 && sx < W) ? __bfloat162float(__float2bfloat16_rn(x[sy * W + sx])) : 0.f;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(out + (size_t)p * kC);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            float acc[2] = {0.f, 0.f};
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int oc = 8 * q + 2 * h + e;
+#pragma unroll
+                for (int t = 0; t < 9; ++t) acc[e] = fmaf(in[t], ws[t * kC + oc], acc[e]);
+            }
+            const __nv_bfloat162 v2 = __floats2bfloat162_rn(fmaxf(acc[0], 0.f), fmaxf(acc[1], 0.f));
+            pk[h] = *reinterpret_cast<const uint32_t*>(&v2);
+        }
+        dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+}
+
+// layer 17 + residual: out = x - sum_taps sum_ic h[ic] w17[tap][ic]  (fp32)
+__global__ void k_conv_last(const __nv_bfloat16* __restrict__ h, const float* __restrict__ w17,
+                            const float* __restrict__ x, float* out, int H, int W)
+{
+    __shared__ float ws[9 * kC];
+    for (int i = threadIdx.x; i < 9 * kC; i += blockDim.x) ws[i] = w17[i];
+    __syncthreads();
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= H * W) return;
+    const int yy = p / W, xx = p % W;
+    float acc = 0.f;
+    for (int t = 0; t < 9; ++t) {
+        const int sy = yy + t / 3 - 1, sx = xx + t % 3 - 1;
+        if (sy < 0 || sy >= H || sx < 0 || sx >= W) continue;
+        const uint4* src = reinterpret_cast<const uint4*>(h + ((size_t)sy * W + sx) * kC);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint4 v = src[q];
+            const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&u[e]);
+                const float2 f = __bfloat1622float2(b2);
+                acc = fmaf(f.x, ws[t * kC + 8 * q + 2 * e], acc);
+                acc = fmaf(f.y, ws[t * kC + 8 * q + 2 * e + 1], acc);
+            }
+        }
+    }
+    out[p] = x[p] - acc;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn()
+{
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// 4-D view of an NHWC [H][W][64] bf16 image: (ch-in-group 8, x, y, group 8), box {8, 130, 1, 8}
+CUtensorMap make_act_map(void* base, int H, int W)
+{
+    CUtensorMap m;
+    const cuuint64_t dims[4] = {8, (cuuint64_t)W, (cuuint64_t)H, 8};
+    const cuuint64_t strides[3] = {(cuuint64_t)kC * 2, (cuuint64_t)W * kC * 2, 16};  // bytes, dims 1..3
+    const cuuint32_t box[4] = {8, (cuuint32_t)kHaloX, 1, 8};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+}  // namespace
+
+#define CKC(x)                                                                                             \
+    do {                                                                                                   \
+        cudaError_t e_ = (x);                                                                              \
+        if (e_ != cudaSuccess) throw std::runtime_error(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+void Cnn::set_weights(const uint16_t* bf16, int layers, int channels)
+{
+    if (layers != 17 || channels != kC) throw std::runtime_error("the denoiser is 17 layers x 64 channels");
+    // input layout per layer l: PyTorch OIHW [oc][ic][3][3] as bf16 bits
+    const size_t n1 = (size_t)kC * 1 * 9, nm = (size_t)kC * kC * 9, n17 = (size_t)1 * kC * 9;
+    auto f = [](uint16_t b) {
+        uint32_t u = (uint32_t)b << 16;
+        float v;
+        std::memcpy(&v, &u, 4);
+        return v;
+    };
+    std::vector<float> w1(9 * kC), w17(9 * kC);
+    for (int oc = 0; oc < kC; ++oc)
+        for (int t = 0; t < 9; ++t) w1[t * kC + oc] = f(bf16[oc * 9 + t]);
+    const uint16_t* wl = bf16 + n1 + 15 * nm;
+    for (int ic = 0; ic < kC; ++ic)
+        for (int t = 0; t < 9; ++t) w17[t * kC + ic] = f(wl[ic * 9 + t]);
+    // middle layers: [layer][tap][ic-group][oc][8 ic]
+    std::vector<uint16_t> wm(15 * (size_t)9 * kC * kC);
+    for (int l = 0; l < 15; ++l) {
+        const uint16_t* src = bf16 + n1 + l * nm;
+        uint16_t* dst = wm.data() + (size_t)l * 9 * kC * kC;
+        for (int oc = 0; oc < kC; ++oc)
+            for (int ic = 0; ic < kC; ++ic)
+                for (int t = 0; t < 9; ++t)
+                    dst[(size_t)t * kC * kC + (ic / 8) * kC * 8 + oc * 8 + (ic % 8)] = src[(oc * kC + ic) * 9 + t];
+    }
+    (void)n17;
+    w_first.alloc(w1.size());
+    w_last.alloc(w17.size());
+    w_mid.alloc(wm.size());
+    CKC(cudaMemcpy(w_first.p, w1.data(), w1.size() * 4, cudaMemcpyHostToDevice));
+    CKC(cudaMemcpy(w_last.p, w17.data(), w17.size() * 4, cudaMemcpyHostToDevice));
+    CKC(cudaMemcpy(w_mid.p, wm.data(), wm.size() * 2, cudaMemcpyHostToDevice));
+    ready = true;
+}
+
+void Cnn::ensure(int h, int w)
+{
+    if (h == H && w == W && act0.p) return;
+    H = h;
+    W = w;
+    act0.alloc((size_t)H * W * kC);
+    act1.alloc((size_t)H * W * kC);
+    map0 = make_act_map(act0.p, H, W);
+    map1 = make_act_map(act1.p, H, W);
+    CKC(cudaFuncSetAttribute(k_conv64_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+}
+
+void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int num_sms, int* launches)
+{
+    if (!ready) throw std::runtime_error("denoiser weights not set");
+    ensure(h, w);
+    const int npx = H * W;
+    k_conv_first<<<(npx + 255) / 256, 256, 0, s>>>(x, w_first.p, act0.p, H, W);
+    // one CTA per (128-px strip, run of rows); one CTA per SM (140 KB smem)
+    const int strips = (W + kTileX - 1) / kTileX;
+    const int ctas_y = std::max(1, num_sms / strips);
+    const int per = (H + ctas_y - 1) / ctas_y;  // rows per CTA
+    const int ctas = strips * ((H + per - 1) / per);
+    for (int l = 0; l < 15; ++l) {
+        const CUtensorMap& m = (l & 1) ? map1 : map0;
+        __nv_bfloat16* dst = (l & 1) ? act0.p : act1.p;
+        k_conv64_tc<<<ctas, 128, kSmem, s>>>(m, w_mid.p + (size_t)l * 9 * kC * kC, dst, H, W, per);
+    }
+    // 15 middle layers: the last one wrote act1 (l = 14 even -> dst act1)
+    k_conv_last<<<(npx + 255) / 256, 256, 0, s>>>(act1.p, w_last.p, x, out, H, W);
+    CKC(cudaGetLastError());
+    if (launches) *launches += 17;
+}
+
+}  // namespace mace

@@ -1,0 +1,47 @@
+// K5 denoiser host object (see cnn.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+
+namespace mace {
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count)
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = count;
+        if (count && cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) {
+            p = nullptr;
+            n = 0;
+            throw std::runtime_error("cudaMalloc failed (denoiser buffers)");
+        }
+    }
+    ~DevBuf()
+    {
+        if (p) cudaFree(p);
+    }
+};
+
+struct Cnn {
+    bool ready = false;
+    int H = 0, W = 0;
+    DevBuf<float> w_first, w_last;       // [9][64] fp32 holding bf16 values
+    DevBuf<__nv_bfloat16> w_mid;         // [15][9 taps][8 ic-groups][64 oc][8 ic]
+    DevBuf<__nv_bfloat16> act0, act1;    // NHWC [H][W][64]
+    CUtensorMap map0{}, map1{};
+    // weights: 17 layers in PyTorch OIHW order, bf16 bits, concatenated
+    void set_weights(const uint16_t* bf16, int layers, int channels);
+    void ensure(int h, int w);
+    // out = x - net(x) for an h x w fp32 image (device pointers), on stream s
+    void apply(const float* x, float* out, int h, int w, cudaStream_t s, int num_sms, int* launches);
+};
+
+}  // namespace mace

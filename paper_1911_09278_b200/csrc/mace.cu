@@ -22,6 +22,7 @@
 #include "kernels.cuh"
 #include "k_sv.cuh"
 #include "k_sweep64.cuh"
+#include "cnn.cuh"
 #include "mace_b200.h"
 
 namespace mace {
@@ -117,6 +118,8 @@ struct Ctx {
     int num_sms = 148;
     // timing of the last iterate call
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // K5 PnP denoiser (cnn.cu)
+    Cnn cnn;
     // optional per-launch timing of K2 (bench roofline): event pairs on the launch stream
     bool time_k2 = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k2ev;
@@ -1191,6 +1194,42 @@ int mace_sv_layout_probe(int n_side, int n_ch, int n_views, const int64_t* row_p
     stats[3] = L.n_sv;
     stats[4] = L.duplicates;
     stats[5] = k;
+    API_END
+}
+
+// ------------------------------------------------------------------ K5 PnP denoiser (cnn.cu)
+int mace_cnn_set_weights(void* p, const uint16_t* bf16, int layers, int channels)
+{
+    API_BEGIN
+    C(p)->cnn.set_weights(bf16, layers, channels);
+    API_END
+}
+
+// g = H(wbar) on the device (the denoiser agent inside consensus_GH, mace.py:105-108)
+int mace_cnn_apply(void* p)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    c->cnn.apply(c->wbar.p, c->g.p, c->n_side, c->n_side, c->stream, c->num_sms, nullptr);
+    API_END
+}
+
+// standalone: out = H(x) for an h x w image (host pointers); ms_out = device time of the 17 layers
+int mace_cnn_run(void* p, const float* x, float* out, int h, int w, float* ms_out)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    DBuf<float> dx, dy;
+    dx.alloc((size_t)h * w);
+    dy.alloc((size_t)h * w);
+    CK(cudaMemcpyAsync(dx.p, x, sizeof(float) * h * w, cudaMemcpyHostToDevice, c->stream));
+    c->cnn.ensure(h, w);
+    CK(cudaEventRecord(c->ev0, c->stream));
+    c->cnn.apply(dx.p, dy.p, h, w, c->stream, c->num_sms, nullptr);
+    CK(cudaEventRecord(c->ev1, c->stream));
+    CK(cudaMemcpyAsync(out, dy.p, sizeof(float) * h * w, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (ms_out) CK(cudaEventElapsedTime(ms_out, c->ev0, c->ev1));
     API_END
 }
 

@@ -44,3 +44,84 @@ def make_denoiser(spec: DenoiserSpec, n_side: int):
 
 def denoise(spec: DenoiserSpec, v, n_side: int):
     return make_denoiser(spec, n_side)(v)
+
+
+# --------------------------------------------------------------------------- K5: CNN denoiser agent
+
+CNN_LAYERS, CNN_CHANNELS = 17, 64
+
+
+def to_bf16_bits(a) -> np.ndarray:
+    """float32 -> bf16 bit patterns, round to nearest even."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    return u.astype(np.uint16)
+
+
+def from_bf16_bits(b) -> np.ndarray:
+    return (np.asarray(b, np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def cnn_weights(seed: int = 0, scale: float = 0.1) -> list:
+    """BASELINE config 3: 17 bias-free 3x3 conv layers (1->64, 15x 64->64, 64->1), He-normal
+    from `seed` times `scale`, stored as bf16 (returned as float32 arrays holding bf16 values,
+    PyTorch OIHW shapes)."""
+    rng = np.random.default_rng(seed)
+    shapes = [(CNN_CHANNELS, 1)] + [(CNN_CHANNELS, CNN_CHANNELS)] * 15 + [(1, CNN_CHANNELS)]
+    out = []
+    for oc, ic in shapes:
+        std = np.sqrt(2.0 / (ic * 9)) * scale
+        w = (rng.standard_normal((oc, ic, 3, 3)) * std).astype(np.float32)
+        out.append(from_bf16_bits(to_bf16_bits(w)).reshape(oc, ic, 3, 3))
+    return out
+
+
+class CnnDenoiser:
+    """H(v) = v - net(v) with the 17-layer CNN on the tensor cores (kernel K5).
+
+    Usable as a plain callable (host round trip) or, inside ``mace_pnp_solve``, on the
+    device: ``device_apply(plan)`` maps the consensus average to G_H without leaving HBM.
+    """
+
+    def __init__(self, n_side: int, weights=None, seed: int = 0, device: int = 0):
+        self.n_side = n_side
+        self.weights = cnn_weights(seed) if weights is None else [np.asarray(w, np.float32) for w in weights]
+        if len(self.weights) != CNN_LAYERS:
+            raise ValueError("the denoiser has 17 layers")
+        self._bits = np.concatenate([to_bf16_bits(w).ravel() for w in self.weights])
+        self.device = device
+        self._ctx = None
+        self._loaded = set()
+        self.last_ms = None
+
+    def _load(self, ctx):
+        from . import _native as N
+
+        key = id(ctx) if not hasattr(ctx, "h") else ctx.h.value
+        if key not in self._loaded:
+            ctx.call("mace_cnn_set_weights", N.ptr(self._bits), CNN_LAYERS, CNN_CHANNELS)
+            self._loaded.add(key)
+
+    def device_apply(self, plan):
+        self._load(plan)
+        plan.call("mace_cnn_apply")
+
+    def __call__(self, v):
+        import ctypes
+
+        from . import _native as N
+        from .engine import _Context
+
+        if self._ctx is None:
+            self._ctx = _Context(self.device)
+        self._load(self._ctx)
+        x = N.f32(np.asarray(v).reshape(-1))
+        h = self.n_side
+        w = x.shape[0] // h
+        if h * w != x.shape[0]:
+            raise ValueError("image size does not match n_side")
+        out = np.empty_like(x)
+        ms = ctypes.c_float(0.0)
+        self._ctx.call("mace_cnn_run", N.ptr(x), N.ptr(out), int(h), int(w), ctypes.byref(ms))
+        self.last_ms = ms.value
+        return out.astype(np.float64)
