@@ -26,29 +26,63 @@ def rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - b) / np.linalg.norm(b))
 
 
+def _net(x, out):
+    """net(x) = x32 - H(x): the GPU applies the residual to the fp32 input."""
+    return np.asarray(x, np.float32).astype(np.float64) - out
+
+
 @pytest.mark.parametrize("n_side,seed", [(64, 0), (512, 1), (200, 2), (130, 3)])
 def test_cnn_matches_cpu_oracle(n_side, seed):
+    """He-normal weights at unit scale so every layer's activations are O(1) and the
+    residual net(x) is O(x): a wrong descriptor, tap or channel mapping cannot hide."""
     rng = np.random.default_rng(seed)
-    x = 0.02 + 0.01 * rng.standard_normal(n_side * n_side)
-    w = cnn_weights(seed)
+    x = rng.random(n_side * n_side)
+    w = cnn_weights(seed, scale=1.0)
     H = CnnDenoiser(n_side, weights=w)
     out = H(x)
-    ref = cnn_apply(x, w, n_side)
-    assert rel(x - out, x - ref) < 2e-2, rel(x - out, x - ref)
-    assert rel(out, ref) < 1e-4
-    print(f"n={n_side}: K5 {H.last_ms:.3f} ms, residual rel err {rel(x - out, x - ref):.2e}")
+    ref = cnn_apply(np.asarray(x, np.float32), w, n_side)
+    r_gpu, r_ref = _net(x, out), np.asarray(x, np.float32) - ref
+    assert rel(r_ref, x) > 0.05
+    print(f"n={n_side}: K5 {H.last_ms:.3f} ms, net rel err {rel(r_gpu, r_ref):.2e}, "
+          f"max abs {np.max(np.abs(r_gpu - r_ref)):.2e} of max {np.max(np.abs(r_ref)):.2e}")
+    # bf16 activations: fp32 sums that straddle a rounding boundary land one bf16 ulp apart,
+    # and such differences compound over 17 random layers -> a few percent, not a bug signal
+    # (the exact-arithmetic test below pins the tap / channel / padding mapping bit for bit)
+    assert rel(r_gpu, r_ref) < 4e-2, rel(r_gpu, r_ref)
 
 
-def test_cnn_non_trivial_weights():
-    """Unit-scale weights (no 0.1 factor): the net output is O(x), so the check is not vacuous."""
-    n = 128
-    rng = np.random.default_rng(7)
-    x = rng.random(n * n)
-    w = cnn_weights(5, scale=1.0)
-    out = CnnDenoiser(n, weights=w)(x)
-    ref = cnn_apply(x, w, n)
-    assert rel(x - ref, x) > 0.05
-    assert rel(x - out, x - ref) < 2e-2
+@pytest.mark.parametrize("n_side,seed", [(64, 11), (200, 12), (512, 13)])
+def test_cnn_exact_taps_channels_padding(n_side, seed):
+    """Every middle layer is a single 3x3 tap and a channel permutation (one nonzero product per
+    output), so both sides compute exactly: the GPU must reproduce the oracle bit for bit,
+    which pins the UMMA descriptors (tap shift, channel groups), the TMA zero padding and the
+    TMEM -> NHWC epilogue."""
+    rng = np.random.default_rng(seed)
+    C = 64
+    w = [np.zeros((C, 1, 3, 3), np.float32)]
+    w[0][:, 0, 1, 1] = rng.choice([0.5, 1.0, 2.0], C)  # layer 1: scaled copies of x
+    for _ in range(15):
+        m = np.zeros((C, C, 3, 3), np.float32)
+        t = rng.integers(9)
+        perm = rng.permutation(C)
+        m[np.arange(C), perm, t // 3, t % 3] = rng.choice([0.5, 1.0, 2.0], C)
+        w.append(m)
+    last = np.zeros((1, C, 3, 3), np.float32)
+    last[0, rng.integers(C), 1, 1] = 1.0
+    w.append(last)
+    x = rng.integers(0, 256, n_side * n_side).astype(np.float64) / 256.0
+    out = CnnDenoiser(n_side, weights=w)(x)
+    ref = cnn_apply(np.asarray(x, np.float32), w, n_side)
+    assert np.array_equal(np.asarray(out, np.float32), np.asarray(ref, np.float32))
+
+
+def test_cnn_config3_weights_run():
+    """The literal BASELINE config-3 weights (He-normal x 0.1 per layer) shrink the residual
+    by ~0.1 per layer, so H is the identity to fp32 precision: check exactly that."""
+    n = 512
+    x = np.random.default_rng(9).random(n * n) * 0.03
+    out = CnnDenoiser(n, weights=cnn_weights(0))(x)
+    assert np.allclose(out, np.asarray(x, np.float32), rtol=1e-6, atol=0)
 
 
 def test_mace_pnp_with_cnn_denoiser_vs_oracle_loop():
@@ -60,7 +94,7 @@ def test_mace_pnp_with_cnn_denoiser_vs_oracle_loop():
     ph = gen.ellipse_phantom(ns, pitch, 10, seed=0)
     y, lam = gen.poisson_sinogram(gen.host_forward_project(mats, ph), 1e4, seed=1)
     prob = mb.ReconProblem(geom, mats, y, lam, mb.PriorParams("qggmrf", 25.0, 2.0, 1.2, 1.0, 0.01))
-    w = cnn_weights(3)
+    w = cnn_weights(3, scale=0.5)
     H = CnnDenoiser(ns, weights=w)
     sigma, iters = 2e-4, 20
     cfg = mb.MaceConfig(n_subsets=N, rho=0.8, sigma=sigma, mode="pnp", denoiser=mb.DenoiserSpec("identity"),
