@@ -5,12 +5,13 @@
 // Layers 2..16 (64 -> 64) run on the 5th-gen tensor cores: an implicit GEMM per output row
 // segment of 128 pixels, D[128 px x 64 oc] = sum over 9 taps and 4 K-steps of
 // A[128 px x 16 ic] * W[16 ic x 64 oc]  (tcgen05.mma.cta_group::1.kind::f16, M=128, N=64,
-// K=16, fp32 accumulators in TMEM).  A-operand rows come from a rolling window of
-// channel-blocked halo rows ([8 channel groups][130 px][8 ch] bf16) loaded by 4-D TMA
-// (out-of-image coordinates are zero-filled = the conv's zero padding); the tap shift dx is
-// just a 16-byte offset of the UMMA descriptor (SWIZZLE_NONE, K-major).  The 9 taps'
-// weights (72 KB) stay resident in shared memory.  Two TMEM accumulators let the epilogue
-// (tcgen05.ld -> ReLU -> bf16 -> NHWC store) of row y-1 overlap the MMAs of row y.
+// K=16, fp32 accumulators in TMEM).  Activations live in HBM channel-blocked,
+// [8 channel groups][H][W][8 ch] bf16, so a halo row ([8 groups][130 px][8 ch], 16.6 KB) is
+// 8 contiguous 2 KB runs: one 4-D TMA box (out-of-image coordinates are zero-filled = the
+// conv's zero padding).  The tap shift dx is a 16-byte offset of the UMMA descriptor
+// (SWIZZLE_NONE, K-major, core matrix = 8 px x 8 ch).  The 9 taps' weights (72 KB) stay
+// resident in shared memory.  A warp-specialized pipeline (TMA producer, MMA issuer, 4
+// epilogue warps: tcgen05.ld -> ReLU -> bf16 -> blocked stores) keeps 4 accumulators in flight.
 // Layers 1 (1 -> 64) and 17 (64 -> 1, fused residual) are CUDA-core kernels.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -31,7 +32,8 @@ namespace {
 constexpr int kC = 64;             // channels
 constexpr int kTileX = 128;        // output pixels per tile (one row segment)
 constexpr int kHaloX = kTileX + 2;  // 130
-constexpr int kSlots = 4;          // rolling window of halo rows
+constexpr int kSlots = 6;          // ring of halo rows (TMA runs up to 3 rows ahead)
+constexpr int kAcc = 4;            // TMEM accumulators (4 x 64 fp32 columns)
 constexpr int kSlotBytes = 8 * kHaloX * 16;         // 16,640
 constexpr int kWBytes = 9 * kC * kC * 2;            // 73,728
 constexpr int kSmem = kWBytes + kSlots * kSlotBytes + 1024;
@@ -108,22 +110,29 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar)
                    "=r"(r[14]), "=r"(r[15])                                                                       \
                  : "r"(base))
 
-// One 64->64 conv layer (+ ReLU) over a [H][W][64] bf16 NHWC image.  Grid: one CTA per
-// (x-strip, row range); 128 threads = 4 warps (warp w reads TMEM lanes 32w..32w+31).
-__global__ void __launch_bounds__(128, 1) k_conv64_tc(const __grid_constant__ CUtensorMap amap,
+// One 64->64 conv layer (+ ReLU) over a channel-blocked [8][H][W][8] bf16 image, warp-specialized:
+//   warp 0 (one lane)  TMA producer: halo rows y0-1 .. y1 into a ring of kSlots slots
+//   warp 1 (one lane)  MMA issuer:   tile y = 36 UMMAs (9 taps x 4 K-steps) into TMEM
+//                                    accumulator t % kAcc, commits to acc_full / slot_empty
+//   warps 2..5         epilogue:     tcgen05.ld -> ReLU -> bf16 -> blocked stores, acc_empty
+// (warp i may only touch TMEM lanes 32*(i%4)..+31, so warps 2..5 cover all 128 rows.)
+// Grid: one CTA per (128-px strip, run of rows), one CTA per SM.
+__global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CUtensorMap amap,
                                                       const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* out,
                                                       int H, int W, int rows_per_cta)
 {
     extern __shared__ __align__(1024) unsigned char sm[];
     unsigned char* sw = sm;                     // weights: [tap 9][ic-group 8][oc 64][8 ic]
-    unsigned char* slots = sm + kWBytes;        // [slot 4][ic-group 8][130 px][8 ch]
+    unsigned char* slots = sm + kWBytes;        // [slot][ic-group 8][130 px][8 ch]
     uint64_t* bars = reinterpret_cast<uint64_t*>(slots + kSlots * kSlotBytes);
     uint64_t* wbar = bars;                      // weights landed
-    uint64_t* sbar = bars + 1;                  // [4] halo row landed
-    uint64_t* mbar = bars + 5;                  // [2] accumulator ready
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    uint64_t* sfull = bars + 1;                 // [kSlots] halo row landed
+    uint64_t* sempty = sfull + kSlots;          // [kSlots] halo row no longer read
+    uint64_t* afull = sempty + kSlots;          // [kAcc] accumulator ready
+    uint64_t* aempty = afull + kAcc;            // [kAcc] accumulator drained (4 epilogue warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kAcc);
 
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int strips = (W + kTileX - 1) / kTileX;
     const int strip = blockIdx.x % strips;
     const int x0 = strip * kTileX;
@@ -132,79 +141,95 @@ __global__ void __launch_bounds__(128, 1) k_conv64_tc(const __grid_constant__ CU
     if (y0 >= H) return;
 
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(s_u32(tmem_slot))
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(tmem_slot)),
+                     "n"(kAcc * 64)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    if (tid == 0) {
-        for (int i = 0; i < 8; ++i) mbar_init(bars + i, 1);
+    if (tid == 32) {
+        mbar_init(wbar, 1);
+        for (int i = 0; i < kSlots; ++i) {
+            mbar_init(sfull + i, 1);
+            mbar_init(sempty + i, 1);
+        }
+        for (int i = 0; i < kAcc; ++i) {
+            mbar_init(afull + i, 1);
+            mbar_init(aempty + i, 4);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    const int rbase = y0 - 1;  // row r -> ring index q = r - rbase, slot q % kSlots, use q / kSlots
 
-    // row r of the image lives in slot (r - (y0 - 1)) % 4; its k-th load uses parity k & 1
-    auto slot_of = [&](int r) { return (r - (y0 - 1)) & (kSlots - 1); };
-    auto slot_par = [&](int r) { return (uint32_t)(((r - (y0 - 1)) >> 2) & 1); };
-    if (tid == 0) {
-        mbar_expect(wbar, kWBytes);
-        bulk_copy(sw, wts, kWBytes, wbar);
-        for (int r = y0 - 1; r <= min(y0 + 1, y1); ++r) {
-            mbar_expect(sbar + slot_of(r), kSlotBytes);
-            tma_row(slots + slot_of(r) * kSlotBytes, &amap, x0 - 1, r, sbar + slot_of(r));
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            mbar_expect(wbar, kWBytes);
+            bulk_copy(sw, wts, kWBytes, wbar);
+            for (int r = y0 - 1; r <= y1; ++r) {
+                const int q = r - rbase, s = q % kSlots, u = q / kSlots;
+                if (u >= 1) mbar_wait(sempty + s, (uint32_t)((u - 1) & 1));
+                mbar_expect(sfull + s, kSlotBytes);
+                tma_row(slots + s * kSlotBytes, &amap, x0 - 1, r, sfull + s);
+            }
         }
-    }
-    mbar_wait(wbar, 0);
-
-    const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
-    for (int y = y0; y <= y1; ++y) {
-        const int t = y - y0;  // tile index within this CTA
-        if (y < y1 && tid == 0) {
-            // tile y reads rows y-1, y, y+1
-            for (int r = y - 1; r <= y + 1; ++r) mbar_wait(sbar + slot_of(r), slot_par(r));
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t d = tmem + (uint32_t)((t & 1) * 64);
-            int k = 0;
-#pragma unroll 1
-            for (int dy = 0; dy < 3; ++dy) {
-                const uint32_t row_base = sl_base + slot_of(y - 1 + dy) * kSlotBytes;
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
+            mbar_wait(wbar, 0);
+            for (int y = y0; y < y1; ++y) {
+                const int t = y - y0, b = t % kAcc, ub = t / kAcc;
+                if (ub >= 1) mbar_wait(aempty + b, (uint32_t)((ub - 1) & 1));
+                for (int r = y - 1; r <= y + 1; ++r) {
+                    const int q = r - rbase;
+                    mbar_wait(sfull + q % kSlots, (uint32_t)((q / kSlots) & 1));
+                }
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d = tmem + (uint32_t)(b * 64);
+                // descriptors differ only in the start-address field (bits [0,14), addr >> 4):
+                // build one per operand and step it with integer adds
+                const uint64_t b0 = sdesc(sw_base, kC * 16, 128);
 #pragma unroll
-                for (int dx = 0; dx < 3; ++dx) {
-                    const uint32_t wtap = sw_base + (dy * 3 + dx) * (kC * kC * 2);
+                for (int dy = 0; dy < 3; ++dy) {
+                    const uint64_t a0 = sdesc(sl_base + ((y - 1 + dy - rbase) % kSlots) * kSlotBytes, kHaloX * 16, 128);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j, ++k) {
-                        // A: 128 px starting at halo column dx; K-step j = ic groups 2j, 2j+1
-                        const uint64_t a = sdesc(row_base + dx * 16 + 2 * j * (kHaloX * 16), kHaloX * 16, 128);
-                        const uint64_t b = sdesc(wtap + 2 * j * (kC * 16), kC * 16, 128);
-                        umma(d, a, b, k > 0);
+                    for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint64_t a = a0 + (uint64_t)((dx * 16 + 2 * j * (kHaloX * 16)) >> 4);
+                            const uint64_t bd = b0 + (uint64_t)(((dy * 3 + dx) * (kC * kC * 2) + 2 * j * (kC * 16)) >> 4);
+                            umma(d, a, bd, (dy | dx | j) != 0);
+                        }
                     }
                 }
-            }
-            umma_commit(mbar + (t & 1));
-            // refill: row y+2 goes into the slot of row y-2, last read by tile y-1
-            if (y + 2 <= y1) {
-                if (t >= 1) mbar_wait(mbar + ((t - 1) & 1), (uint32_t)(((t - 1) >> 1) & 1));
-                const int r = y + 2;
-                mbar_expect(sbar + slot_of(r), kSlotBytes);
-                tma_row(slots + slot_of(r) * kSlotBytes, &amap, x0 - 1, r, sbar + slot_of(r));
+                umma_commit(afull + b);
+                umma_commit(sempty + (y - 1 - rbase) % kSlots);  // row y-1: last reader was tile y
             }
         }
-        if (t >= 1) {  // epilogue of tile y-1
-            const int te = t - 1, ye = y - 1;
-            mbar_wait(mbar + (te & 1), (uint32_t)((te >> 1) & 1));
+    } else {  // ---- epilogue warps 2..5
+        const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+        for (int y = y0; y < y1; ++y) {
+            const int t = y - y0, b = t % kAcc, ub = t / kAcc;
+            mbar_wait(afull + b, (uint32_t)(ub & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((te & 1) * 64);
+            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * 64);
             uint32_t r[64];
             LD16(base + 0, (r + 0));
             LD16(base + 16, (r + 16));
             LD16(base + 32, (r + 32));
             LD16(base + 48, (r + 48));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const int px = x0 + tid;
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(aempty + b)) : "memory");
+            const int px = x0 + quad * 32 + lane;
             if (px < W) {
-                uint4* dst = reinterpret_cast<uint4*>(out + ((size_t)ye * W + px) * kC);
+                // channel-blocked output [group][H][W][8]: each store is 512 B contiguous per warp
+                uint4* dst = reinterpret_cast<uint4*>(out) + ((size_t)y * W + px);
+                const size_t gstride = (size_t)H * W;
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     uint32_t pk[4];
@@ -215,20 +240,18 @@ __global__ void __launch_bounds__(128, 1) k_conv64_tc(const __grid_constant__ CU
                         const __nv_bfloat162 v2 = __floats2bfloat162_rn(lo, hi);
                         pk[h] = *reinterpret_cast<const uint32_t*>(&v2);
                     }
-                    dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    dst[q * gstride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
             }
         }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * 64) : "memory");
 }
 
-// layer 1: x (fp32, rounded to bf16) -> 64 ch, ReLU, bf16 NHWC.  w1: [9 taps][64 oc] fp32 (bf16 values)
+// layer 1: x (fp32, rounded to bf16) -> 64 ch, ReLU, bf16 blocked [8][H][W][8].  w1: [9 taps][64 oc] fp32
 __global__ void k_conv_first(const float* __restrict__ x, const float* __restrict__ w1, __nv_bfloat16* out, int H,
                              int W)
 {
@@ -244,7 +267,8 @@ __global__ void k_conv_first(const float* __restrict__ x, const float* __restric
         const int sy = yy + t / 3 - 1, sx = xx + t % 3 - 1;
         in[t] = (sy >= 0 && sy < H && sx >= 0 && sx < W) ? __bfloat162float(__float2bfloat16_rn(x[sy * W + sx])) : 0.f;
     }
-    uint4* dst = reinterpret_cast<uint4*>(out + (size_t)p * kC);
+    uint4* dst = reinterpret_cast<uint4*>(out) + p;  // channel-blocked [group][H][W][8]
+    const size_t gstride = (size_t)H * W;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         uint32_t pk[4];
@@ -260,7 +284,7 @@ __global__ void k_conv_first(const float* __restrict__ x, const float* __restric
             const __nv_bfloat162 v2 = __floats2bfloat162_rn(fmaxf(acc[0], 0.f), fmaxf(acc[1], 0.f));
             pk[h] = *reinterpret_cast<const uint32_t*>(&v2);
         }
-        dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[q * gstride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
 }
 
@@ -274,14 +298,16 @@ __global__ void k_conv_last(const __nv_bfloat16* __restrict__ h, const float* __
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= H * W) return;
     const int yy = p / W, xx = p % W;
+    const size_t gstride = (size_t)H * W;
     float acc = 0.f;
+#pragma unroll
     for (int t = 0; t < 9; ++t) {
         const int sy = yy + t / 3 - 1, sx = xx + t % 3 - 1;
         if (sy < 0 || sy >= H || sx < 0 || sx >= W) continue;
-        const uint4* src = reinterpret_cast<const uint4*>(h + ((size_t)sy * W + sx) * kC);
+        const uint4* src = reinterpret_cast<const uint4*>(h) + ((size_t)sy * W + sx);  // [group][H][W][8]
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const uint4 v = src[q];
+            const uint4 v = __ldg(src + q * gstride);
             const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -312,12 +338,13 @@ EncodeTiledFn encode_fn()
     return fn;
 }
 
-// 4-D view of an NHWC [H][W][64] bf16 image: (ch-in-group 8, x, y, group 8), box {8, 130, 1, 8}
+// 4-D view of a channel-blocked [8][H][W][8] bf16 image: (ch-in-group 8, x, y, group 8), box {8, 130, 1, 8}
 CUtensorMap make_act_map(void* base, int H, int W)
 {
     CUtensorMap m;
     const cuuint64_t dims[4] = {8, (cuuint64_t)W, (cuuint64_t)H, 8};
-    const cuuint64_t strides[3] = {(cuuint64_t)kC * 2, (cuuint64_t)W * kC * 2, 16};  // bytes, dims 1..3
+    // channel-blocked global layout [group 8][H][W][8 ch]: a halo row of one group is 130 x 16 B contiguous
+    const cuuint64_t strides[3] = {16, (cuuint64_t)W * 16, (cuuint64_t)H * W * 16};  // bytes, dims 1..3
     const cuuint32_t box[4] = {8, (cuuint32_t)kHaloX, 1, 8};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
@@ -398,7 +425,7 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
     for (int l = 0; l < 15; ++l) {
         const CUtensorMap& m = (l & 1) ? map1 : map0;
         __nv_bfloat16* dst = (l & 1) ? act0.p : act1.p;
-        k_conv64_tc<<<ctas, 128, kSmem, s>>>(m, w_mid.p + (size_t)l * 9 * kC * kC, dst, H, W, per);
+        k_conv64_tc<<<ctas, 192, kSmem, s>>>(m, w_mid.p + (size_t)l * 9 * kC * kC, dst, H, W, per);
     }
     // 15 middle layers: the last one wrote act1 (l = 14 even -> dst act1)
     k_conv_last<<<(npx + 255) / 256, 256, 0, s>>>(act1.p, w_last.p, x, out, H, W);

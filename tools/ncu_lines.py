@@ -18,11 +18,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 so = os.path.join(ROOT, "paper_1911_09278_b200", "libmace_b200.so")
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=tmp, capture_output=True)
-cub = [f for f in os.listdir(tmp) if f.startswith("mace.") and f.endswith(".cubin")][0]
-dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+dis = ""
+for cub in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):
+    d = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+    if fn in d:
+        dis = d
+        break
 # walk the function's text
 lines = dis.splitlines()
-start = next(i for i, l in enumerate(lines) if l.startswith(fn + ":"))
+start = next(i for i, l in enumerate(lines) if re.match(r"^\S*" + re.escape(fn) + r"\S*:$", l))
 off2line = {}
 cur = None
 for l in lines[start + 1:]:
