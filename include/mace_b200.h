@@ -69,9 +69,11 @@ int mace_load_matrix(void* ctx, int n_side, int n_views, int n_ch, const int64_t
                      const float* vals);
 /* kind 0 = quadratic-mrf, 1 = qggmrf */
 int mace_set_prior(void* ctx, int kind, double p, double q, double T, double sigma_x, double eps_reg);
-/* n_local agents, agent a owns views[sum(view_counts[:a]) ...]; schedule 0 = super-voxel, 1 = raster */
-int mace_setup_agents(void* ctx, int n_local, const int* view_counts, const int* views, int schedule, int sv_side,
-                      int colours, int n_threads);
+/* n_agents agents, agent a owns views[sum(view_counts[:a]) ...]; schedule 0 = super-voxel, 1 = raster.
+ * n_slices > 1 batches independent slices that share the operator (config 4): local agent
+ * index = slice * n_agents + agent; y/weights, images and stacks gain a leading slice axis. */
+int mace_setup_agents(void* ctx, int n_agents, const int* view_counts, const int* views, int schedule, int sv_side,
+                      int colours, int n_threads, int n_slices);
 /* super-voxel schedule: at most `concurrency` x (tiles in the pass) tiles in flight (>= 1 per agent);
  * max_warps > 0 caps the number of resident warps */
 int mace_set_schedule(void* ctx, double concurrency, int64_t max_warps);

@@ -37,7 +37,7 @@ _SIGS = {
     "mace_agent_info": (c_int, [P, c_int, P]),
     "mace_load_matrix": (c_int, [P, c_int, c_int, c_int, P, P, P]),
     "mace_set_prior": (c_int, [P, c_int, c_double, c_double, c_double, c_double, c_double]),
-    "mace_setup_agents": (c_int, [P, c_int, P, P, c_int, c_int, c_int, c_int]),
+    "mace_setup_agents": (c_int, [P, c_int, P, P, c_int, c_int, c_int, c_int, c_int]),
     "mace_set_schedule": (c_int, [P, c_double, c_int64]),
     "mace_set_agent_params": (c_int, [P, c_int, c_double, c_double, c_int]),
     "mace_load_data": (c_int, [P, P, P]),

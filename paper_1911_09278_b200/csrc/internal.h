@@ -60,9 +60,9 @@ void build_agent_csc(int n_side, int n_ch, const int64_t* row_ptr, const int32_t
                      const std::vector<int>& views, AgentCSC& out);
 void build_raster_layout(const AgentCSC& csc, int n, RasterLayout& out);
 void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int n_views_agent, int svs, SVLayout& out);
-// Queue of (agent << 24 | sv) items: colour classes (sv_row mod C, sv_col mod C) in
+// Queue of (agent << 22 | sv) items: colour classes (sv_row mod C, sv_col mod C) in
 // order, SVs of a class in raster order, agents interleaved within a position.
-std::vector<uint32_t> build_queue(int n_agents, int n_sv_side, int colours);
+std::vector<uint32_t> build_queue(int n_agents, int n_sv_side, int colours, int n_slices = 1);
 
 void set_error(const std::string& msg);
 

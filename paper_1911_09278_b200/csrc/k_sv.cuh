@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(128, 4) k_icd_sv(PassParams P)
         item = __shfl_sync(FULL, item, 0);
         if (item >= (unsigned)P.n_items) break;
         const uint32_t code = __ldg(P.queue + item);
-        const AgentDev& A = P.agents[code >> 24];
-        const int sv = (int)(code & 0xffffffu);
+        const AgentDev& A = P.agents[code >> kAgentShift];
+        const int sv = (int)(code & kSvMask);
         float2* __restrict__ el = A.el;
         float* __restrict__ z = A.z;
         float* __restrict__ w = A.w;
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(128, 4) k_icd_sv(PassParams P)
                     sth[i] = A.th[s];
                     const float wo = w[s];
                     swo[i] = wo;
-                    svv[i] = P.mode ? 2.f * __ldg(P.g + s) - wo : A.vt[s];
+                    svv[i] = P.mode ? 2.f * __ldg(P.g + (size_t)A.slice * n * n + s) - wo : A.vt[s];
                 } else {
                     sth[i] = 0.f;
                     svv[i] = 0.f;

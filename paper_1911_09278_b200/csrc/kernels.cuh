@@ -16,6 +16,9 @@
 namespace mace {
 
 constexpr unsigned FULL = 0xffffffffu;
+// work-queue item = (local agent << kAgentShift) | super-voxel index (layout.cpp build_queue)
+constexpr int kAgentShift = 22;
+constexpr uint32_t kSvMask = (1u << kAgentShift) - 1;
 
 struct PriorC {
     int kind;  // 0 quadratic-mrf, 1 qggmrf  (models.py:43-44)
@@ -38,6 +41,7 @@ struct AgentDev {
     float* w;          // [n] stack component w_i
     float* th;         // [n] theta2 data term, sum a^2 lambda (icd.py:193-195)
     float* vt;         // [n] explicit proximal target (plain passes)
+    int slice;         // slice of a multi-slice batch (config 4); consensus images are [slice][n]
     const int* views;  // [V] global view index of local view j
     // super-voxel layout
     const int2* band;   // [n_sv * V]
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(32) k_icd_raster(PassParams P, int agent_base)
             g += __shfl_xor_sync(FULL, g, o);
             c += __shfl_xor_sync(FULL, c, o);
         }
-        const float v = P.mode ? 2.f * P.g[s] - A.w[s] : A.vt[s];
+        const float v = P.mode ? 2.f * P.g[(size_t)A.slice * N + s] - A.w[s] : A.vt[s];
         float alpha;
         if (pixel_step(t, g, c, zs, v, A.th[s], beta, inv_s2, A.clamp, PR, alpha)) {
             if (lane == 0) {
@@ -244,7 +248,7 @@ __global__ void __launch_bounds__(32) k_icd_raster(PassParams P, int agent_base)
         for (size_t s = lane; s < N; s += 32) {
             const float zn = __ldcg(z + s);
             const float wo = A.w[s];
-            const float v = 2.f * P.g[s] - wo;
+            const float v = 2.f * P.g[(size_t)A.slice * N + s] - wo;
             const float wn = P.rho * (2.f * zn - v) + (1.f - P.rho) * wo;
             A.w[s] = wn;
             const double dd = (double)wn - (double)wo;
@@ -277,6 +281,18 @@ struct FPParams {
     int n_ch;
 };
 
+// agent owning concatenated row `wr`: last a with row_base[a] <= wr (row_base ascending)
+__device__ __forceinline__ int agent_of_row(const int* row_base, int n_agents, int wr)
+{
+    int lo = 0, hi = n_agents - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (row_base[mid] <= wr) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
 __global__ void k_fp_agents(FPParams F, const AgentDev* agents, const int* row_base, int n_agents,
                             int total_rows, const int* done)
 {
@@ -285,8 +301,7 @@ __global__ void k_fp_agents(FPParams F, const AgentDev* agents, const int* row_b
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     for (int wr = gw; wr < total_rows; wr += nw) {
-        int a = 0;
-        while (a + 1 < n_agents && row_base[a + 1] <= wr) ++a;
+        const int a = agent_of_row(row_base, n_agents, wr);
         const AgentDev& A = agents[a];
         const int r = wr - row_base[a];
         if (r >= A.R) continue;  // alignment padding between agents
@@ -401,8 +416,8 @@ __global__ void __launch_bounds__(128) k_theta2_sv(const AgentDev* agents, int n
     const int SS = S * S;
     for (int item = gw; item < n_items; item += nw) {
         const uint32_t code = queue[item];
-        const AgentDev& A = agents[code >> 24];
-        const int sv = (int)(code & 0xffffffu);
+        const AgentDev& A = agents[code >> kAgentShift];
+        const int sv = (int)(code & kSvMask);
         const int r0 = (sv / A.n_sv_side) * S, c0 = (sv % A.n_sv_side) * S;
         const int2* bt = A.band + (size_t)sv * A.V;
         for (int j = lane >> 4; j < A.V; j += 2) {
@@ -430,15 +445,14 @@ __global__ void __launch_bounds__(128) k_theta2_sv(const AgentDev* agents, int n
 
 // agent rows <- global y / lambda (local row r = j n_ch + c, icd.py:187-188)
 __global__ void k_gather_data(const AgentDev* agents, const int* row_base, int n_agents, int total_rows, int n_ch,
-                              const float* y, const float* lam)
+                              const float* y, const float* lam, int64_t slice_rows)
 {
     for (int wr = blockIdx.x * blockDim.x + threadIdx.x; wr < total_rows; wr += gridDim.x * blockDim.x) {
-        int a = 0;
-        while (a + 1 < n_agents && row_base[a + 1] <= wr) ++a;
+        const int a = agent_of_row(row_base, n_agents, wr);
         const AgentDev& A = agents[a];
         const int r = wr - row_base[a];
         if (r >= A.R) continue;
-        const int64_t g = (int64_t)A.views[r / n_ch] * n_ch + r % n_ch;
+        const int64_t g = (int64_t)A.slice * slice_rows + (int64_t)A.views[r / n_ch] * n_ch + r % n_ch;
         A.y[r] = y[g];
         A.el[r].y = lam[g];
     }
@@ -447,15 +461,19 @@ __global__ void k_gather_data(const AgentDev* agents, const int* row_base, int n
 // ===========================================================================
 // K4: consensus average in the reference's fixed pairwise-tree order
 // (mace.py:71-90), optionally the local partial sum for multi-rank runs.
+// W is [group][n_local][n] (a group = one slice of a multi-slice batch); out is [group][n].
 // ===========================================================================
 __global__ void k_consensus(const float* W, int n_local, size_t n, float scale, float* out, const float* ref,
-                            double* ref_part, const int* done)
+                            double* ref_part, const int* done, int n_groups = 1)
 {
     if (done && *done) return;
     double loc = 0.0;
-    for (size_t s = blockIdx.x * (size_t)blockDim.x + threadIdx.x; s < n; s += (size_t)gridDim.x * blockDim.x) {
+    for (size_t gs = blockIdx.x * (size_t)blockDim.x + threadIdx.x; gs < n * n_groups;
+         gs += (size_t)gridDim.x * blockDim.x) {
+        const size_t grp = gs / n, s = gs % n;
+        const float* Wg = W + grp * n_local * n;
         float acc[64];
-        for (int i = 0; i < n_local; ++i) acc[i] = W[(size_t)i * n + s];
+        for (int i = 0; i < n_local; ++i) acc[i] = Wg[(size_t)i * n + s];
         int m = n_local;
         while (m > 1) {
             const int half = m / 2;
@@ -468,8 +486,8 @@ __global__ void k_consensus(const float* W, int n_local, size_t n, float scale, 
             }
         }
         const float v = acc[0] / scale;
-        out[s] = v;
-        if (ref) {
+        out[gs] = v;
+        if (ref && grp == 0) {
             const double d = (double)v - (double)ref[s];
             loc += d * d;
         }
@@ -554,10 +572,13 @@ __global__ void k_fill(float* p, size_t n, float v)
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
+// X_i = x[slice(i)] for every local (virtual) agent; x is [slice][n]
 __global__ void k_broadcast_state(const AgentDev* agents, int n_agents, const float* x, size_t n)
 {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n * n_agents; i += (size_t)gridDim.x * blockDim.x)
-        agents[i / n].z[i % n] = x[i % n];
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n * n_agents; i += (size_t)gridDim.x * blockDim.x) {
+        const AgentDev& A = agents[i / n];
+        A.z[i % n] = x[(size_t)A.slice * n + i % n];
+    }
 }
 
 }  // namespace mace

@@ -89,6 +89,7 @@ struct Ctx {
     PriorC prior{};
     // agents
     int n_local = 0, schedule = 0, S = 8, NV = 1;
+    int n_real = 0, n_slices = 1;  // n_local = n_real agents x n_slices slices (config 4 batches)
     std::vector<std::unique_ptr<AgentMem>> am;
     std::vector<AgentDev> h_agents;
     DBuf<AgentDev> d_agents;
@@ -307,8 +308,9 @@ static void compute_theta2(Ctx* c)
 static void consensus(Ctx* c, float scale, float* out, bool with_ref)
 {
     const int blocks = kRefBlocks;
-    k_consensus<<<blocks, 256, 0, c->stream>>>(c->W.p, c->n_local, c->n, scale, out, with_ref ? c->ref.p : nullptr,
-                                                with_ref ? c->refpart.p : nullptr, c->done.p);
+    // per slice: tree over that slice's n_real agents (W is [slice][agent][n])
+    k_consensus<<<blocks, 256, 0, c->stream>>>(c->W.p, c->n_real, c->n, scale, out, with_ref ? c->ref.p : nullptr,
+                                                with_ref ? c->refpart.p : nullptr, c->done.p, c->n_slices);
     CK(cudaGetLastError());
 }
 
@@ -487,20 +489,26 @@ int mace_set_prior(void* p, int kind, double p_, double q, double T, double sx, 
     API_END
 }
 
-int mace_setup_agents(void* p, int n_local, const int* view_counts, const int* views, int schedule, int svs,
-                      int colours, int n_threads)
+int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* views, int schedule, int svs,
+                      int colours, int n_threads, int n_slices)
 {
     API_BEGIN
     Ctx* c = C(p);
     if (!c->nnz && !c->rp.p) throw std::runtime_error("load the system matrix first");
-    if (n_local < 1 || n_local > 64) throw std::runtime_error("1..64 agents per context");
+    if (n_agents < 1 || n_agents > 64) throw std::runtime_error("1..64 agents per context");
+    if (n_slices < 1 || n_agents * n_slices > 1024) throw std::runtime_error("1..1024 agents x slices per context");
+    if (schedule == 1 && n_slices != 1) throw std::runtime_error("multi-slice batches need the super-voxel schedule");
     if (schedule == 0 && (svs < 2 || (svs & 1))) throw std::runtime_error("super-voxel side must be even and >= 2");
+    // local (virtual) agent va = slice * n_agents + a shares real agent a's layout
+    const int n_local = n_agents * n_slices;
+    c->n_real = n_agents;
+    c->n_slices = n_slices;
     c->n_local = n_local;
     c->schedule = schedule;
     c->S = schedule == 0 ? svs : c->n_side;
     c->am.clear();
     int off = 0;
-    for (int a = 0; a < n_local; ++a) {
+    for (int a = 0; a < n_agents; ++a) {
         auto m = std::make_unique<AgentMem>();
         m->views.assign(views + off, views + off + view_counts[a]);
         off += view_counts[a];
@@ -509,7 +517,7 @@ int mace_setup_agents(void* p, int n_local, const int* view_counts, const int* v
         m->R = (int)m->views.size() * c->n_ch;
         c->am.push_back(std::move(m));
     }
-    // host layout build (CSR download is avoided: we keep a host copy only transiently)
+    // host layout build from a transient host copy of the global CSR
     const int64_t rows = (int64_t)c->n_views * c->n_ch;
     std::vector<int64_t> h_rp(rows + 1);
     std::vector<int32_t> h_cols(c->nnz);
@@ -518,15 +526,15 @@ int mace_setup_agents(void* p, int n_local, const int* view_counts, const int* v
     CK(cudaMemcpy(h_cols.data(), c->cols.p, sizeof(int32_t) * c->nnz, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(h_vals.data(), c->vals.p, sizeof(float) * c->nnz, cudaMemcpyDeviceToHost));
     if (n_threads <= 0) n_threads = (int)std::max(1u, std::thread::hardware_concurrency());
-    std::vector<std::exception_ptr> errs(n_local);
-    std::vector<RasterLayout> rl(n_local);
-    std::vector<SVLayout> sl(n_local);
+    std::vector<std::exception_ptr> errs(n_agents);
+    std::vector<RasterLayout> rl(n_agents);
+    std::vector<SVLayout> sl(n_agents);
     {
         std::atomic<int> next(0);
         auto work = [&]() {
             for (;;) {
                 int a = next.fetch_add(1);
-                if (a >= n_local) break;
+                if (a >= n_agents) break;
                 try {
                     AgentCSC csc;
                     build_agent_csc(c->n_side, c->n_ch, h_rp.data(), h_cols.data(), h_vals.data(), c->am[a]->views, csc);
@@ -539,44 +547,17 @@ int mace_setup_agents(void* p, int n_local, const int* view_counts, const int* v
             }
         };
         std::vector<std::thread> th;
-        for (int t = 0; t < std::min(n_threads, n_local); ++t) th.emplace_back(work);
+        for (int t = 0; t < std::min(n_threads, n_agents); ++t) th.emplace_back(work);
         for (auto& t : th) t.join();
         for (auto& e : errs)
             if (e) std::rethrow_exception(e);
     }
-    // device buffers
-    c->total_rows = 0;
-    std::vector<int> rb(n_local + 1, 0);
-    // each agent's {e, lambda} block starts on a 16-byte boundary (TMA bulk copies)
-    for (int a = 0; a < n_local; ++a) rb[a + 1] = rb[a] + ((c->am[a]->R + 1) & ~1);
-    c->total_rows = rb[n_local];
-    c->row_base.alloc(n_local + 1);
-    CK(cudaMemcpy(c->row_base.p, rb.data(), sizeof(int) * (n_local + 1), cudaMemcpyHostToDevice));
-    c->EL.alloc(c->total_rows);
-    c->Y.alloc(c->total_rows);
-    c->Z.alloc((size_t)n_local * c->n);
-    c->W.alloc((size_t)n_local * c->n);
-    c->TH.alloc((size_t)n_local * c->n);
-    c->VT.alloc((size_t)n_local * c->n);
-    CK(cudaMemset(c->Z.p, 0, sizeof(float) * n_local * c->n));
-    CK(cudaMemset(c->W.p, 0, sizeof(float) * n_local * c->n));
-    CK(cudaMemset(c->EL.p, 0, sizeof(float2) * c->total_rows));
+    // per real agent: layout on the device
     int max_col = 0, max_band = 0, n_sv_side = 1;
-    c->h_agents.assign(n_local, AgentDev{});
-    for (int a = 0; a < n_local; ++a) {
+    for (int a = 0; a < n_agents; ++a) {
         AgentMem& m = *c->am[a];
         m.d_views.alloc(m.views.size());
         CK(cudaMemcpy(m.d_views.p, m.views.data(), sizeof(int) * m.views.size(), cudaMemcpyHostToDevice));
-        AgentDev& A = c->h_agents[a];
-        A.el = c->EL.p + rb[a];
-        A.y = c->Y.p + rb[a];
-        A.z = c->Z.p + (size_t)a * c->n;
-        A.w = c->W.p + (size_t)a * c->n;
-        A.th = c->TH.p + (size_t)a * c->n;
-        A.vt = c->VT.p + (size_t)a * c->n;
-        A.views = m.d_views.p;
-        A.R = m.R;
-        A.V = (int)m.views.size();
         if (schedule == 1) {
             RasterLayout& L = rl[a];
             m.rpix.alloc(L.pix.size());
@@ -589,11 +570,8 @@ int mace_setup_agents(void* p, int n_local, const int* view_counts, const int* v
             }
             m.entries = (int64_t)L.idx.size();
             m.max_col = L.max_col;
-            A.rpix = m.rpix.p;
-            A.ridx = m.ridx.p;
-            A.rval = m.rval.p;
-            A.n_sv_side = 1;
             m.n_sv = 1;
+            m.n_sv_side = 1;
         } else {
             SVLayout& L = sl[a];
             m.band.alloc(L.band.size());
@@ -614,31 +592,70 @@ int mace_setup_agents(void* p, int n_local, const int* view_counts, const int* v
             m.n_sv = L.n_sv;
             m.n_sv_side = L.n_sv_side;
             m.duplicates = L.duplicates;
-            A.band = m.band.p;
-            A.bsize = m.bsize.p;
-            A.pix = m.pix.p;
-            A.val = m.val.p;
-            A.idx = m.idx.p;
-            A.n_sv_side = L.n_sv_side;
             n_sv_side = L.n_sv_side;
-            std::vector<uint32_t> q1 = build_queue(1, L.n_sv_side, colours);
-            for (auto& v : q1) v |= ((uint32_t)a << 24);
-            m.queue.alloc(q1.size());
-            CK(cudaMemcpy(m.queue.p, q1.data(), sizeof(uint32_t) * q1.size(), cudaMemcpyHostToDevice));
+            if (n_slices == 1) {  // single-agent queue for plain passes (AgentWorkspace)
+                std::vector<uint32_t> q1 = build_queue(1, L.n_sv_side, colours);
+                for (auto& v : q1) v |= ((uint32_t)a << kAgentShift);
+                m.queue.alloc(q1.size());
+                CK(cudaMemcpy(m.queue.p, q1.data(), sizeof(uint32_t) * q1.size(), cudaMemcpyHostToDevice));
+            }
         }
         max_col = std::max(max_col, m.max_col);
         max_band = std::max(max_band, m.max_band);
+    }
+    // per local (virtual) agent: data arrays; each {e, lambda} block starts on a 16-byte boundary
+    std::vector<int> rb(n_local + 1, 0);
+    for (int va = 0; va < n_local; ++va) rb[va + 1] = rb[va] + ((c->am[va % n_agents]->R + 1) & ~1);
+    c->total_rows = rb[n_local];
+    c->row_base.alloc(n_local + 1);
+    CK(cudaMemcpy(c->row_base.p, rb.data(), sizeof(int) * (n_local + 1), cudaMemcpyHostToDevice));
+    c->EL.alloc(c->total_rows);
+    c->Y.alloc(c->total_rows);
+    c->Z.alloc((size_t)n_local * c->n);
+    c->W.alloc((size_t)n_local * c->n);
+    c->TH.alloc((size_t)n_local * c->n);
+    c->VT.alloc((size_t)n_local * c->n);
+    CK(cudaMemset(c->Z.p, 0, sizeof(float) * n_local * c->n));
+    CK(cudaMemset(c->W.p, 0, sizeof(float) * n_local * c->n));
+    CK(cudaMemset(c->EL.p, 0, sizeof(float2) * c->total_rows));
+    c->h_agents.assign(n_local, AgentDev{});
+    for (int va = 0; va < n_local; ++va) {
+        const int a = va % n_agents;
+        AgentMem& m = *c->am[a];
+        AgentDev& A = c->h_agents[va];
+        A.el = c->EL.p + rb[va];
+        A.y = c->Y.p + rb[va];
+        A.z = c->Z.p + (size_t)va * c->n;
+        A.w = c->W.p + (size_t)va * c->n;
+        A.th = c->TH.p + (size_t)va * c->n;
+        A.vt = c->VT.p + (size_t)va * c->n;
+        A.slice = va / n_agents;
+        A.views = m.d_views.p;
+        A.R = m.R;
+        A.V = (int)m.views.size();
+        A.rpix = m.rpix.p;
+        A.ridx = m.ridx.p;
+        A.rval = m.rval.p;
+        A.band = m.band.p;
+        A.bsize = m.bsize.p;
+        A.pix = m.pix.p;
+        A.val = m.val.p;
+        A.idx = m.idx.p;
+        A.n_sv_side = m.n_sv_side;
+        A.beta_eff = m.beta_eff;
+        A.inv_s2 = m.inv_s2;
+        A.clamp = m.clamp;
     }
     c->NV = max_col <= 128 ? 1 : (max_col <= 256 ? 2 : 4);
     if (max_col > 512) throw std::runtime_error("column longer than 512 entries");
     c->band_cap = (max_band + 1 + 3) & ~3;  // + the dummy row that pad slots point at
     if (schedule == 0) {
-        std::vector<uint32_t> q = build_queue(n_local, n_sv_side, colours);
+        std::vector<uint32_t> q = build_queue(n_agents, n_sv_side, colours, n_slices);
         c->queue.alloc(q.size());
         CK(cudaMemcpy(c->queue.p, q.data(), sizeof(uint32_t) * q.size(), cudaMemcpyHostToDevice));
         c->n_items = (int)q.size();
         int vmax = 0;
-        for (int a = 0; a < n_local; ++a) vmax = std::max(vmax, (int)c->am[a]->views.size());
+        for (int a = 0; a < n_agents; ++a) vmax = std::max(vmax, (int)c->am[a]->views.size());
         c->view_cap = (vmax + 1) & ~1;
         c->sv_smem = 4 * sv_warp_bytes(c->S, c->band_cap, c->view_cap);
         if (c->sv_smem > 227 * 1024) throw std::runtime_error("super-voxel band does not fit in shared memory");
@@ -647,12 +664,11 @@ int mace_setup_agents(void* p, int n_local, const int* view_counts, const int* v
     }
     c->part.alloc((size_t)std::max(c->n_items, n_local) * 4);
     c->d_agents.alloc(n_local);
-    for (int a = 0; a < n_local; ++a) {
-        c->h_agents[a].beta_eff = c->am[a]->beta_eff;
-        c->h_agents[a].inv_s2 = c->am[a]->inv_s2;
-        c->h_agents[a].clamp = c->am[a]->clamp;
-    }
     CK(cudaMemcpy(c->d_agents.p, c->h_agents.data(), sizeof(AgentDev) * n_local, cudaMemcpyHostToDevice));
+    // consensus images are [slice][n]
+    c->wbar.alloc(c->n * n_slices);
+    c->g.alloc(c->n * n_slices);
+    c->wsum.alloc(c->n * n_slices);
     c->passes = 0;
     API_END
 }
@@ -661,7 +677,7 @@ int mace_agent_info(void* p, int local, int64_t* info /* [8] */)
 {
     API_BEGIN
     Ctx* c = C(p);
-    if (local < 0 || local >= c->n_local) throw std::runtime_error("bad agent");
+    if (local < 0 || local >= c->n_real) throw std::runtime_error("bad agent");
     AgentMem& m = *c->am[local];
     info[0] = m.nnz;
     info[1] = m.entries;
@@ -705,11 +721,13 @@ int mace_set_agent_params(void* p, int local, double beta_eff, double inv_sigma2
 {
     API_BEGIN
     Ctx* c = C(p);
+    if (local >= c->n_local) throw std::runtime_error("bad agent");
     int a0 = local < 0 ? 0 : local, a1 = local < 0 ? c->n_local : local + 1;
     for (int a = a0; a < a1; ++a) {
-        c->am[a]->beta_eff = (float)beta_eff;
-        c->am[a]->inv_s2 = (float)inv_sigma2;
-        c->am[a]->clamp = clamp;
+        AgentMem& m = *c->am[a % c->n_real];
+        m.beta_eff = (float)beta_eff;
+        m.inv_s2 = (float)inv_sigma2;
+        m.clamp = clamp;
         c->h_agents[a].beta_eff = (float)beta_eff;
         c->h_agents[a].inv_s2 = (float)inv_sigma2;
         c->h_agents[a].clamp = clamp;
@@ -724,12 +742,18 @@ int mace_load_data(void* p, const float* y, const float* lam)
 {
     API_BEGIN
     Ctx* c = C(p);
+    // y / lam: [n_slices][n_views * n_ch] (one sinogram per slice of a batch)
     const size_t rows = (size_t)c->n_views * c->n_ch;
-    CK(cudaMemcpyAsync(c->y.p, y, sizeof(float) * rows, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->lam.p, lam, sizeof(float) * rows, cudaMemcpyHostToDevice, c->stream));
+    const size_t total = rows * std::max(1, c->n_slices);
+    if (c->y.n < total) {
+        c->y.alloc(total);
+        c->lam.alloc(total);
+    }
+    CK(cudaMemcpyAsync(c->y.p, y, sizeof(float) * total, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->lam.p, lam, sizeof(float) * total, cudaMemcpyHostToDevice, c->stream));
     if (c->n_local) {
         k_gather_data<<<c->num_sms * 4, 256, 0, c->stream>>>(c->d_agents.p, c->row_base.p, c->n_local, c->total_rows,
-                                                              c->n_ch, c->y.p, c->lam.p);
+                                                              c->n_ch, c->y.p, c->lam.p, (int64_t)rows);
         CK(cudaGetLastError());
         compute_theta2(c);
     }
@@ -794,6 +818,7 @@ int mace_pass(void* p, int local, const float* v, int n_passes, int64_t s_begin,
     API_BEGIN
     Ctx* c = C(p);
     if (local < 0 || local >= c->n_local) throw std::runtime_error("bad agent");
+    if (c->n_slices != 1) throw std::runtime_error("plain passes need a single-slice context");
     CK(cudaMemcpyAsync(c->h_agents[local].vt, v, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(c->done.p, 0, 2 * sizeof(int), c->stream));
     std::vector<double> part;
@@ -906,7 +931,8 @@ int mace_get_image(void* p, int which, float* out)
 {
     API_BEGIN
     Ctx* c = C(p);
-    CK(cudaMemcpyAsync(out, which ? c->g.p : c->wbar.p, sizeof(float) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(out, which ? c->g.p : c->wbar.p, sizeof(float) * c->n * c->n_slices, cudaMemcpyDeviceToHost,
+                       c->stream));
     sync(c);
     API_END
 }
@@ -915,7 +941,8 @@ int mace_set_image(void* p, int which, const float* img)
 {
     API_BEGIN
     Ctx* c = C(p);
-    CK(cudaMemcpyAsync(which ? c->g.p : c->wbar.p, img, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(which ? c->g.p : c->wbar.p, img, sizeof(float) * c->n * c->n_slices, cudaMemcpyHostToDevice,
+                       c->stream));
     sync(c);
     API_END
 }
@@ -996,7 +1023,7 @@ int mace_mean_from_sum(void* p, int n_total)
     Ctx* c = C(p);
     // wbar = wsum / N: a one-agent "tree" over the reduced sum
     k_consensus<<<kRefBlocks, 256, 0, c->stream>>>(c->wsum.p, 1, c->n, (float)n_total, c->wbar.p, nullptr, nullptr,
-                                                   nullptr);
+                                                   nullptr, c->n_slices);
     CK(cudaGetLastError());
     API_END
 }
@@ -1007,7 +1034,7 @@ int mace_iterate_finish(void* p, int n_total, double tol, int iter)
     Ctx* c = C(p);
     ensure_log(c, iter + 1);
     k_consensus<<<kRefBlocks, 256, 0, c->stream>>>(c->wsum.p, 1, c->n, (float)n_total, c->wbar.p, nullptr, nullptr,
-                                                   c->done.p);
+                                                   c->done.p, c->n_slices);
     k_finish<<<1, 1, 0, c->stream>>>(c->sums5.p, 0.0, tol, iter, c->log.p, c->done.p, c->head.p);
     if (c->passes % 50 == 0) refresh(c, 0, c->n_local);
     CK(cudaGetLastError());

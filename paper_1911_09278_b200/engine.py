@@ -139,7 +139,7 @@ class AgentPlan(_Context):
     """Context with the layouts of ``agent_views`` (one tuple of view indices per local agent)."""
 
     def __init__(self, matrices, agent_views, schedule: str = "sv", sv: int = DEFAULT_SV,
-                 colours: int = DEFAULT_COLOURS, device: int = 0):
+                 colours: int = DEFAULT_COLOURS, device: int = 0, n_slices: int = 1):
         super().__init__(device)
         if schedule not in SCHEDULES:
             raise ValueError(f"schedule must be one of {sorted(SCHEDULES)}")
@@ -152,9 +152,12 @@ class AgentPlan(_Context):
         if schedule == "sv":
             lim = min(sv, self.n_side + (self.n_side & 1))
             sv_eff = max([s for s in SV_SIDES if s <= max(lim, 2)])
+        self.n_slices = int(n_slices)
         self.call("mace_setup_agents", len(self.agent_views), N.ptr(counts), N.ptr(flat), SCHEDULES[schedule],
-                  int(sv_eff), int(colours), 0)
-        self.n_local = len(self.agent_views)
+                  int(sv_eff), int(colours), 0, self.n_slices)
+        # local (virtual) agents: slice-major, index = slice * n_agents + agent
+        self.n_agents = len(self.agent_views)
+        self.n_local = self.n_agents * self.n_slices
         self.set_schedule(DEFAULT_CONCURRENCY, int(os.environ.get("MACE_SV_MAX_WARPS", "0")))
 
     def agent_info(self, a):
@@ -164,8 +167,8 @@ class AgentPlan(_Context):
                         buf.tolist()))
 
     def load_data(self, y, weights):
-        """y / weights (n_views x n_ch, any float dtype) -> pinned float32 staging -> device."""
-        rows = self.n_views * self.n_ch
+        """y / weights ([n_slices x] n_views x n_ch, any float dtype) -> pinned float32 staging -> device."""
+        rows = self.n_views * self.n_ch * getattr(self, "n_slices", 1)
         if getattr(self, "_pin", None) is None:
             p = ctypes.c_void_p()
             N.check(self.L.mace_host_alloc(2 * rows * 4, ctypes.byref(p)), "host_alloc")
@@ -273,16 +276,21 @@ class AgentPlan(_Context):
         return lg[:n], (int(done[0]), int(done[1]))
 
     def get_image(self, which) -> np.ndarray:
-        out = np.empty(self.n, np.float32)
+        """wbar (which=0) or G_H(w) (which=1): shape (n,), or (n_slices, n) for a batch."""
+        out = np.empty((self.n_slices, self.n) if self.n_slices > 1 else self.n, np.float32)
         self.call("mace_get_image", int(which), N.ptr(out))
         return out
 
     def set_image(self, which, img):
         img = N.f32(img)
+        if img.size != self.n * self.n_slices:
+            raise ValueError("image size mismatch")
         self.call("mace_set_image", int(which), N.ptr(img))
 
     def get_stack(self) -> np.ndarray:
-        out = np.empty((self.n_local, self.n), np.float32)
+        """(n_local, n) for one slice, (n_slices, n_agents, n) for a batch."""
+        shape = (self.n_slices, self.n_agents, self.n) if self.n_slices > 1 else (self.n_local, self.n)
+        out = np.empty(shape, np.float32)
         self.call("mace_get_stack", N.ptr(out))
         return out
 
@@ -295,6 +303,7 @@ class _DevArray:
                                          "strides": None}
 
 
-def plan_for(matrices, agent_views, schedule="sv", sv=DEFAULT_SV, colours=DEFAULT_COLOURS, device=0) -> AgentPlan:
-    key = ("plan", id(matrices), tuple(tuple(v) for v in agent_views), schedule, sv, colours, device)
-    return _cached(key, lambda: AgentPlan(matrices, agent_views, schedule, sv, colours, device), matrices)
+def plan_for(matrices, agent_views, schedule="sv", sv=DEFAULT_SV, colours=DEFAULT_COLOURS, device=0,
+             n_slices=1) -> AgentPlan:
+    key = ("plan", id(matrices), tuple(tuple(v) for v in agent_views), schedule, sv, colours, device, n_slices)
+    return _cached(key, lambda: AgentPlan(matrices, agent_views, schedule, sv, colours, device, n_slices), matrices)

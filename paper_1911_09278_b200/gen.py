@@ -97,6 +97,35 @@ def make_scan(config: int = 1, seed: int = 0, slice_index: int = 0, matrices=Non
     return geom, matrices, phantom, y, lam
 
 
+def make_batch(config: int = 4, seed: int = 0, n_slices: int | None = None, device_fp: bool = True):
+    """Config-4 batch: one geometry, `n_slices` seeded phantoms (seed + 1000 s), Poisson data.
+    device_fp: project the phantoms with the GPU operator (K3, float32) instead of the float64
+    host projector — 64 host projections at 512^2 take ~45 s; the data is synthetic either way."""
+    from .geometry import Geometry, build_system_matrix
+
+    c = CONFIGS[config]
+    ns = c["n_side"]
+    S = c["slices"] if n_slices is None else n_slices
+    pitch = pitch_for(ns)
+    geom = Geometry(ns, pitch, c["n_views"], c["n_channels"], pitch)
+    mats = build_system_matrix(geom)
+    if device_fp:
+        from .engine import operator_for
+
+        op = operator_for(mats)
+        fp = lambda x: op.forward_project(x).astype(np.float64)  # noqa: E731
+    else:
+        fp = lambda x: host_forward_project(mats, x)  # noqa: E731
+    phantoms, ys, lams = [], [], []
+    for s in range(S):
+        ph = ellipse_phantom(ns, pitch, c["n_ellipses"], seed=seed + 1000 * s)
+        y, lam = poisson_sinogram(fp(ph), c["I0"], seed=seed + 1000 * s + 1)
+        phantoms.append(ph)
+        ys.append(y)
+        lams.append(lam)
+    return geom, mats, phantoms, ys, lams
+
+
 def poisson_sinogram(proj: np.ndarray, I0: float, seed: int = 1):
     """counts ~ Poisson(I0 exp(-proj)), clamped >= 1; returns (y, weights=counts)."""
     rng = np.random.default_rng(seed)

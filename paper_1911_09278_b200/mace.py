@@ -30,7 +30,7 @@ from .icd import AgentWorkspace, ConvergenceError, prox_solve
 
 __all__ = ["MaceConfig", "MaceResult", "ConvergenceLog", "ResidualReport", "WorkerPool", "new_stack", "average",
            "consensus_G", "reflect_G", "consensus_GH", "mann_step", "mace_solve", "mace_pnp_solve",
-           "equilibrium_residuals", "EquitCounter", "nrmse"]
+           "equilibrium_residuals", "EquitCounter", "nrmse", "mace_solve_batch"]
 
 CONVENTIONAL = "conventional"
 PNP = "pnp"
@@ -452,6 +452,57 @@ def mace_pnp_solve(problem, config: MaceConfig, pool: WorkerPool | None = None, 
     if denoiser is None:
         denoiser = make_denoiser(config.denoiser, problem.geom.n_side)
     return _run_outer(problem, config, pool, ref_image, w0, denoiser=denoiser, comm=comm, backend=_backend)
+
+
+def mace_solve_batch(problems, config: MaceConfig) -> list:
+    """Independent conventional MACE solves of several slices that share one scan geometry
+    (BASELINE config 4: 64 slices, N view agents, one operator).  Equivalent to
+    ``[mace_solve(p, config) for p in problems]`` except that the stop test uses the Mann
+    relnorm of the whole batch.  On the GPU the slices of an agent run as concurrent agents
+    on the same super-voxel tile, so each tile's A columns stream from HBM once per
+    iteration for all slices.  Returns one MaceResult per slice (the log is shared); raises
+    ConvergenceError (``last_iterate`` = that list) when the budget runs out."""
+    problems = list(problems)
+    if not problems:
+        raise ValueError("need at least one problem")
+    if config.mode != CONVENTIONAL:
+        raise ValueError("mace_solve_batch requires mode='conventional'")
+    p0 = problems[0]
+    for p in problems[1:]:
+        if p.matrices is not p0.matrices or p.y.shape != p0.y.shape:
+            raise ValueError("batched slices must share the matrices object and geometry")
+        if p.prior != p0.prior:
+            raise ValueError("batched slices must share the prior")
+    S, N, n = len(problems), config.n_subsets, p0.geom.n_pixels
+    subsets = partition_views(p0.geom.n_views, N)
+    plan = plan_for(p0.matrices, [s.view_indices for s in subsets], schedule="sv",
+                    sv=getattr(config, "sv_side", DEFAULT_SV), colours=getattr(config, "colours", DEFAULT_COLOURS),
+                    device=getattr(config, "device", 0), n_slices=S)
+    beta = p0.prior.beta if config.beta is None else config.beta
+    plan.load_data(np.stack([p.y for p in problems]), np.stack([p.weights for p in problems]))
+    plan.set_prior(p0.prior)
+    plan.set_agent_params(-1, beta / N, 1.0 / (config.sigma * config.sigma), config.clamp_nonneg)
+    plan.stack_init(None, N)
+    plan.states_from(0)
+    plan.set_ref(None)
+    t0 = time.perf_counter()
+    ms = plan.iterate(config.max_outer, 0, config.rho, False, config.tol, N, False)
+    lg, done = plan.read_log(config.max_outer)
+    wall = time.perf_counter() - t0
+    if done[0] == 2:
+        raise ConvergenceError(f"MACE diverged at iteration {done[1]} (reduce sigma)", last_iterate=None)
+    iters = done[1] if done[0] == 1 else config.max_outer
+    images = plan.get_image(0).reshape(S, n).astype(np.float64)
+    stacks = plan.get_stack().reshape(S, N, n).astype(np.float64)
+    log = ConvergenceLog()
+    counter = EquitCounter(n, N)
+    _fill_log(log, [(lg[j, 0], None, wall * (j + 1) / max(iters, 1)) for j in range(iters)], counter, N, n)
+    results = [MaceResult(image=images[s], stack=stacks[s], log=log, iterations=iters, converged=done[0] == 1,
+                          equits=counter.equits(), device_ms=ms) for s in range(S)]
+    if done[0] != 1:
+        raise ConvergenceError(f"MACE batch: relnorm did not reach {config.tol:g} in {config.max_outer} iterations",
+                               last_iterate=results, log=log)
+    return results
 
 
 def equilibrium_residuals(problem, config: MaceConfig, w, prox_tol: float = 1e-9, denoiser=None) -> ResidualReport:
