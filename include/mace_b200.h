@@ -131,7 +131,7 @@ int mace_sweep_f64(double* z, const double* v, double* e, const int64_t* col_ptr
 /* ---- host-only layout probes (no device needed; used by the CPU test suite).
  * mace_agent_csc: the stacked agent CSC of icd.py:185-192; col_ptr[n+1] always, rows/vals if non-null.
  * mace_sv_layout_probe: the super-voxel layout decoded back to (pixel, local row, value) triples;
- * stats[6] = entries, max_band, max_col, n_sv, duplicates, decoded. */
+ * stats[6] = lane slots, widest band window, max_col, n_sv, duplicates, decoded. */
 int mace_agent_csc(int n_side, int n_ch, int n_views, const int64_t* row_ptr, const int32_t* cols, const float* vals,
                    int n_agent_views, const int* views, int64_t* col_ptr, uint32_t* rows, float* out_vals);
 int mace_sv_layout_probe(int n_side, int n_ch, int n_views, const int64_t* row_ptr, const int32_t* cols,

@@ -8,7 +8,7 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libmace_b200.so")
+LIB = os.environ.get("MACE_LIB") or os.path.join(PKG, "libmace_b200.so")  # MACE_LIB: ablation builds
 SOURCES = ["mace.cu", "cnn.cu", "layout.cpp", "sysmat.cpp"]
 HEADERS = ["kernels.cuh", "internal.h", "cnn.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

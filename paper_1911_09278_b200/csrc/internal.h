@@ -43,23 +43,49 @@ struct RasterLayout {
 };
 
 // Super-voxel layout: S x S pixel tiles; the error-sinogram rows a tile touches
-// (its "band": one contiguous channel window per view) are staged in shared
-// memory, so entries carry a 16-bit band index instead of the 32-bit row.
+// (its "band": one contiguous channel window per view) are staged in shared memory.
+// Lane-per-view super-voxel layout.  Parallel-beam geometry gives every (pixel, view)
+// pair at most a few entries on consecutive channels, so view j is owned by lane j % 32
+// (view group g = j / 32, at most 4 groups): per tile, view j's band window is the rows
+// [start_j, start_j + cnt_j) the tile touches; per pixel, lane l of group g holds the K
+// lengths of view 32g+l and their offset inside that window (one byte per group).  In
+// shared memory the window of view j lives in bank j % 32, so gathers and scatters are
+// bank-conflict free and rows are lane-private.
+//
+// Pixels of a tile are visited in four parity classes (row mod 2, col mod 2), raster order
+// inside a class, in batches of kSvBatch: pixels of one batch are never 8-neighbours, so their
+// prior terms are independent and their coupling through shared sinogram rows is one
+// precomputed cross term per pair (k_sv.cuh).  Slot records are stored in visit order,
+// batch-contiguous, so a batch is one contiguous copy.
+constexpr int kSvBatch = 4;
 struct SVLayout {
     int svs = 0, n_sv_side = 0, n_sv = 0, views = 0;
-    std::vector<int2_t> band;    // [n_sv * views] {local row start, (pos << 16) | cnt}
-    std::vector<int32_t> bsize;  // [n_sv] band rows
-    std::vector<int2_t> pix;     // [n_sv * S * S] {entry start, length}; length 0 outside image
-    std::vector<uint16_t> idx;   // band-local row
-    std::vector<float> val;
-    int max_band = 0, max_col = 0;
+    int ng = 0;                  // view groups ceil(views / 32) (<= 4)
+    int K = 0;                   // entries per (pixel, view) slot (max over the agent, 2 for pitch = channel pitch)
+    int wcap = 0;                // max window rows over tiles and views
+    int nb = 0;                  // batches per tile
+    int rec = 0;                 // words per pixel slot: ng*32*K lengths ([g][lane][k]) + 32 offset words
+    std::vector<int2_t> band;    // [n_sv * views] {local row start, cnt}
+    std::vector<uint32_t> data;  // [n_sv][nb][kSvBatch][rec] (lengths as float bits; empty slots 0)
+    int max_col = 0;             // max entries per column (info)
+    int64_t entries = 0;         // stored nonzeros (== nnz of the agent)
     int64_t duplicates = 0;      // repeated (row, pixel) pairs merged (never seen in practice)
 };
+// Visit-order slot t of an S x S tile -> local pixel (lr * S + lc), or -1 for a padding slot.
+inline int sv_slot_pixel(int S, int t)
+{
+    const int h = S / 2, per_class = h * h, bpc = (per_class + kSvBatch - 1) / kSvBatch;
+    const int b = t / kSvBatch, cls = b / bpc, i = (b % bpc) * kSvBatch + t % kSvBatch;
+    if (i >= per_class) return -1;
+    return ((cls >> 1) + 2 * (i / h)) * S + (cls & 1) + 2 * (i % h);
+}
+inline int sv_batches(int S) { return 4 * (((S / 2) * (S / 2) + kSvBatch - 1) / kSvBatch); }
 
 void build_agent_csc(int n_side, int n_ch, const int64_t* row_ptr, const int32_t* cols, const float* vals,
                      const std::vector<int>& views, AgentCSC& out);
 void build_raster_layout(const AgentCSC& csc, int n, RasterLayout& out);
-void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int n_views_agent, int svs, SVLayout& out);
+// ng: view groups of the record (0: ceil(views / 32)); agents of one context share one ng
+void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int n_views_agent, int svs, SVLayout& out, int ng = 0);
 // Queue of (agent << 22 | sv) items: colour classes (sv_row mod C, sv_col mod C) in
 // order, SVs of a class in raster order, agents interleaved within a position.
 std::vector<uint32_t> build_queue(int n_agents, int n_sv_side, int colours, int n_slices = 1);

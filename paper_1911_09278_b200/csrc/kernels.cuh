@@ -35,7 +35,8 @@ struct PriorC {
 };
 
 struct AgentDev {
-    float2* el;        // [R] {e, lambda}: error sinogram and weights, interleaved
+    float* e;          // [R] error sinogram y_i - A_i X_i (icd.py:200)
+    float* lam;        // [R] weights lambda
     float* y;          // [R]
     float* z;          // [n] agent state X_i
     float* w;          // [n] stack component w_i
@@ -44,11 +45,10 @@ struct AgentDev {
     int slice;         // slice of a multi-slice batch (config 4); consensus images are [slice][n]
     const int* views;  // [V] global view index of local view j
     // super-voxel layout
-    const int2* band;   // [n_sv * V]
-    const int* bsize;   // [n_sv]
-    const int2* pix;    // [n_sv * S * S]
-    const float* val;
-    const uint16_t* idx;
+    const int2* band;      // [n_sv * V] {local row start, window rows}
+    const uint32_t* rec;   // [n_sv][nb][4][rec_words] slot records (layout.cpp, lane-per-view)
+    float* bc;             // [n_sv][nb][16] batch constants: theta2 x4, cross terms x6 (per local agent)
+    int ng, rec_words;     // view groups ceil(V / 32); words per slot record
     // raster layout
     const int2* rpix;   // [n]
     const uint32_t* ridx;
@@ -68,8 +68,7 @@ struct PassParams {
     int n_items;
     unsigned* head;
     double* part;  // [n_items * 4]: sum alpha^2, sum (w'-w)^2, sum w'^2, sum w^2
-    int band_cap, view_cap;
-    int stage_tma;  // 1: stage bands with TMA bulk copies; 0: LDGSTS (cp.async.cg)
+    int ng, wcap, view_cap;  // shared-memory band geometry (max over agents)
     const int* done;
     long s_begin, s_end;  // raster passes: pixel range [s_begin, s_end) (icd.py:222-246)
 };
@@ -175,7 +174,8 @@ __global__ void __launch_bounds__(32) k_icd_raster(PassParams P, int agent_base)
     const AgentDev& A = P.agents[agent_base + item];
     const int n = P.n_side;
     const PriorC& PR = P.pr;
-    float2* el = A.el;
+    float* eg = A.e;
+    const float* lam = A.lam;
     float* z = A.z;
     const float beta = A.beta_eff, inv_s2 = A.inv_s2;
     double dsq = 0.0;
@@ -204,8 +204,8 @@ __global__ void __launch_bounds__(32) k_icd_raster(PassParams P, int agent_base)
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 if (e0 + q < pe.y) {
-                    const float2 x = __ldcg(el + ii4[j][q]);
-                    t = fmaf(vv4[j][q] * x.y, x.x, t);
+                    const uint32_t r = ii4[j][q];
+                    t = fmaf(vv4[j][q] * __ldg(lam + r), __ldcg(eg + r), t);
                 }
         }
         float g, c;
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(32) k_icd_raster(PassParams P, int agent_base)
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     if (e0 + q < pe.y) {
-                        float* ep = &el[ii4[j][q]].x;
+                        float* ep = eg + ii4[j][q];
                         __stcg(ep, __ldcg(ep) - alpha * vv4[j][q]);
                     }
             }
@@ -310,7 +310,7 @@ __global__ void k_fp_agents(FPParams F, const AgentDev* agents, const int* row_b
         float acc = 0.f;
         for (int64_t k = F.rp[g] + lane; k < F.rp[g + 1]; k += 32) acc = fmaf(F.vals[k], __ldcg(A.z + F.cols[k]), acc);
         acc = warp_sum(acc);
-        if (lane == 0) A.el[r].x = A.y[r] - acc;
+        if (lane == 0) A.e[r] = A.y[r] - acc;
     }
 }
 
@@ -398,48 +398,73 @@ __global__ void k_theta2_raster(const AgentDev* agents, int n_agents, int n)
         float acc = 0.f;
         for (int k = lane; k < pe.y; k += 32) {
             const float a = A.rval[pe.x + k];
-            acc = fmaf(a * a, A.el[A.ridx[pe.x + k]].y, acc);
+            acc = fmaf(a * a, A.lam[A.ridx[pe.x + k]], acc);
         }
         acc = warp_sum(acc);
         if (lane == 0) A.th[s] = acc;
     }
 }
 
-__global__ void __launch_bounds__(128) k_theta2_sv(const AgentDev* agents, int n_items, const uint32_t* queue,
-                                                   int n_side, int S, int cap)
+// Super-voxel batch constants from the lane-per-view layout (one warp per (agent, tile) item):
+// theta2_p = sum a_p^2 lambda (icd.py:193-195) for the kSvBatch slots of each batch, and the
+// cross terms c_ij = sum_r a_ir a_jr lambda_r that couple two pixels of a batch through shared
+// rows (k_sv.cuh).  Depends on lambda only, so it is recomputed per data load.
+__global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n_items, const uint32_t* queue,
+                                                   int n_side, int S, int K, int nb)
 {
-    extern __shared__ __align__(16) unsigned char smem[];
-    float* lamb = reinterpret_cast<float*>(smem) + (threadIdx.x >> 5) * (size_t)cap;
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
-    const int SS = S * S;
+    const int SS = S * S, h = S / 2, per_class = h * h, bpc = (per_class + 3) / 4;
     for (int item = gw; item < n_items; item += nw) {
         const uint32_t code = queue[item];
         const AgentDev& A = agents[code >> kAgentShift];
         const int sv = (int)(code & kSvMask);
         const int r0 = (sv / A.n_sv_side) * S, c0 = (sv % A.n_sv_side) * S;
         const int2* bt = A.band + (size_t)sv * A.V;
-        for (int j = lane >> 4; j < A.V; j += 2) {
-            const int2 b = bt[j];
-            const int cnt = b.y & 0xffff, pos = b.y >> 16;
-            for (int c = lane & 15; c < cnt; c += 16) lamb[pos + c] = A.el[b.x + c].y;
+        int start[4];
+        for (int g = 0; g < 4; ++g) {
+            const int j = 32 * g + lane;
+            start[g] = (g < A.ng && j < A.V) ? bt[j].x : 0;
         }
-        if (lane == 0) lamb[A.bsize[sv]] = 0.f;  // dummy row referenced by pad slots (value 0)
-        __syncwarp();
-        for (int k = 0; k < SS; ++k) {
-            const int rr = r0 + k / S, cc = c0 + k % S;
-            if (rr >= n_side || cc >= n_side) continue;
-            const int2 pe = A.pix[(size_t)sv * SS + k];
-            float acc = 0.f;
-            for (int e = lane; e < ((pe.y + 7) & ~7); e += 32) {
-                const float a = A.val[pe.x + e];
-                acc = fmaf(a * a, lamb[A.idx[pe.x + e]], acc);
+        for (int b = 0; b < nb; ++b) {
+            const uint32_t* rb = A.rec + ((size_t)sv * nb + b) * 4 * A.rec_words;
+            float t2[4] = {0.f, 0.f, 0.f, 0.f}, cx[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int g = 0; g < A.ng; ++g) {
+                float a[4][4];
+                int o[4];
+                for (int p = 0; p < 4; ++p) {
+                    const uint32_t* r = rb + (size_t)p * A.rec_words;
+                    o[p] = (int)((r[A.ng * 32 * K + lane] >> (8 * g)) & 0xffu);
+                    for (int q = 0; q < K; ++q) a[p][q] = __uint_as_float(r[(g * 32 + lane) * K + q]);
+                }
+                for (int p = 0; p < 4; ++p)
+                    for (int q = 0; q < K; ++q)
+                        if (a[p][q] != 0.f) t2[p] = fmaf(a[p][q] * a[p][q], A.lam[start[g] + o[p] + q], t2[p]);
+                int x = 0;
+                for (int i = 0; i < 4; ++i)
+                    for (int j = i + 1; j < 4; ++j, ++x)
+                        for (int q = 0; q < K; ++q) {  // row o_i + q of pixel i is row q - (o_j - o_i) of j
+                            const int qj = q - (o[j] - o[i]);
+                            if (qj >= 0 && qj < K && a[i][q] != 0.f && a[j][qj] != 0.f)
+                                cx[x] = fmaf(a[i][q] * a[j][qj], A.lam[start[g] + o[i] + q], cx[x]);
+                        }
             }
-            acc = warp_sum(acc);
-            if (lane == 0) A.th[(size_t)rr * n_side + cc] = acc;
+            for (int p = 0; p < 4; ++p) t2[p] = warp_sum(t2[p]);
+            for (int x = 0; x < 6; ++x) cx[x] = warp_sum(cx[x]);
+            float* out = A.bc + ((size_t)sv * nb + b) * 16;
+            if (lane < 4) out[lane] = t2[lane];
+            else if (lane < 10) out[lane] = cx[lane - 4];
+            else if (lane < 16) out[lane] = 0.f;
+            if (lane < 4) {  // theta2 image (cost kernels, diagnostics)
+                const int i = (b % bpc) * 4 + lane, cls = b / bpc;
+                if (i < per_class) {
+                    const int lr = (cls >> 1) + 2 * (i / h), lc = (cls & 1) + 2 * (i % h);
+                    if (r0 + lr < n_side && c0 + lc < n_side && lr * S + lc < SS)
+                        A.th[(size_t)(r0 + lr) * n_side + c0 + lc] = t2[lane];
+                }
+            }
         }
-        __syncwarp();
     }
 }
 
@@ -454,7 +479,7 @@ __global__ void k_gather_data(const AgentDev* agents, const int* row_base, int n
         if (r >= A.R) continue;
         const int64_t g = (int64_t)A.slice * slice_rows + (int64_t)A.views[r / n_ch] * n_ch + r % n_ch;
         A.y[r] = y[g];
-        A.el[r].y = lam[g];
+        A.lam[r] = lam[g];
     }
 }
 

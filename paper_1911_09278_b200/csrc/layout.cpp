@@ -5,8 +5,8 @@
 // then tocsc) as a counting sort; the result is index-identical to scipy's
 // canonical CSC (asserted by tests/test_layout.py against the reference's
 // golden col_ptr/row_idx).  The raster and super-voxel layouts are B200-side
-// re-packings of that CSC: columns padded to 4 entries for 128-bit loads and,
-// for super-voxels, 16-bit band-local row indices.
+// re-packings of that CSC: columns padded to 4 entries for 128-bit loads (raster) and
+// lane-per-view slot records in batch visit order (super-voxels, internal.h).
 #include <algorithm>
 #include <cstring>
 #include <stdexcept>
@@ -46,7 +46,6 @@ void build_agent_csc(int n_side, int n_ch, const int64_t* row_ptr, const int32_t
 }
 
 static inline int64_t pad4(int64_t x) { return (x + 3) & ~int64_t(3); }
-static inline int64_t pad8(int64_t x) { return (x + 7) & ~int64_t(7); }
 
 void build_raster_layout(const AgentCSC& csc, int n, RasterLayout& out)
 {
@@ -73,117 +72,97 @@ void build_raster_layout(const AgentCSC& csc, int n, RasterLayout& out)
     }
 }
 
-void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SVLayout& out)
+void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SVLayout& out, int ng)
 {
+    if (V > 128) throw std::runtime_error("super-voxel layout: at most 128 views per agent (4 lane groups)");
     out.svs = S;
     out.views = V;
+    out.ng = std::max((V + 31) / 32, ng);
+    if (out.ng > 4) throw std::runtime_error("super-voxel layout: at most 4 view groups");
     out.n_sv_side = (n_side + S - 1) / S;
     out.n_sv = out.n_sv_side * out.n_sv_side;
     out.band.assign((size_t)out.n_sv * V, {0, 0});
-    out.bsize.assign(out.n_sv, 0);
-    out.pix.assign((size_t)out.n_sv * S * S, {0, 0});
-    out.max_band = 0;
     out.max_col = 0;
     out.duplicates = 0;
-    // pass 1: band windows and entry counts
-    std::vector<int> lo(V), hi(V);
-    int64_t total = 0;
-    std::vector<int64_t> sv_entries(out.n_sv, 0);
+    out.entries = 0;
+    // pass 1: windows per (tile, view), entries per (pixel, view); rows of a (pixel, view) pair
+    // must be consecutive channels (a convex pixel in parallel-beam geometry)
+    std::vector<int> lo(V), hi(V), first(V), cntpv(V);
+    int K = 1, wcap = 1;
     for (int sv = 0; sv < out.n_sv; ++sv) {
         const int r0 = (sv / out.n_sv_side) * S, c0 = (sv % out.n_sv_side) * S;
         std::fill(lo.begin(), lo.end(), INT32_MAX);
         std::fill(hi.begin(), hi.end(), -1);
-        int64_t ent = 0;
         for (int k = 0; k < S * S; ++k) {
             const int r = r0 + k / S, c = c0 + k % S;
             if (r >= n_side || c >= n_side) continue;
             const int64_t s = (int64_t)r * n_side + c;
-            int64_t L = 0;
+            std::fill(cntpv.begin(), cntpv.end(), 0);
+            std::fill(first.begin(), first.end(), -1);
             uint32_t prev = UINT32_MAX;
+            int L = 0;
             for (int64_t q = csc.col_ptr[s]; q < csc.col_ptr[s + 1]; ++q) {
                 const uint32_t row = csc.row[q];
-                if (row == prev) continue;  // duplicate (row, pixel) -> merged below
+                if (row == prev) continue;
                 prev = row;
                 ++L;
                 const int j = (int)(row / n_ch), ch = (int)(row % n_ch);
+                if (first[j] < 0) first[j] = ch;
+                else if (ch != first[j] + cntpv[j]) throw std::runtime_error("non-contiguous channels in a (pixel, view)");
+                cntpv[j]++;
                 lo[j] = std::min(lo[j], ch);
                 hi[j] = std::max(hi[j], ch);
             }
-            out.max_col = std::max<int>(out.max_col, (int)L);
-            ent += pad8(L);
+            out.max_col = std::max(out.max_col, L);
+            for (int j = 0; j < V; ++j) K = std::max(K, cntpv[j]);
         }
-        int pos = 0;
         for (int j = 0; j < V; ++j) {
-            // window of local rows, widened to 16-byte ({e, lambda} float2 pairs) alignment so the
-            // kernel can stage it with one bulk (TMA) copy per view; pads are never referenced
-            int start = 0, cnt = 0;
-            if (hi[j] >= 0) {
-                start = (j * n_ch + lo[j]) & ~1;
-                const int end = ((j * n_ch + hi[j]) | 1) + 1;
-                cnt = end - start;
-            }
-            out.band[(size_t)sv * V + j] = {(int32_t)start, (int32_t)((pos << 16) | cnt)};
-            pos += cnt;
-            if (pos > 65534) throw std::runtime_error("super-voxel band exceeds 65534 rows; use a smaller tile");
+            const int cnt = hi[j] >= 0 ? hi[j] - lo[j] + 1 : 0;
+            if (cnt > 255) throw std::runtime_error("super-voxel window exceeds 255 rows; use a smaller tile");
+            out.band[(size_t)sv * V + j] = {(int32_t)(j * n_ch + (cnt ? lo[j] : 0)), (int32_t)cnt};
+            wcap = std::max(wcap, cnt);
         }
-        out.bsize[sv] = pos;
-        out.max_band = std::max(out.max_band, pos);
-        sv_entries[sv] = ent;
-        total += ent;
     }
-    if (total >= (int64_t)1 << 31) throw std::runtime_error("super-voxel layout exceeds 2^31 entries per agent");
-    out.idx.assign(total, 0);
-    out.val.assign(total, 0.0f);
-    // pass 2: entries, SV-major, pixels in tile-raster order, band-local indices.
-    // Within a column, entries are stored in groups of 128 (16 lanes x 8 slots); inside
-    // a group of Lg entries (L8 = ceil(Lg/8)) slot 8l+q holds entry l + q*L8, so lane l's
-    // two 128-bit value loads and one 128-bit index load bring entries l, l+L8, ...,
-    // l+7L8: at every step the half-warp touches consecutive entries (consecutive
-    // views' windows -> spread shared-memory banks).  Columns are padded to 8 slots.
-    // Pads carry value 0 and the tile's dummy band row B (never a real row).
-    int64_t pos = 0;
-    std::vector<uint16_t> ci;
-    std::vector<float> cv;
+    if (K > 4) throw std::runtime_error("more than 4 entries per (pixel, view): channel pitch far below pixel pitch");
+    if (S & 1) throw std::runtime_error("super-voxel side must be even");
+    out.K = K <= 2 ? 2 : 4;
+    out.wcap = wcap;
+    out.nb = sv_batches(S);
+    const int G = out.ng, KK = out.K;
+    out.rec = G * 32 * KK + 32;
+    const size_t per_tile = (size_t)out.nb * kSvBatch * out.rec;
+    out.data.assign((size_t)out.n_sv * per_tile, 0u);
+    // pass 2: scatter each entry into its (slot, group, lane, k) position
     for (int sv = 0; sv < out.n_sv; ++sv) {
         const int r0 = (sv / out.n_sv_side) * S, c0 = (sv % out.n_sv_side) * S;
         const int2_t* bt = &out.band[(size_t)sv * V];
-        const uint16_t dummy = (uint16_t)out.bsize[sv];
-        for (int k = 0; k < S * S; ++k) {
+        for (int t = 0; t < out.nb * kSvBatch; ++t) {
+            const int k = sv_slot_pixel(S, t);
+            if (k < 0) continue;
             const int r = r0 + k / S, c = c0 + k % S;
-            if (r >= n_side || c >= n_side) {
-                out.pix[(size_t)sv * S * S + k] = {(int32_t)pos, 0};
-                continue;
-            }
+            if (r >= n_side || c >= n_side) continue;
             const int64_t s = (int64_t)r * n_side + c;
-            ci.clear();
-            cv.clear();
+            uint32_t* rec = &out.data[(size_t)sv * per_tile + (size_t)t * out.rec];
+            float* pv = reinterpret_cast<float*>(rec);
+            uint32_t* po = rec + G * 32 * KK;
+            std::fill(cntpv.begin(), cntpv.end(), 0);
             uint32_t prev = UINT32_MAX;
             for (int64_t q = csc.col_ptr[s]; q < csc.col_ptr[s + 1]; ++q) {
                 const uint32_t row = csc.row[q];
-                if (row == prev) {  // merge duplicate entry (sum of lengths)
-                    cv.back() += csc.val[q];
+                const int j = (int)(row / n_ch);
+                const int g = j >> 5, l = j & 31;
+                if (row == prev) {  // merge a duplicate (row, pixel) entry
+                    pv[((size_t)g * 32 + l) * KK + (cntpv[j] - 1)] += csc.val[q];
                     out.duplicates++;
                     continue;
                 }
                 prev = row;
-                const int j = (int)(row / n_ch), ch = (int)(row % n_ch);
-                const int2_t b = bt[j];
-                ci.push_back((uint16_t)((b.y >> 16) + (j * n_ch + ch - b.x)));
-                cv.push_back(csc.val[q]);
+                const int o = (int)row - bt[j].x;  // offset of this entry in view j's window
+                if (cntpv[j] == 0) po[l] |= (uint32_t)o << (8 * g);
+                pv[((size_t)g * 32 + l) * KK + cntpv[j]] = csc.val[q];
+                cntpv[j]++;
+                out.entries++;
             }
-            const int L = (int)ci.size();
-            for (int g0 = 0; g0 < std::max(L, 1); g0 += 128) {
-                const int Lg = std::min(128, L - g0), L8 = (std::max(Lg, 0) + 7) / 8;
-                for (int l = 0; l < L8; ++l)
-                    for (int q = 0; q < 8; ++q) {
-                        const int e = l + q * L8;
-                        const int64_t slot = pos + g0 + 8 * l + q;
-                        out.idx[slot] = e < Lg ? ci[g0 + e] : dummy;
-                        out.val[slot] = e < Lg ? cv[g0 + e] : 0.0f;
-                    }
-            }
-            out.pix[(size_t)sv * S * S + k] = {(int32_t)pos, (int32_t)L};
-            pos += pad8(L);
         }
     }
 }

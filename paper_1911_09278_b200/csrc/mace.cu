@@ -63,12 +63,11 @@ struct DBuf {
 struct AgentMem {
     std::vector<int> views;
     DBuf<int> d_views;
-    DBuf<int2> band, pix, rpix;
-    DBuf<int> bsize;
-    DBuf<float> val, rval;
-    DBuf<uint16_t> idx;
-    DBuf<uint32_t> ridx;
-    int R = 0, n_sv_side = 0, n_sv = 0, max_band = 0, max_col = 0;
+    DBuf<int2> band, rpix;
+    DBuf<float> rval;
+    DBuf<uint32_t> rec, ridx;
+    int R = 0, n_sv_side = 0, n_sv = 0, max_col = 0;
+    int wcap = 0, ng = 1, K = 2, nb = 0, rec_words = 0;  // lane-per-view layout geometry
     int64_t entries = 0, nnz = 0, duplicates = 0;
     DBuf<uint32_t> queue;  // this agent alone, colour order
     float beta_eff = 0.f, inv_s2 = 0.f;
@@ -95,7 +94,8 @@ struct Ctx {
     DBuf<AgentDev> d_agents;
     DBuf<int> row_base;
     int total_rows = 0;
-    DBuf<float2> EL;
+    DBuf<float> E, LAM;  // error sinograms, weights (per local agent rows)
+    DBuf<float> BC;      // super-voxel batch constants (per local agent, k_sv_consts)
     DBuf<float> Y, Z, W, TH, VT;
     DBuf<uint32_t> queue;
     int n_items = 0;
@@ -108,13 +108,11 @@ struct Ctx {
     DBuf<float> wbar, g, ref, wsum;
     DBuf<double> refpart;
     double ref_norm2 = 0.0;
-    int band_cap = 0, view_cap = 0;
+    int sv_ng = 1, sv_wcap = 1, sv_K = 2, view_cap = 0;  // lane-per-view band geometry (max over agents)
     size_t sv_smem = 0;
     int sv_grid = 0, sv_warps = 0;
     double sv_frac = 1.0 / 16.0;  // max fraction of an agent's tiles in flight
     long sv_max_warps = 0;        // optional hard cap (0: none)
-    int sv_depth = 4;             // column prefetch depth (steps ahead), 2 or 4
-    int stage_tma = 0;            // band staging: 0 LDGSTS (default), 1 TMA bulk copies
     int passes = 0;
     int num_sms = 148;
     // timing of the last iterate call
@@ -171,24 +169,27 @@ static void upload_prior_consts()
 static void sync(Ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
 
 // ------------------------------------------------------------------ K2 launch helpers
-template <int S, int D, bool P2>
+constexpr int kSvThreads = 32;
+
+template <int S, int K, int NG>
 static void launch_sv(Ctx* c, const PassParams& P, int items, int agents_in_queue)
 {
-    auto kern = k_icd_sv<S, D, P2>;
+    auto kern = k_icd_sv<S, K, NG>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sv_smem));
     int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, c->sv_smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSvThreads, c->sv_smem));
     if (nb < 1) throw std::runtime_error("super-voxel kernel does not fit on an SM (band too large)");
     // Concurrency bound: at most a fraction `sv_frac` of an agent's tiles are in flight at once
     // (bounded staleness), never fewer than one tile per agent, never more than
     // the resident warps of the whole GPU.
-    long warps = (long)nb * 4 * c->num_sms;
+    constexpr int wpb = kSvThreads / 32;
+    long warps = (long)nb * wpb * c->num_sms;
     long cap = (long)std::floor(c->sv_frac * (double)items);
     cap = std::max<long>(cap, agents_in_queue);
     if (c->sv_max_warps > 0) cap = std::min<long>(cap, c->sv_max_warps);
     warps = std::max(1L, std::min(warps, cap));
-    const int threads = warps >= 4 ? 128 : (int)warps * 32;
-    const long grid = warps >= 4 ? warps / 4 : 1;
+    const int threads = warps >= wpb ? kSvThreads : (int)warps * 32;
+    const long grid = warps >= wpb ? warps / wpb : 1;
     c->sv_grid = (int)grid;
     c->sv_warps = (int)(grid * threads / 32);
     kern<<<(int)grid, threads, c->sv_smem, c->stream>>>(P);
@@ -202,17 +203,28 @@ static void launch_raster(Ctx* c, const PassParams& P, int n_agents, int agent_b
     CK(cudaGetLastError());
 }
 
-template <int D, bool P2>
+template <int K, int NG>
 static void dispatch_sv(Ctx* c, const PassParams& P, int na)
 {
     switch (c->S) {
-        case 2: launch_sv<2, D, P2>(c, P, P.n_items, na); break;
-        case 4: launch_sv<4, D, P2>(c, P, P.n_items, na); break;
-        case 6: launch_sv<6, D, P2>(c, P, P.n_items, na); break;
-        case 8: launch_sv<8, D, P2>(c, P, P.n_items, na); break;
-        case 12: launch_sv<12, D, P2>(c, P, P.n_items, na); break;
-        case 16: launch_sv<16, D, P2>(c, P, P.n_items, na); break;
+        case 2: launch_sv<2, K, NG>(c, P, P.n_items, na); break;
+        case 4: launch_sv<4, K, NG>(c, P, P.n_items, na); break;
+        case 6: launch_sv<6, K, NG>(c, P, P.n_items, na); break;
+        case 8: launch_sv<8, K, NG>(c, P, P.n_items, na); break;
+        case 12: launch_sv<12, K, NG>(c, P, P.n_items, na); break;
+        case 16: launch_sv<16, K, NG>(c, P, P.n_items, na); break;
         default: throw std::runtime_error("super-voxel side must be one of 2, 4, 6, 8, 12, 16");
+    }
+}
+
+template <int K>
+static void dispatch_sv_ng(Ctx* c, const PassParams& P, int na)
+{
+    switch (c->sv_ng) {
+        case 1: dispatch_sv<K, 1>(c, P, na); break;
+        case 2: dispatch_sv<K, 2>(c, P, na); break;
+        case 3: dispatch_sv<K, 3>(c, P, na); break;
+        default: dispatch_sv<K, 4>(c, P, na); break;
     }
 }
 
@@ -223,9 +235,9 @@ static PassParams base_params(Ctx* c)
     P.pr = c->prior;
     P.n_side = c->n_side;
     P.S = c->S;
-    P.band_cap = c->band_cap;
+    P.ng = c->sv_ng;
+    P.wcap = c->sv_wcap;
     P.view_cap = c->view_cap;
-    P.stage_tma = c->stage_tma;
     P.head = c->head.p;
     P.part = c->part.p;
     P.done = c->done.p;
@@ -263,14 +275,8 @@ static void run_pass(Ctx* c, int mode, float rho, const float* gimg, int a0, int
         P.queue = c->am[a0]->queue.p;
         P.n_items = c->am[a0]->n_sv;
     }
-    const bool p2 = c->prior.kind == 0 || c->prior.p_is_2;
-    if (c->sv_depth <= 2) {
-        if (p2) dispatch_sv<2, true>(c, P, na);
-        else dispatch_sv<2, false>(c, P, na);
-    } else {
-        if (p2) dispatch_sv<4, true>(c, P, na);
-        else dispatch_sv<4, false>(c, P, na);
-    }
+    if (c->sv_K <= 2) dispatch_sv_ng<2>(c, P, na);
+    else dispatch_sv_ng<4>(c, P, na);
     k2_end(c, ev);
 }
 
@@ -297,10 +303,8 @@ static void compute_theta2(Ctx* c)
     if (c->schedule == 1) {
         k_theta2_raster<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_agents.p, c->n_local, (int)c->n);
     } else {
-        const size_t smem = (size_t)4 * c->band_cap * 4;
-        CK(cudaFuncSetAttribute(k_theta2_sv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_theta2_sv<<<std::max(1, std::min(c->num_sms * 4, (c->n_items + 3) / 4)), 128, smem, c->stream>>>(
-            c->d_agents.p, c->n_items, c->queue.p, c->n_side, c->S, c->band_cap);
+        k_sv_consts<<<std::max(1, std::min(c->num_sms * 4, (c->n_items + 3) / 4)), 128, 0, c->stream>>>(
+            c->d_agents.p, c->n_items, c->queue.p, c->n_side, c->S, c->sv_K, sv_batches(c->S));
     }
     CK(cudaGetLastError());
 }
@@ -526,6 +530,8 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
     CK(cudaMemcpy(h_cols.data(), c->cols.p, sizeof(int32_t) * c->nnz, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(h_vals.data(), c->vals.p, sizeof(float) * c->nnz, cudaMemcpyDeviceToHost));
     if (n_threads <= 0) n_threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    int ng_all = 1;  // one record geometry for the context (the kernel is specialised on it)
+    for (int a = 0; a < n_agents; ++a) ng_all = std::max(ng_all, ((int)c->am[a]->views.size() + 31) / 32);
     std::vector<std::exception_ptr> errs(n_agents);
     std::vector<RasterLayout> rl(n_agents);
     std::vector<SVLayout> sl(n_agents);
@@ -540,7 +546,7 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
                     build_agent_csc(c->n_side, c->n_ch, h_rp.data(), h_cols.data(), h_vals.data(), c->am[a]->views, csc);
                     c->am[a]->nnz = csc.col_ptr.back();
                     if (schedule == 1) build_raster_layout(csc, (int)c->n, rl[a]);
-                    else build_sv_layout(csc, c->n_side, c->n_ch, (int)c->am[a]->views.size(), svs, sl[a]);
+                    else build_sv_layout(csc, c->n_side, c->n_ch, (int)c->am[a]->views.size(), svs, sl[a], ng_all);
                 } catch (...) {
                     errs[a] = std::current_exception();
                 }
@@ -553,7 +559,10 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
             if (e) std::rethrow_exception(e);
     }
     // per real agent: layout on the device
-    int max_col = 0, max_band = 0, n_sv_side = 1;
+    int max_col = 0, n_sv_side = 1;
+    c->sv_ng = 1;
+    c->sv_wcap = 1;
+    c->sv_K = 2;
     for (int a = 0; a < n_agents; ++a) {
         AgentMem& m = *c->am[a];
         m.d_views.alloc(m.views.size());
@@ -575,20 +584,16 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
         } else {
             SVLayout& L = sl[a];
             m.band.alloc(L.band.size());
-            m.bsize.alloc(L.bsize.size());
-            m.pix.alloc(L.pix.size());
-            m.val.alloc(L.val.size());
-            m.idx.alloc(L.idx.size());
+            m.rec.alloc(L.data.size());
             CK(cudaMemcpy(m.band.p, L.band.data(), sizeof(int2) * L.band.size(), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(m.bsize.p, L.bsize.data(), sizeof(int) * L.bsize.size(), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(m.pix.p, L.pix.data(), sizeof(int2) * L.pix.size(), cudaMemcpyHostToDevice));
-            if (L.val.size()) {
-                CK(cudaMemcpy(m.val.p, L.val.data(), sizeof(float) * L.val.size(), cudaMemcpyHostToDevice));
-                CK(cudaMemcpy(m.idx.p, L.idx.data(), sizeof(uint16_t) * L.idx.size(), cudaMemcpyHostToDevice));
-            }
-            m.entries = (int64_t)L.val.size();
+            CK(cudaMemcpy(m.rec.p, L.data.data(), sizeof(uint32_t) * L.data.size(), cudaMemcpyHostToDevice));
+            m.nb = L.nb;
+            m.rec_words = L.rec;
+            m.entries = L.entries;
             m.max_col = L.max_col;
-            m.max_band = L.max_band;
+            m.wcap = L.wcap;
+            m.ng = L.ng;
+            m.K = L.K;
             m.n_sv = L.n_sv;
             m.n_sv_side = L.n_sv_side;
             m.duplicates = L.duplicates;
@@ -601,7 +606,9 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
             }
         }
         max_col = std::max(max_col, m.max_col);
-        max_band = std::max(max_band, m.max_band);
+        c->sv_ng = std::max(c->sv_ng, m.ng);
+        c->sv_wcap = std::max(c->sv_wcap, m.wcap);
+        c->sv_K = std::max(c->sv_K, m.K);
     }
     // per local (virtual) agent: data arrays; each {e, lambda} block starts on a 16-byte boundary
     std::vector<int> rb(n_local + 1, 0);
@@ -609,7 +616,8 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
     c->total_rows = rb[n_local];
     c->row_base.alloc(n_local + 1);
     CK(cudaMemcpy(c->row_base.p, rb.data(), sizeof(int) * (n_local + 1), cudaMemcpyHostToDevice));
-    c->EL.alloc(c->total_rows);
+    c->E.alloc(c->total_rows);
+    c->LAM.alloc(c->total_rows);
     c->Y.alloc(c->total_rows);
     c->Z.alloc((size_t)n_local * c->n);
     c->W.alloc((size_t)n_local * c->n);
@@ -617,13 +625,20 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
     c->VT.alloc((size_t)n_local * c->n);
     CK(cudaMemset(c->Z.p, 0, sizeof(float) * n_local * c->n));
     CK(cudaMemset(c->W.p, 0, sizeof(float) * n_local * c->n));
-    CK(cudaMemset(c->EL.p, 0, sizeof(float2) * c->total_rows));
+    CK(cudaMemset(c->E.p, 0, sizeof(float) * c->total_rows));
+    CK(cudaMemset(c->LAM.p, 0, sizeof(float) * c->total_rows));
+    std::vector<size_t> bcb(n_local + 1, 0);  // batch-constant blocks: one per local agent
+    for (int va = 0; va < n_local; ++va)
+        bcb[va + 1] = bcb[va] + (size_t)c->am[va % n_agents]->n_sv * c->am[va % n_agents]->nb * 16;
+    c->BC.alloc(std::max<size_t>(bcb[n_local], 1));
+    CK(cudaMemset(c->BC.p, 0, sizeof(float) * std::max<size_t>(bcb[n_local], 1)));
     c->h_agents.assign(n_local, AgentDev{});
     for (int va = 0; va < n_local; ++va) {
         const int a = va % n_agents;
         AgentMem& m = *c->am[a];
         AgentDev& A = c->h_agents[va];
-        A.el = c->EL.p + rb[va];
+        A.e = c->E.p + rb[va];
+        A.lam = c->LAM.p + rb[va];
         A.y = c->Y.p + rb[va];
         A.z = c->Z.p + (size_t)va * c->n;
         A.w = c->W.p + (size_t)va * c->n;
@@ -637,10 +652,10 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
         A.ridx = m.ridx.p;
         A.rval = m.rval.p;
         A.band = m.band.p;
-        A.bsize = m.bsize.p;
-        A.pix = m.pix.p;
-        A.val = m.val.p;
-        A.idx = m.idx.p;
+        A.rec = m.rec.p;
+        A.bc = schedule == 0 ? c->BC.p + bcb[va] : nullptr;
+        A.ng = m.ng;
+        A.rec_words = m.rec_words;
         A.n_sv_side = m.n_sv_side;
         A.beta_eff = m.beta_eff;
         A.inv_s2 = m.inv_s2;
@@ -648,7 +663,6 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
     }
     c->NV = max_col <= 128 ? 1 : (max_col <= 256 ? 2 : 4);
     if (max_col > 512) throw std::runtime_error("column longer than 512 entries");
-    c->band_cap = (max_band + 1 + 3) & ~3;  // + the dummy row that pad slots point at
     if (schedule == 0) {
         std::vector<uint32_t> q = build_queue(n_agents, n_sv_side, colours, n_slices);
         c->queue.alloc(q.size());
@@ -657,7 +671,9 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
         int vmax = 0;
         for (int a = 0; a < n_agents; ++a) vmax = std::max(vmax, (int)c->am[a]->views.size());
         c->view_cap = (vmax + 1) & ~1;
-        c->sv_smem = 4 * sv_warp_bytes(c->S, c->band_cap, c->view_cap);
+        for (int a = 0; a < n_agents; ++a)
+            if (c->am[a]->K != c->sv_K) throw std::runtime_error("agents with different (pixel, view) slot widths");
+        c->sv_smem = (kSvThreads / 32) * sv_warp_bytes(c->S, c->sv_ng, c->sv_wcap);
         if (c->sv_smem > 227 * 1024) throw std::runtime_error("super-voxel band does not fit in shared memory");
     } else {
         c->n_items = n_local;
@@ -683,10 +699,10 @@ int mace_agent_info(void* p, int local, int64_t* info /* [8] */)
     info[1] = m.entries;
     info[2] = m.R;
     info[3] = m.max_col;
-    info[4] = m.max_band;
+    info[4] = m.wcap;
     info[5] = m.n_sv;
     info[6] = m.duplicates;
-    info[7] = c->band_cap;
+    info[7] = c->sv_wcap;
     API_END
 }
 
@@ -712,8 +728,6 @@ int mace_set_schedule(void* p, double concurrency, int64_t max_warps)
     if (!(concurrency > 0.0) || concurrency > 1.0) throw std::runtime_error("concurrency must be in (0, 1]");
     c->sv_frac = concurrency;
     c->sv_max_warps = (long)max_warps;
-    if (const char* d = std::getenv("MACE_SV_DEPTH")) c->sv_depth = std::atoi(d) <= 2 ? 2 : 4;
-    if (const char* t = std::getenv("MACE_SV_STAGE")) c->stage_tma = std::string(t) == "tma";
     API_END
 }
 
@@ -787,7 +801,7 @@ int mace_get_error(void* p, int local, float* e)
     API_BEGIN
     Ctx* c = C(p);
     const AgentDev& A = c->h_agents.at(local);
-    CK(cudaMemcpy2DAsync(e, sizeof(float), A.el, sizeof(float2), sizeof(float), A.R, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(e, A.e, sizeof(float) * A.R, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     API_END
 }
@@ -1191,32 +1205,39 @@ int mace_sv_layout_probe(int n_side, int n_ch, int n_views, const int64_t* row_p
     SVLayout L;
     build_sv_layout(csc, n_side, n_ch, n_agent_views, svs, L);
     int64_t k = 0;
-    const int S = L.svs;
+    const int S = L.svs, G = L.ng, KK = L.K;
+    const size_t per_tile = (size_t)L.nb * kSvBatch * L.rec;
     for (int sv = 0; sv < L.n_sv; ++sv) {
         const int r0 = (sv / L.n_sv_side) * S, c0 = (sv % L.n_sv_side) * S;
         const int2_t* bt = &L.band[(size_t)sv * L.views];
-        for (int q = 0; q < S * S; ++q) {
-            const int2_t pe = L.pix[(size_t)sv * S * S + q];
-            const int B = L.bsize[sv];
-            for (int e = 0; e < ((pe.y + 7) & ~7); ++e) {
-                const int li = L.idx[pe.x + e];
-                if (li == B) {  // pad slot
-                    if (L.val[pe.x + e] != 0.0f) throw std::runtime_error("pad slot with a value");
-                    continue;
+        std::vector<int> seen(S * S, 0);
+        for (int t = 0; t < L.nb * kSvBatch; ++t) {
+            const uint32_t* rec = &L.data[(size_t)sv * per_tile + (size_t)t * L.rec];
+            const int q = sv_slot_pixel(S, t);
+            if (q >= 0) seen[q]++;
+            for (int j = 0; j < L.views; ++j) {
+                const int g = j >> 5, l = j & 31;
+                const int o = (int)((rec[G * 32 * KK + l] >> (8 * g)) & 0xffu);
+                for (int e = 0; e < KK; ++e) {
+                    float a;
+                    std::memcpy(&a, &rec[((size_t)g * 32 + l) * KK + e], 4);
+                    if (a == 0.0f) continue;
+                    if (q < 0) throw std::runtime_error("padding slot with a value");
+                    if (o + e >= bt[j].y) throw std::runtime_error("slot outside its band window");
+                    if (pix_out) {
+                        pix_out[k] = (r0 + q / S) * n_side + (c0 + q % S);
+                        row_out[k] = bt[j].x + o + e;
+                        val_out[k] = a;
+                    }
+                    ++k;
                 }
-                int j = 0;
-                while (!(bt[j].y & 0xffff) || li >= (bt[j].y >> 16) + (bt[j].y & 0xffff) || li < (bt[j].y >> 16)) ++j;
-                if (pix_out) {
-                    pix_out[k] = (r0 + q / S) * n_side + (c0 + q % S);
-                    row_out[k] = bt[j].x + (li - (bt[j].y >> 16));
-                    val_out[k] = L.val[pe.x + e];
-                }
-                ++k;
             }
         }
+        for (int q = 0; q < S * S; ++q)
+            if (seen[q] != 1) throw std::runtime_error("visit order does not cover the tile once");
     }
-    stats[0] = (int64_t)L.val.size();
-    stats[1] = L.max_band;
+    stats[0] = (int64_t)L.data.size();
+    stats[1] = L.wcap;
     stats[2] = L.max_col;
     stats[3] = L.n_sv;
     stats[4] = L.duplicates;

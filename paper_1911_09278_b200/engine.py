@@ -163,7 +163,7 @@ class AgentPlan(_Context):
     def agent_info(self, a):
         buf = np.zeros(8, np.int64)
         self.call("mace_agent_info", int(a), N.ptr(buf))
-        return dict(zip(["nnz", "entries", "R", "max_col", "max_band", "n_sv", "duplicates", "band_cap"],
+        return dict(zip(["nnz", "entries", "R", "max_col", "wcap", "n_sv", "duplicates", "ctx_wcap"],
                         buf.tolist()))
 
     def load_data(self, y, weights):

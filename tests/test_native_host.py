@@ -133,7 +133,7 @@ def test_sv_layout_is_lossless_repacking(ns, nv, nc, Nsub, svs):
         got = sorted(zip(pix.tolist(), row.tolist(), val.tolist()))
         assert stats[4] == 0  # no duplicate (row, pixel) entries in the reference matrices
         assert got == want
-        assert stats[0] % 4 == 0 and stats[1] < 65536
+        assert stats[0] % 64 == 0 and 0 < stats[1] <= 255  # lane slots; widest band window
 
 
 def test_bad_views_rejected():
