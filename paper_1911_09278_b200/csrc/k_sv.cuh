@@ -30,6 +30,10 @@ namespace mace {
 constexpr int kMaxGroups = 4;  // <= 128 views per agent
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async4(void* dst, const void* src)
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
@@ -41,12 +45,13 @@ __device__ __forceinline__ void cp_async_wait()
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// shared-memory bytes per warp: the e, lambda and e0 band planes, the state tile with
-// halo, and per-pixel v and w
+// shared-memory bytes per warp: the band (per row unit u = g W + o: e, lambda and e0 as three
+// 32-word lane vectors at word 96 u), the state tile with halo, and per-pixel v and w
 __host__ __device__ constexpr size_t sv_warp_bytes(int S, int ng, int wcap)
 {
     return 12 * (size_t)ng * wcap * 32 + 4 * (size_t)((((S + 2) * (S + 2)) + 3) & ~3) + 8 * (size_t)S * S;
 }
+__host__ __device__ constexpr int sv_rec_words(int ng, int K) { return ng * 32 * K + 32; }
 
 __device__ __forceinline__ float fast_exp2(float x)
 {
@@ -90,27 +95,30 @@ struct SvBatch {
 
 template <int K, int NG>
 __device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __restrict__ r,
-                                           const float* __restrict__ bk, int recw, int lane)
+                                           const float* __restrict__ bk, int lane)
 {
+    constexpr int RECW = sv_rec_words(NG, K);
+    r += lane * K;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
-            const uint32_t* q = r + p * recw + (g * 32 + lane) * K;
+            const uint32_t* q = r + p * RECW + g * 32 * K;
             if constexpr (K == 2) {
                 asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];"
                     : "=f"(B.a[p][g][0]), "=f"(B.a[p][g][1])
                     : "l"(q));
             } else {
-                const float4 v = __ldg(reinterpret_cast<const float4*>(q));
-                B.a[p][g][0] = v.x;
-                B.a[p][g][1] = v.y;
-                B.a[p][g][2] = v.z;
-                B.a[p][g][3] = v.w;
+                asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                    : "=f"(B.a[p][g][0]), "=f"(B.a[p][g][1]), "=f"(B.a[p][g][2]), "=f"(B.a[p][g][3])
+                    : "l"(q));
             }
         }
-        asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(B.ob[p]) : "l"(r + p * recw + NG * 32 * K + lane));
     }
+    r += lane - lane * K;
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+        asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(B.ob[p]) : "l"(r + p * RECW + NG * 32 * K));
     B.k0 = __ldg(reinterpret_cast<const float4*>(bk));
     B.k1 = __ldg(reinterpret_cast<const float4*>(bk) + 1);
     B.k2 = __ldg(reinterpret_cast<const float4*>(bk) + 2);
@@ -123,13 +131,13 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
     if (P.done && *P.done) return;
     constexpr int SS = S * S, S2 = S + 2, T2 = S2 * S2, T2p = (T2 + 3) & ~3;
     constexpr int H = S / 2, PER_CLASS = H * H, BPC = (PER_CLASS + 3) / 4, NB = 4 * BPC;
+    constexpr int RECW = sv_rec_words(NG, K);
+    constexpr int U = 96;  // words per band row unit: e | lambda | e0
     const int lane = threadIdx.x & 31;
     const int W = P.wcap;
     unsigned char* base = smem + (threadIdx.x >> 5) * sv_warp_bytes(S, NG, W);
-    float* se = reinterpret_cast<float*>(base);  // band planes, row R = (g W + o) 32 + lane
-    float* sl = se + NG * W * 32;                 // lambda
-    float* se0 = sl + NG * W * 32;                // e at staging time
-    float* zt = se0 + NG * W * 32;
+    float* sb = reinterpret_cast<float*>(base);  // band: e at U u + lane, lambda +32, e0 +64
+    float* zt = sb + NG * W * U;
     float* svv = zt + T2p;
     float* swo = svv + SS;
     const int n = P.n_side;
@@ -140,6 +148,7 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
     const int pp = lane >> 3;
     const int ndr = c_dr[kk], ndc = c_dc[kk];
     const float nwk = c_nw[kk];
+    const int nofs = ndr * S2 + ndc;
 
     for (;;) {
         unsigned item = 0;
@@ -152,45 +161,44 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
         float* __restrict__ eg = A.e;
         float* __restrict__ z = A.z;
         float* __restrict__ w = A.w;
-        const int V = A.V, recw = A.rec_words;
-        constexpr int ng = NG;  // dispatch guarantees A.ng == NG
+        const int V = A.V;
         const int nsv = A.n_sv_side;
         const int r0 = (sv / nsv) * S, c0 = (sv % nsv) * S;
+        const bool full = r0 + S <= n && c0 + S <= n;  // interior tile: no image-edge checks
         const float beta = A.beta_eff, inv_s2 = A.inv_s2;
         const int clamp = A.clamp;
-        const uint32_t* __restrict__ recs = A.rec + (size_t)sv * NB * 4 * recw;
+        const uint32_t* __restrict__ recs = A.rec + (size_t)sv * NB * 4 * RECW;
         const float* __restrict__ bcs = A.bc + (size_t)sv * NB * 16;
 
         // -- 1. band windows of this lane's views -> its own bank (cp.async; zero past the window)
-        int2 myb[kMaxGroups];
+        int2 myb[NG];
 #pragma unroll
-        for (int g = 0; g < kMaxGroups; ++g) {
+        for (int g = 0; g < NG; ++g) {
             const int j = 32 * g + lane;
-            myb[g] = (g < ng && j < V) ? __ldg(A.band + (size_t)sv * V + j) : make_int2(0, 0);
+            myb[g] = j < V ? __ldg(A.band + (size_t)sv * V + j) : make_int2(0, 0);
         }
+        // e windows: 16-byte loads over the aligned span of each window (a lane's window is one
+        // contiguous run of rows; the loads of one instruction hit 32 different lines)
+        constexpr int EV = 6;  // float4 loads per group in flight (windows up to 21 rows)
+        float4 ew[NG][EV];
+        int sh[NG];
 #pragma unroll
-        for (int g = 0; g < kMaxGroups; ++g) {
-            if (g >= ng) break;
-            const int cnt = myb[g].y;
-            const float* ep = eg + myb[g].x;
-            const float* lp = A.lam + myb[g].x;
-            for (int o = 0; o < W; ++o) {
-                const int R = (g * W + o) * 32 + lane;
-                if (o < cnt) {
-                    cp_async4(se + R, ep + o);
-                    cp_async4(sl + R, lp + o);
-                    cp_async4(se0 + R, ep + o);
-                } else {
-                    se[R] = 0.f;
-                    sl[R] = 0.f;
-                    se0[R] = 0.f;
-                }
-            }
+        for (int g = 0; g < NG; ++g) {
+            const int st = myb[g].x, cnt = myb[g].y;
+            sh[g] = st & 3;
+            const float4* ep = reinterpret_cast<const float4*>(eg + (st - sh[g]));
+            const int nv = (cnt + sh[g] + 3) >> 2;
+#pragma unroll
+            for (int v = 0; v < EV; ++v) ew[g][v] = v < nv ? __ldcg(ep + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        {  // lambda: pre-arranged per tile (k_sv_consts) as [u][32]; 16-byte copies into the units
+            const float* lsrc = A.lb + (size_t)sv * NG * W * 32;
+            for (int c = lane; c < NG * W * 8; c += 32) cp_async16(sb + (c >> 3) * U + 32 + 4 * (c & 7), lsrc + 4 * c);
         }
         cp_async_commit();
         // -- 2. first batch of records
         SvBatch<K, NG> cur, nxt;
-        load_batch<K, NG>(cur, recs, bcs, recw, lane);
+        load_batch<K, NG>(cur, recs, bcs, lane);
         // -- 3. tile state + halo, w and v = 2 G(w) - w
 #pragma unroll
         for (int i0 = 0; i0 < T2p; i0 += 32) {
@@ -218,31 +226,60 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
         }
 
         // -- 4. batches of four same-parity pixels
-        double dsq = 0.0;
-        cp_async_wait<0>();  // this lane's band copies have landed
-        __syncwarp();        // ... and every other lane's; zt / v / w stores visible
+        float dsq = 0.f;
+        // e and e0 planes from the registers (rows past the window are zero)
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            const int cnt = myb[g].y;
+            float* d = sb + g * W * U + lane;
+            if (W <= 4 * EV - 3) {
+#pragma unroll
+                for (int v = 0; v < EV; ++v) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int o = 4 * v + i - sh[g];
+                        if (o >= 0 && o < W) {
+                            const float xi = i == 0 ? ew[g][v].x : i == 1 ? ew[g][v].y : i == 2 ? ew[g][v].z : ew[g][v].w;
+                            const float x = o < cnt ? xi : 0.f;
+                            d[o * U] = x;
+                            d[o * U + 64] = x;
+                        }
+                    }
+                }
+            } else {  // wide windows: plain row loads
+                for (int o = 0; o < W; ++o) {
+                    const float x = o < cnt ? __ldcg(eg + myb[g].x + o) : 0.f;
+                    d[o * U] = x;
+                    d[o * U + 64] = x;
+                }
+            }
+        }
+        cp_async_wait<0>();  // this lane's lambda copies have landed
+        __syncwarp();        // ... and every other lane's; band / zt / v / w stores visible
 #pragma unroll 1
         for (int b = 0; b < NB; ++b) {
-            if (b + 1 < NB) load_batch<K, NG>(nxt, recs + (size_t)(b + 1) * 4 * recw, bcs + (size_t)(b + 1) * 16, recw, lane);
+            if (b + 1 < NB) load_batch<K, NG>(nxt, recs + (size_t)(b + 1) * 4 * RECW, bcs + (size_t)(b + 1) * 16, lane);
             const float bk[10] = {cur.k0.x, cur.k0.y, cur.k0.z, cur.k0.w, cur.k1.x,
                                   cur.k1.y, cur.k1.z, cur.k1.w, cur.k2.x, cur.k2.y};
+            // local pixel (lr, lc) of slot p; ok = real and inside the image
             const int cls = b / BPC, ib = (b % BPC) * 4;
-            // local pixel of slot p; -1 for padding or off-image slots
-            int loc[4];
+            int kx[4];
+            bool ok[4];
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 const int i = ib + p;
                 const int lr = (cls >> 1) + 2 * (i / H), lc = (cls & 1) + 2 * (i % H);
-                loc[p] = (i < PER_CLASS && r0 + lr < n && c0 + lc < n) ? lr * S + lc : -1;
+                kx[p] = lr * S + lc;
+                ok[p] = (PER_CLASS % 4 == 0 || i < PER_CLASS) && (full || (r0 + lr < n && c0 + lc < n));
             }
             // theta1 partials against the band as it stands before the batch
             float num[4];
-            int addr[4][NG];
+            int ab[4][NG];
             const auto& av = cur.a;
 #pragma unroll
             for (int p = 0; p < 4; ++p)
 #pragma unroll
-                for (int g = 0; g < NG; ++g) addr[p][g] = (g * W + (int)((cur.ob[p] >> (8 * g)) & 0xffu)) * 32 + lane;
+                for (int g = 0; g < NG; ++g) ab[p][g] = (g * W + (int)((cur.ob[p] >> (8 * g)) & 0xffu)) * U + lane;
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 float a0 = 0.f, a1 = 0.f;
@@ -250,7 +287,7 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
                 for (int g = 0; g < NG; ++g)
 #pragma unroll
                     for (int q = 0; q < K; ++q) {
-                        const float ee = se[addr[p][g] + q * 32], ll = sl[addr[p][g] + q * 32];
+                        const float ee = sb[ab[p][g] + q * U], ll = sb[ab[p][g] + q * U + 32];
                         if (q & 1) a1 = fmaf(av[p][g][q] * ll, ee, a1);
                         else a0 = fmaf(av[p][g][q] * ll, ee, a0);
                     }
@@ -259,14 +296,16 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
             // prior of batch pixel pp, neighbour kk (independent across the batch)
             float den_l;
             {
-                const int lp = pp == 0 ? loc[0] : pp == 1 ? loc[1] : pp == 2 ? loc[2] : loc[3];
+                const int kl = pp == 0 ? kx[0] : pp == 1 ? kx[1] : pp == 2 ? kx[2] : kx[3];
+                const bool okl = pp == 0 ? ok[0] : pp == 1 ? ok[1] : pp == 2 ? ok[2] : ok[3];
                 float g = 0.f, c = 0.f;
-                if (lp >= 0 && beta > 0.f) {
-                    const int lr = lp / S, lc = lp % S;
+                if (okl && beta > 0.f) {
+                    const int lr = kl / S, lc = kl % S;
                     const int gr = r0 + lr + ndr, gc = c0 + lc + ndc;
                     const bool valid = gr >= 0 && gr < n && gc >= 0 && gc < n;
                     const float wk = valid ? nwk : 0.f;
-                    const float d = zt[(lr + 1) * S2 + lc + 1] - zt[(lr + 1 + ndr) * S2 + (lc + 1 + ndc)];
+                    const int ci = (lr + 1) * S2 + lc + 1;
+                    const float d = zt[ci] - zt[ci + nofs];
                     if (quad) {
                         g = wk * d;
                         c = wk;
@@ -291,8 +330,8 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 const float den_p = __shfl_sync(FULL, den_l, 8 * p);
-                const int k = loc[p];
-                const float zs = k >= 0 ? zt[(k / S + 1) * S2 + k % S + 1] : 0.f;
+                const int ci = (kx[p] / S + 1) * S2 + kx[p] % S + 1;
+                const float zs = zt[ci];
                 float nm = num[p], dn = den_p + bk[p] + inv_s2;
                 // coupling to the earlier pixels of the batch (exact Gauss-Seidel order)
                 if (p >= 1) nm -= alpha[0] * bk[4 + p - 1];   // c01, c02, c03
@@ -302,13 +341,13 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
                     nm -= beta * PR.eps2 * zs;
                     dn += beta * PR.eps2;
                 }
-                nm -= inv_s2 * (zs - (k >= 0 ? svv[k] : 0.f));
+                nm -= inv_s2 * (zs - svv[kx[p]]);
                 // 1-D solve (icd.py:128-134); the reference skips pixels with den <= 0
-                float al = (k >= 0 && dn > 0.f) ? __fdividef(nm, dn) : 0.f;
+                float al = (ok[p] && dn > 0.f) ? __fdividef(nm, dn) : 0.f;
                 if (clamp && zs + al < 0.f) al = -zs;
                 alpha[p] = al;
-                if (k >= 0 && lane == p) zt[(k / S + 1) * S2 + k % S + 1] = zs + al;
-                dsq += (double)al * al;
+                if (lane == p && ok[p]) zt[ci] = zs + al;
+                dsq = fmaf(al, al, dsq);
             }
             // scatter e -= alpha_p a_p in pixel order (a row may be shared within the batch, never
             // within one pixel: load a pixel's rows, then store them)
@@ -318,11 +357,11 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
 #pragma unroll
                 for (int g = 0; g < NG; ++g)
 #pragma unroll
-                    for (int q = 0; q < K; ++q) ev[g][q] = se[addr[p][g] + q * 32];
+                    for (int q = 0; q < K; ++q) ev[g][q] = sb[ab[p][g] + q * U];
 #pragma unroll
                 for (int g = 0; g < NG; ++g)
 #pragma unroll
-                    for (int q = 0; q < K; ++q) se[addr[p][g] + q * 32] = fmaf(-alpha[p], av[p][g][q], ev[g][q]);
+                    for (int q = 0; q < K; ++q) sb[ab[p][g] + q * U] = fmaf(-alpha[p], av[p][g][q], ev[g][q]);
             }
             __syncwarp();  // zt updates visible to the next batch's prior lanes
             cur = nxt;
@@ -330,14 +369,13 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
 
         // -- 5. fold the band's net change into global e; write z, Mann, partial norms
 #pragma unroll
-        for (int g = 0; g < kMaxGroups; ++g) {
-            if (g >= ng) break;
+        for (int g = 0; g < NG; ++g) {
             const int cnt = myb[g].y;
             float* ep = eg + myb[g].x;
+            const float* d = sb + g * W * U + lane;
             for (int o = 0; o < cnt; ++o) {
-                const int R = (g * W + o) * 32 + lane;
-                const float dv = se[R] - se0[R];
-                if (dv != 0.f) atomicAdd(ep + o, dv);
+                const float dv = d[o * U] - d[o * U + 64];
+                if (dv != 0.f) asm volatile("red.global.add.f32 [%0], %1;" ::"l"(ep + o), "f"(dv) : "memory");
             }
         }
         double dw2 = 0.0, wn2 = 0.0, wo2 = 0.0;
@@ -365,7 +403,7 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
         wo2 = warp_sum_d(wo2);
         if (lane == 0) {  // dsq: every lane holds the same sum (alpha is warp-uniform)
             double* o = P.part + (size_t)item * 4;
-            o[0] = dsq;
+            o[0] = (double)dsq;
             o[1] = dw2;
             o[2] = wn2;
             o[3] = wo2;

@@ -48,6 +48,7 @@ struct AgentDev {
     const int2* band;      // [n_sv * V] {local row start, window rows}
     const uint32_t* rec;   // [n_sv][nb][4][rec_words] slot records (layout.cpp, lane-per-view)
     float* bc;             // [n_sv][nb][16] batch constants: theta2 x4, cross terms x6 (per local agent)
+    float* lb;             // [n_sv][ng][wcap][32] band lambda in shared-memory order (per local agent)
     int ng, rec_words;     // view groups ceil(V / 32); words per slot record
     // raster layout
     const int2* rpix;   // [n]
@@ -410,7 +411,7 @@ __global__ void k_theta2_raster(const AgentDev* agents, int n_agents, int n)
 // cross terms c_ij = sum_r a_ir a_jr lambda_r that couple two pixels of a batch through shared
 // rows (k_sv.cuh).  Depends on lambda only, so it is recomputed per data load.
 __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n_items, const uint32_t* queue,
-                                                   int n_side, int S, int K, int nb)
+                                                   int n_side, int S, int K, int nb, int W)
 {
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -426,6 +427,11 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
         for (int g = 0; g < 4; ++g) {
             const int j = 32 * g + lane;
             start[g] = (g < A.ng && j < A.V) ? bt[j].x : 0;
+            if (g < A.ng) {  // the band's lambda rows, laid out as the kernel's shared-memory plane
+                const int cnt = j < A.V ? bt[j].y : 0;
+                float* lb = A.lb + (((size_t)sv * A.ng + g) * W) * 32 + lane;
+                for (int o = 0; o < W; ++o) lb[o * 32] = o < cnt ? A.lam[start[g] + o] : 0.f;
+            }
         }
         for (int b = 0; b < nb; ++b) {
             const uint32_t* rb = A.rec + ((size_t)sv * nb + b) * 4 * A.rec_words;

@@ -96,6 +96,7 @@ struct Ctx {
     int total_rows = 0;
     DBuf<float> E, LAM;  // error sinograms, weights (per local agent rows)
     DBuf<float> BC;      // super-voxel batch constants (per local agent, k_sv_consts)
+    DBuf<float> LB;      // super-voxel band lambda in shared-memory order (per local agent)
     DBuf<float> Y, Z, W, TH, VT;
     DBuf<uint32_t> queue;
     int n_items = 0;
@@ -304,7 +305,7 @@ static void compute_theta2(Ctx* c)
         k_theta2_raster<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_agents.p, c->n_local, (int)c->n);
     } else {
         k_sv_consts<<<std::max(1, std::min(c->num_sms * 4, (c->n_items + 3) / 4)), 128, 0, c->stream>>>(
-            c->d_agents.p, c->n_items, c->queue.p, c->n_side, c->S, c->sv_K, sv_batches(c->S));
+            c->d_agents.p, c->n_items, c->queue.p, c->n_side, c->S, c->sv_K, sv_batches(c->S), c->sv_wcap);
     }
     CK(cudaGetLastError());
 }
@@ -612,7 +613,8 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
     }
     // per local (virtual) agent: data arrays; each {e, lambda} block starts on a 16-byte boundary
     std::vector<int> rb(n_local + 1, 0);
-    for (int va = 0; va < n_local; ++va) rb[va + 1] = rb[va] + ((c->am[va % n_agents]->R + 1) & ~1);
+    // (K2 reads e windows as aligned float4 spans, which may run up to 3 rows past R)
+    for (int va = 0; va < n_local; ++va) rb[va + 1] = rb[va] + ((c->am[va % n_agents]->R + 3) & ~3);
     c->total_rows = rb[n_local];
     c->row_base.alloc(n_local + 1);
     CK(cudaMemcpy(c->row_base.p, rb.data(), sizeof(int) * (n_local + 1), cudaMemcpyHostToDevice));
@@ -632,6 +634,10 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
         bcb[va + 1] = bcb[va] + (size_t)c->am[va % n_agents]->n_sv * c->am[va % n_agents]->nb * 16;
     c->BC.alloc(std::max<size_t>(bcb[n_local], 1));
     CK(cudaMemset(c->BC.p, 0, sizeof(float) * std::max<size_t>(bcb[n_local], 1)));
+    std::vector<size_t> lbb(n_local + 1, 0);  // band-lambda blocks
+    for (int va = 0; va < n_local; ++va)
+        lbb[va + 1] = lbb[va] + (schedule == 0 ? (size_t)c->am[va % n_agents]->n_sv * c->sv_ng * c->sv_wcap * 32 : 0);
+    c->LB.alloc(std::max<size_t>(lbb[n_local], 1));
     c->h_agents.assign(n_local, AgentDev{});
     for (int va = 0; va < n_local; ++va) {
         const int a = va % n_agents;
@@ -654,6 +660,7 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
         A.band = m.band.p;
         A.rec = m.rec.p;
         A.bc = schedule == 0 ? c->BC.p + bcb[va] : nullptr;
+        A.lb = schedule == 0 ? c->LB.p + lbb[va] : nullptr;
         A.ng = m.ng;
         A.rec_words = m.rec_words;
         A.n_sv_side = m.n_sv_side;

@@ -14,6 +14,7 @@ import tempfile
 
 rep, fn = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+extra = sys.argv[4] if len(sys.argv) > 4 else "L1 Wavefronts Shared"  # third column, summed per line
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 so = os.path.join(ROOT, "paper_1911_09278_b200", "libmace_b200.so")
 tmp = tempfile.mkdtemp()
@@ -45,8 +46,9 @@ src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_ou
 rows = list(csv.reader(io.StringIO(src)))
 h = rows[1]
 A, S, I, SRC = h.index("Address"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed"), h.index("Source")
+X = h.index(extra) if extra in h else None
 base = None
-agg_s, agg_i = collections.Counter(), collections.Counter()
+agg_s, agg_i, agg_x = collections.Counter(), collections.Counter(), collections.Counter()
 for r in rows[2:]:
     try:
         addr = int(r[A], 16)
@@ -57,7 +59,9 @@ for r in rows[2:]:
     key = off2line.get(addr - base, ("?", -1))
     agg_s[key] += float(r[S] or 0)
     agg_i[key] += float(r[I] or 0)
-ts, ti = sum(agg_s.values()), sum(agg_i.values())
+    if X is not None:
+        agg_x[key] += float(r[X] or 0)
+ts, ti, tx = sum(agg_s.values()), sum(agg_i.values()), max(sum(agg_x.values()), 1.0)
 srcfiles = {}
 def text(f, n):
     p = os.path.join(ROOT, "paper_1911_09278_b200", "csrc", f)
@@ -66,4 +70,6 @@ def text(f, n):
     L = srcfiles[f]
     return L[n - 1].strip()[:90] if 0 < n <= len(L) else ""
 for k, v in agg_s.most_common(top):
-    print(f"{v / ts * 100:5.1f}% stall {agg_i[k] / ti * 100:5.1f}% inst  {k[0]}:{k[1]:<4} {text(*k)}")
+    print(f"{v / ts * 100:5.1f}% stall {agg_i[k] / ti * 100:5.1f}% inst {agg_x[k] / tx * 100:5.1f}% x  "
+          f"{k[0]}:{k[1]:<4} {text(*k)}")
+print(f"total {extra}: {tx:.4g}")
