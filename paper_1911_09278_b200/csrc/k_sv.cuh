@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
             }
             // theta1 partials against the band as it stands before the batch
             float num[4];
+            float e0v[NG][K];  // pixel 0's rows as gathered (nothing in the batch has touched them yet)
             int ab[4][NG];
             const auto& av = cur.a;
 #pragma unroll
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
 #pragma unroll
                     for (int q = 0; q < K; ++q) {
                         const float ee = sb[ab[p][g] + q * U], ll = sb[ab[p][g] + q * U + 32];
+                        if (p == 0) e0v[g][q] = ee;
                         if (q & 1) a1 = fmaf(av[p][g][q] * ll, ee, a1);
                         else a0 = fmaf(av[p][g][q] * ll, ee, a0);
                     }
@@ -326,33 +328,52 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
                 for (int p = 0; p < 4; ++p) num[p] += __shfl_xor_sync(FULL, num[p], o);
 #pragma unroll
             for (int o = 4; o; o >>= 1) den_l += __shfl_xor_sync(FULL, den_l, o);
-            float alpha[4];
+            // the four 1-D solves (icd.py:128-134): everything but the coupling to earlier pixels of
+            // the batch is independent across p; the reference skips pixels with den <= 0
+            float nm[4], rd[4], zs[4];
+            int ci[4];
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 const float den_p = __shfl_sync(FULL, den_l, 8 * p);
-                const int ci = (kx[p] / S + 1) * S2 + kx[p] % S + 1;
-                const float zs = zt[ci];
-                float nm = num[p], dn = den_p + bk[p] + inv_s2;
-                // coupling to the earlier pixels of the batch (exact Gauss-Seidel order)
-                if (p >= 1) nm -= alpha[0] * bk[4 + p - 1];   // c01, c02, c03
-                if (p >= 2) nm -= alpha[1] * bk[7 + p - 2];   // c12, c13
-                if (p >= 3) nm -= alpha[2] * bk[9];           // c23
+                ci[p] = (kx[p] / S + 1) * S2 + kx[p] % S + 1;
+                zs[p] = zt[ci[p]];
+                float dn = den_p + bk[p] + inv_s2;
+                nm[p] = num[p];
                 if (quad && beta > 0.f) {
-                    nm -= beta * PR.eps2 * zs;
+                    nm[p] -= beta * PR.eps2 * zs[p];
                     dn += beta * PR.eps2;
                 }
-                nm -= inv_s2 * (zs - svv[kx[p]]);
-                // 1-D solve (icd.py:128-134); the reference skips pixels with den <= 0
-                float al = (ok[p] && dn > 0.f) ? __fdividef(nm, dn) : 0.f;
-                if (clamp && zs + al < 0.f) al = -zs;
+                nm[p] -= inv_s2 * (zs[p] - svv[kx[p]]);
+                rd[p] = (ok[p] && dn > 0.f) ? __fdividef(1.0f, dn) : 0.f;
+            }
+            // coupling to the earlier pixels of the batch (exact Gauss-Seidel order)
+            float alpha[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                float al = ok[p] ? nm[p] * rd[p] : 0.f;
+                if (clamp && zs[p] + al < 0.f) al = ok[p] ? -zs[p] : 0.f;
                 alpha[p] = al;
-                if (lane == p && ok[p]) zt[ci] = zs + al;
+                if (p == 0) {
+                    nm[1] -= al * bk[4];
+                    nm[2] -= al * bk[5];
+                    nm[3] -= al * bk[6];
+                } else if (p == 1) {
+                    nm[2] -= al * bk[7];
+                    nm[3] -= al * bk[8];
+                } else if (p == 2) {
+                    nm[3] -= al * bk[9];
+                }
+                if (ok[p]) zt[ci[p]] = zs[p] + al;  // every lane writes the same value: no sync needed
                 dsq = fmaf(al, al, dsq);
             }
             // scatter e -= alpha_p a_p in pixel order (a row may be shared within the batch, never
-            // within one pixel: load a pixel's rows, then store them)
+            // within one pixel): pixel 0 from the gathered values, then reload-modify-store
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
+            for (int g = 0; g < NG; ++g)
+#pragma unroll
+                for (int q = 0; q < K; ++q) sb[ab[0][g] + q * U] = fmaf(-alpha[0], av[0][g][q], e0v[g][q]);
+#pragma unroll
+            for (int p = 1; p < 4; ++p) {
                 float ev[NG][K];
 #pragma unroll
                 for (int g = 0; g < NG; ++g)
@@ -363,7 +384,6 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
 #pragma unroll
                     for (int q = 0; q < K; ++q) sb[ab[p][g] + q * U] = fmaf(-alpha[p], av[p][g][q], ev[g][q]);
             }
-            __syncwarp();  // zt updates visible to the next batch's prior lanes
             cur = nxt;
         }
 

@@ -126,7 +126,7 @@ void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SV
     if (K > 4) throw std::runtime_error("more than 4 entries per (pixel, view): channel pitch far below pixel pitch");
     if (S & 1) throw std::runtime_error("super-voxel side must be even");
     out.K = K <= 2 ? 2 : 4;
-    out.wcap = wcap;
+    out.wcap = std::max(wcap, out.K);  // a slot addresses K rows even in a shorter window
     out.nb = sv_batches(S);
     const int G = out.ng, KK = out.K;
     out.rec = G * 32 * KK + 32;
@@ -145,24 +145,38 @@ void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SV
             uint32_t* rec = &out.data[(size_t)sv * per_tile + (size_t)t * out.rec];
             float* pv = reinterpret_cast<float*>(rec);
             uint32_t* po = rec + G * 32 * KK;
-            std::fill(cntpv.begin(), cntpv.end(), 0);
+            // entries of one (pixel, view) are consecutive in the column (rows ascending); the slot
+            // offset is pulled back so that all K addressed rows stay inside the window (rows past
+            // cnt would alias the lane's next window or memory after the band)
+            int cur_j = -1, m = 0, o0 = 0;
+            float vals[4] = {0.f, 0.f, 0.f, 0.f};
+            auto flush = [&]() {
+                if (cur_j < 0) return;
+                const int g = cur_j >> 5, l = cur_j & 31, cnt = bt[cur_j].y;
+                const int o = std::min(o0, std::max(cnt, KK) - KK);
+                po[l] |= (uint32_t)o << (8 * g);
+                for (int u = 0; u < m; ++u) pv[((size_t)g * 32 + l) * KK + (o0 - o) + u] = vals[u];
+                out.entries += m;
+            };
             uint32_t prev = UINT32_MAX;
             for (int64_t q = csc.col_ptr[s]; q < csc.col_ptr[s + 1]; ++q) {
                 const uint32_t row = csc.row[q];
                 const int j = (int)(row / n_ch);
-                const int g = j >> 5, l = j & 31;
                 if (row == prev) {  // merge a duplicate (row, pixel) entry
-                    pv[((size_t)g * 32 + l) * KK + (cntpv[j] - 1)] += csc.val[q];
+                    vals[m - 1] += csc.val[q];
                     out.duplicates++;
                     continue;
                 }
                 prev = row;
-                const int o = (int)row - bt[j].x;  // offset of this entry in view j's window
-                if (cntpv[j] == 0) po[l] |= (uint32_t)o << (8 * g);
-                pv[((size_t)g * 32 + l) * KK + cntpv[j]] = csc.val[q];
-                cntpv[j]++;
-                out.entries++;
+                if (j != cur_j) {
+                    flush();
+                    cur_j = j;
+                    m = 0;
+                    o0 = (int)row - bt[j].x;  // offset of the first entry in view j's window
+                }
+                vals[m++] = csc.val[q];
             }
+            flush();
         }
     }
 }
