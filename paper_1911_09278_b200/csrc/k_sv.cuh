@@ -150,18 +150,54 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
     const float nwk = c_nw[kk];
     const int nofs = ndr * S2 + ndc;
 
+    // work items are pipelined one ahead: the next item's index and code are in flight during the
+    // current tile
+    // float4 loads per group: a window of a parallel-beam tile spans about S sqrt 2 + 2 channels at
+    // channel pitch = pixel pitch, plus up to 3 rows of alignment; wider windows take the slow path
+    constexpr int EV = (S * 1414 / 1000 + 8) / 4;
+    auto fetch_item = [&]() {
+        unsigned it = 0;
+        if (lane == 0) it = atomicAdd(P.head, 1u);
+        return __shfl_sync(FULL, it, 0);
+    };
+    auto band_of = [&](uint32_t cd, int2 (&mb)[NG]) {
+        const AgentDev& An = P.agents[cd >> kAgentShift];
+        const int svn = (int)(cd & kSvMask), Vn = An.V;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            const int j = 32 * g + lane;
+            mb[g] = j < Vn ? __ldg(An.band + (size_t)svn * Vn + j) : make_int2(0, 0);
+        }
+    };
+    // e windows: 16-byte loads over the aligned span of each window (a lane's window is one
+    // contiguous run of rows; the loads of one instruction hit 32 different lines)
+    auto ewin_of = [&](uint32_t cd, const int2 (&mb)[NG], float4 (&ev4)[NG][EV], int (&shf)[NG]) {
+        const float* en = P.agents[cd >> kAgentShift].e;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            const int st = mb[g].x, cnt = mb[g].y;
+            shf[g] = st & 3;
+            const float4* ep = reinterpret_cast<const float4*>(en + (st - shf[g]));
+            const int nv = (cnt + shf[g] + 3) >> 2;
+#pragma unroll
+            for (int v = 0; v < EV; ++v) ev4[g][v] = v < nv ? __ldcg(ep + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    unsigned item = fetch_item();
+    if (item >= (unsigned)P.n_items) return;
+    uint32_t code = __ldg(P.queue + item);
+    int2 myb[NG];
+    float4 ew[NG][EV];
+    int sh[NG];
+    band_of(code, myb);
+    ewin_of(code, myb, ew, sh);
+
     for (;;) {
-        unsigned item = 0;
-        if (lane == 0) item = atomicAdd(P.head, 1u);
-        item = __shfl_sync(FULL, item, 0);
-        if (item >= (unsigned)P.n_items) break;
-        const uint32_t code = __ldg(P.queue + item);
         const AgentDev& A = P.agents[code >> kAgentShift];
         const int sv = (int)(code & kSvMask);
         float* __restrict__ eg = A.e;
         float* __restrict__ z = A.z;
         float* __restrict__ w = A.w;
-        const int V = A.V;
         const int nsv = A.n_sv_side;
         const int r0 = (sv / nsv) * S, c0 = (sv % nsv) * S;
         const bool full = r0 + S <= n && c0 + S <= n;  // interior tile: no image-edge checks
@@ -169,28 +205,12 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
         const int clamp = A.clamp;
         const uint32_t* __restrict__ recs = A.rec + (size_t)sv * NB * 4 * RECW;
         const float* __restrict__ bcs = A.bc + (size_t)sv * NB * 16;
+        // next item
+        const unsigned nitem = fetch_item();
+        const bool more = nitem < (unsigned)P.n_items;
+        const uint32_t ncode = more ? __ldg(P.queue + nitem) : 0u;
 
-        // -- 1. band windows of this lane's views -> its own bank (cp.async; zero past the window)
-        int2 myb[NG];
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-            const int j = 32 * g + lane;
-            myb[g] = j < V ? __ldg(A.band + (size_t)sv * V + j) : make_int2(0, 0);
-        }
-        // e windows: 16-byte loads over the aligned span of each window (a lane's window is one
-        // contiguous run of rows; the loads of one instruction hit 32 different lines)
-        constexpr int EV = 6;  // float4 loads per group in flight (windows up to 21 rows)
-        float4 ew[NG][EV];
-        int sh[NG];
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-            const int st = myb[g].x, cnt = myb[g].y;
-            sh[g] = st & 3;
-            const float4* ep = reinterpret_cast<const float4*>(eg + (st - sh[g]));
-            const int nv = (cnt + sh[g] + 3) >> 2;
-#pragma unroll
-            for (int v = 0; v < EV; ++v) ew[g][v] = v < nv ? __ldcg(ep + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        // -- 1. band: lambda rows by one coalesced copy, e rows from the prefetched windows
         {  // lambda: pre-arranged per tile (k_sv_consts) as [u][32]; 16-byte copies into the units
             const float* lsrc = A.lb + (size_t)sv * NG * W * 32;
             for (int c = lane; c < NG * W * 8; c += 32) cp_async16(sb + (c >> 3) * U + 32 + 4 * (c & 7), lsrc + 4 * c);
@@ -387,7 +407,8 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
             cur = nxt;
         }
 
-        // -- 5. fold the band's net change into global e; write z, Mann, partial norms
+        // -- 5. fold the band's net change into global e; prefetch the next tile's e windows;
+        // write z, Mann, partial norms
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
             const int cnt = myb[g].y;
@@ -398,6 +419,7 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
                 if (dv != 0.f) asm volatile("red.global.add.f32 [%0], %1;" ::"l"(ep + o), "f"(dv) : "memory");
             }
         }
+
         double dw2 = 0.0, wn2 = 0.0, wo2 = 0.0;
 #pragma unroll
         for (int i0 = 0; i0 < SS; i0 += 32) {
@@ -429,6 +451,11 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
             o[3] = wo2;
         }
         __syncwarp();
+        if (!more) break;
+        item = nitem;
+        code = ncode;
+        band_of(code, myb);
+        ewin_of(code, myb, ew, sh);
     }
 }
 
