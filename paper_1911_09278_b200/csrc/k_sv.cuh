@@ -84,18 +84,41 @@ __device__ __forceinline__ void qg_term(float d, float wk, const PriorC& P, floa
     }
 }
 
-// one batch of slot records in registers: lengths a[p][g][k], offset words, batch constants
-// (theta2 x4 | c01 c02 c03 c12 | c13 c23 - -)
+// one batch of slot records in registers: lengths a[p][g][k] and offset words
 template <int K, int NG>
 struct SvBatch {
     float a[4][NG][K];
     uint32_t ob[4];
-    float4 k0, k1, k2;
 };
 
+// Visit order of an S x S tile (internal.h sv_slot_pixel): per batch, the local pixel index of each
+// of the four slots as a byte (0xff: padding slot); a constant-memory table per tile side.
+template <int S>
+struct SvOrder {
+    struct Table {
+        uint32_t v[64];
+    };
+    static constexpr Table make()
+    {
+        Table t{};
+        constexpr int H = S / 2, PC = H * H, BPC = (PC + 3) / 4;
+        for (int b = 0; b < 4 * BPC; ++b) {
+            uint32_t w = 0;
+            for (int p = 0; p < 4; ++p) {
+                const int cls = b / BPC, i = (b % BPC) * 4 + p;
+                const uint32_t k = i < PC ? (uint32_t)(((cls >> 1) + 2 * (i / H)) * S + (cls & 1) + 2 * (i % H)) : 0xffu;
+                w |= k << (8 * p);
+            }
+            t.v[b] = w;
+        }
+        return t;
+    }
+};
+template <int S>
+__constant__ typename SvOrder<S>::Table c_svorder = SvOrder<S>::make();
+
 template <int K, int NG>
-__device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __restrict__ r,
-                                           const float* __restrict__ bk, int lane)
+__device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __restrict__ r, int lane)
 {
     constexpr int RECW = sv_rec_words(NG, K);
     r += lane * K;
@@ -119,13 +142,13 @@ __device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __
 #pragma unroll
     for (int p = 0; p < 4; ++p)
         asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(B.ob[p]) : "l"(r + p * RECW + NG * 32 * K));
-    B.k0 = __ldg(reinterpret_cast<const float4*>(bk));
-    B.k1 = __ldg(reinterpret_cast<const float4*>(bk) + 1);
-    B.k2 = __ldg(reinterpret_cast<const float4*>(bk) + 2);
 }
 
+#ifndef MACE_K2_MINB
+#define MACE_K2_MINB 12  // resident warps per SM the register budget is sized for
+#endif
 template <int S, int K, int NG>
-__global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
+__global__ void __launch_bounds__(32, MACE_K2_MINB) k_icd_sv(PassParams P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     if (P.done && *P.done) return;
@@ -218,7 +241,10 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
         cp_async_commit();
         // -- 2. first batch of records
         SvBatch<K, NG> cur, nxt;
-        load_batch<K, NG>(cur, recs, bcs, lane);
+        load_batch<K, NG>(cur, recs, lane);
+        // batch constants (theta2 x4 | c01 c02 c03 c12 | c13 c23 - -), 1 KB per tile: into L1 now,
+        // read per batch as broadcast loads
+        if (lane < NB / 2) asm volatile("prefetch.global.L1 [%0];" ::"l"(bcs + 32 * lane));
         // -- 3. tile state + halo, w and v = 2 G(w) - w
 #pragma unroll
         for (int i0 = 0; i0 < T2p; i0 += 32) {
@@ -276,31 +302,32 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
         }
         cp_async_wait<0>();  // this lane's lambda copies have landed
         __syncwarp();        // ... and every other lane's; band / zt / v / w stores visible
-#pragma unroll 1
-        for (int b = 0; b < NB; ++b) {
-            if (b + 1 < NB) load_batch<K, NG>(nxt, recs + (size_t)(b + 1) * 4 * RECW, bcs + (size_t)(b + 1) * 16, lane);
-            const float bk[10] = {cur.k0.x, cur.k0.y, cur.k0.z, cur.k0.w, cur.k1.x,
-                                  cur.k1.y, cur.k1.z, cur.k1.w, cur.k2.x, cur.k2.y};
-            // local pixel (lr, lc) of slot p; ok = real and inside the image
-            const int cls = b / BPC, ib = (b % BPC) * 4;
+        auto step = [&](const int b, const SvBatch<K, NG>& C, SvBatch<K, NG>& Nx) {
+            if (b + 1 < NB) load_batch<K, NG>(Nx, recs + (size_t)(b + 1) * 4 * RECW, lane);
+            const float4 k0 = __ldg(reinterpret_cast<const float4*>(bcs + 16 * b));
+            const float4 k1 = __ldg(reinterpret_cast<const float4*>(bcs + 16 * b) + 1);
+            const float2 k2 = __ldg(reinterpret_cast<const float2*>(bcs + 16 * b + 8));
+            const float bk[10] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w, k2.x, k2.y};
+            // local pixel kx = lr S + lc of slot p (visit-order table); ok = real and inside the image
+            const uint32_t kxw = c_svorder<S>.v[b];
             int kx[4];
             bool ok[4];
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
-                const int i = ib + p;
-                const int lr = (cls >> 1) + 2 * (i / H), lc = (cls & 1) + 2 * (i % H);
-                kx[p] = lr * S + lc;
-                ok[p] = (PER_CLASS % 4 == 0 || i < PER_CLASS) && (full || (r0 + lr < n && c0 + lc < n));
+                kx[p] = (int)((kxw >> (8 * p)) & 0xffu);
+                ok[p] = (PER_CLASS % 4 == 0 || kx[p] != 0xff) &&
+                        (full || (r0 + kx[p] / S < n && c0 + kx[p] % S < n));
+                if (PER_CLASS % 4 != 0 && kx[p] == 0xff) kx[p] = 0;
             }
             // theta1 partials against the band as it stands before the batch
             float num[4];
             float e0v[NG][K];  // pixel 0's rows as gathered (nothing in the batch has touched them yet)
             int ab[4][NG];
-            const auto& av = cur.a;
+            const auto& av = C.a;
 #pragma unroll
             for (int p = 0; p < 4; ++p)
 #pragma unroll
-                for (int g = 0; g < NG; ++g) ab[p][g] = (g * W + (int)((cur.ob[p] >> (8 * g)) & 0xffu)) * U + lane;
+                for (int g = 0; g < NG; ++g) ab[p][g] = (g * W + (int)((C.ob[p] >> (8 * g)) & 0xffu)) * U + lane;
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 float a0 = 0.f, a1 = 0.f;
@@ -318,8 +345,9 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
             // prior of batch pixel pp, neighbour kk (independent across the batch)
             float den_l;
             {
-                const int kl = pp == 0 ? kx[0] : pp == 1 ? kx[1] : pp == 2 ? kx[2] : kx[3];
-                const bool okl = pp == 0 ? ok[0] : pp == 1 ? ok[1] : pp == 2 ? ok[2] : ok[3];
+                int kl = (int)((kxw >> (8 * pp)) & 0xffu);
+                const bool okl = (PER_CLASS % 4 == 0 || kl != 0xff) && (full || (r0 + kl / S < n && c0 + kl % S < n));
+                if (PER_CLASS % 4 != 0 && kl == 0xff) kl = 0;
                 float g = 0.f, c = 0.f;
                 if (okl && beta > 0.f) {
                     const int lr = kl / S, lc = kl % S;
@@ -364,7 +392,9 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
                     dn += beta * PR.eps2;
                 }
                 nm[p] -= inv_s2 * (zs[p] - svv[kx[p]]);
-                rd[p] = (ok[p] && dn > 0.f) ? __fdividef(1.0f, dn) : 0.f;
+                float r;
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(dn));
+                rd[p] = (ok[p] && dn > 0.f) ? r : 0.f;
             }
             // coupling to the earlier pixels of the batch (exact Gauss-Seidel order)
             float alpha[4];
@@ -404,7 +434,11 @@ __global__ void __launch_bounds__(32, 12) k_icd_sv(PassParams P)
 #pragma unroll
                     for (int q = 0; q < K; ++q) sb[ab[p][g] + q * U] = fmaf(-alpha[p], av[p][g][q], ev[g][q]);
             }
-            cur = nxt;
+        };
+#pragma unroll 1
+        for (int b = 0; b < NB; b += 2) {  // ping-pong record buffers (NB is a multiple of 4)
+            step(b, cur, nxt);
+            step(b + 1, nxt, cur);
         }
 
         // -- 5. fold the band's net change into global e; prefetch the next tile's e windows;
