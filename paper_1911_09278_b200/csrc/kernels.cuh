@@ -494,8 +494,32 @@ __global__ void k_gather_data(const AgentDev* agents, const int* row_base, int n
 // (mace.py:71-90), optionally the local partial sum for multi-rank runs.
 // W is [group][n_local][n] (a group = one slice of a multi-slice batch); out is [group][n].
 // ===========================================================================
+// Fixed-order pairwise tree over m agent values (mace.py:71-90): halve, folding the odd tail.
+// With M a compile-time count every index is static and the values stay in registers.
+template <int M>
+__device__ __forceinline__ float tree_sum(float* acc)
+{
+    int m = M;
+#pragma unroll
+    for (int r = 0; r < 12; ++r) {
+        if (m <= 1) break;
+        const int half = m / 2;
+#pragma unroll
+        for (int i = 0; i < half; ++i) acc[i] += acc[half + i];
+        if (m % 2) {
+            acc[half] = acc[2 * half];
+            m = half + 1;
+        } else {
+            m = half;
+        }
+    }
+    return acc[0];
+}
+
+// NL > 0: exactly NL agents (register tree); NL == 0: any n_local <= 64 (local-memory tree)
+template <int NL>
 __global__ void k_consensus(const float* W, int n_local, size_t n, float scale, float* out, const float* ref,
-                            double* ref_part, const int* done, int n_groups = 1)
+                            double* ref_part, const int* done, int n_groups)
 {
     if (done && *done) return;
     double loc = 0.0;
@@ -503,20 +527,28 @@ __global__ void k_consensus(const float* W, int n_local, size_t n, float scale, 
          gs += (size_t)gridDim.x * blockDim.x) {
         const size_t grp = gs / n, s = gs % n;
         const float* Wg = W + grp * n_local * n;
-        float acc[64];
-        for (int i = 0; i < n_local; ++i) acc[i] = Wg[(size_t)i * n + s];
-        int m = n_local;
-        while (m > 1) {
-            const int half = m / 2;
-            for (int i = 0; i < half; ++i) acc[i] += acc[half + i];
-            if (m % 2) {
-                acc[half] = acc[2 * half];
-                m = half + 1;
-            } else {
-                m = half;
+        float v;
+        if constexpr (NL > 0) {
+            float acc[NL];
+#pragma unroll
+            for (int i = 0; i < NL; ++i) acc[i] = __ldcg(Wg + (size_t)i * n + s);
+            v = tree_sum<NL>(acc) / scale;
+        } else {
+            float acc[64];
+            for (int i = 0; i < n_local; ++i) acc[i] = Wg[(size_t)i * n + s];
+            int m = n_local;
+            while (m > 1) {
+                const int half = m / 2;
+                for (int i = 0; i < half; ++i) acc[i] += acc[half + i];
+                if (m % 2) {
+                    acc[half] = acc[2 * half];
+                    m = half + 1;
+                } else {
+                    m = half;
+                }
             }
+            v = acc[0] / scale;
         }
-        const float v = acc[0] / scale;
         out[gs] = v;
         if (ref && grp == 0) {
             const double d = (double)v - (double)ref[s];
@@ -564,12 +596,19 @@ __global__ void k_norms(const double* part, int n_items, const double* ref_part,
         last = atomicAdd(counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
-        double s[5] = {0, 0, 0, 0, 0};
-        for (int b = 0; b < (int)gridDim.x; ++b)
-            for (int k = 0; k < 5; ++k) s[k] += __ldcg(scratch + 5 * b + k);
-        for (int k = 0; k < 5; ++k) out5[k] = s[k];
-        *counter = 0u;
+    if (last) {  // fixed-order tree over the block sums (gridDim.x <= blockDim.x)
+        for (int k = 0; k < 5; ++k)
+            sh[k][threadIdx.x] = (int)threadIdx.x < (int)gridDim.x ? __ldcg(scratch + 5 * threadIdx.x + k) : 0.0;
+        __syncthreads();
+        for (int o = blockDim.x / 2; o; o >>= 1) {
+            if ((int)threadIdx.x < o)
+                for (int k = 0; k < 5; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < 5; ++k) out5[k] = sh[k][0];
+            *counter = 0u;
+        }
     }
 }
 

@@ -304,7 +304,8 @@ static void compute_theta2(Ctx* c)
     if (c->schedule == 1) {
         k_theta2_raster<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_agents.p, c->n_local, (int)c->n);
     } else {
-        k_sv_consts<<<std::max(1, std::min(c->num_sms * 4, (c->n_items + 3) / 4)), 128, 0, c->stream>>>(
+        // one warp per (agent, tile) item
+        k_sv_consts<<<std::max(1, (c->n_items + 3) / 4), 128, 0, c->stream>>>(
             c->d_agents.p, c->n_items, c->queue.p, c->n_side, c->S, c->sv_K, sv_batches(c->S), c->sv_wcap);
     }
     CK(cudaGetLastError());
@@ -314,8 +315,18 @@ static void consensus(Ctx* c, float scale, float* out, bool with_ref)
 {
     const int blocks = kRefBlocks;
     // per slice: tree over that slice's n_real agents (W is [slice][agent][n])
-    k_consensus<<<blocks, 256, 0, c->stream>>>(c->W.p, c->n_real, c->n, scale, out, with_ref ? c->ref.p : nullptr,
-                                                with_ref ? c->refpart.p : nullptr, c->done.p, c->n_slices);
+    const float* rf = with_ref ? c->ref.p : nullptr;
+    double* rp = with_ref ? c->refpart.p : nullptr;
+    switch (c->n_real) {
+        case 1: k_consensus<1><<<blocks, 256, 0, c->stream>>>(c->W.p, 1, c->n, scale, out, rf, rp, c->done.p, c->n_slices); break;
+        case 2: k_consensus<2><<<blocks, 256, 0, c->stream>>>(c->W.p, 2, c->n, scale, out, rf, rp, c->done.p, c->n_slices); break;
+        case 4: k_consensus<4><<<blocks, 256, 0, c->stream>>>(c->W.p, 4, c->n, scale, out, rf, rp, c->done.p, c->n_slices); break;
+        case 8: k_consensus<8><<<blocks, 256, 0, c->stream>>>(c->W.p, 8, c->n, scale, out, rf, rp, c->done.p, c->n_slices); break;
+        case 16: k_consensus<16><<<blocks, 256, 0, c->stream>>>(c->W.p, 16, c->n, scale, out, rf, rp, c->done.p, c->n_slices); break;
+        default:
+            k_consensus<0><<<blocks, 256, 0, c->stream>>>(c->W.p, c->n_real, c->n, scale, out, rf, rp, c->done.p,
+                                                          c->n_slices);
+    }
     CK(cudaGetLastError());
 }
 
@@ -1043,7 +1054,7 @@ int mace_mean_from_sum(void* p, int n_total)
     API_BEGIN
     Ctx* c = C(p);
     // wbar = wsum / N: a one-agent "tree" over the reduced sum
-    k_consensus<<<kRefBlocks, 256, 0, c->stream>>>(c->wsum.p, 1, c->n, (float)n_total, c->wbar.p, nullptr, nullptr,
+    k_consensus<1><<<kRefBlocks, 256, 0, c->stream>>>(c->wsum.p, 1, c->n, (float)n_total, c->wbar.p, nullptr, nullptr,
                                                    nullptr, c->n_slices);
     CK(cudaGetLastError());
     API_END
@@ -1054,7 +1065,7 @@ int mace_iterate_finish(void* p, int n_total, double tol, int iter)
     API_BEGIN
     Ctx* c = C(p);
     ensure_log(c, iter + 1);
-    k_consensus<<<kRefBlocks, 256, 0, c->stream>>>(c->wsum.p, 1, c->n, (float)n_total, c->wbar.p, nullptr, nullptr,
+    k_consensus<1><<<kRefBlocks, 256, 0, c->stream>>>(c->wsum.p, 1, c->n, (float)n_total, c->wbar.p, nullptr, nullptr,
                                                    c->done.p, c->n_slices);
     k_finish<<<1, 1, 0, c->stream>>>(c->sums5.p, 0.0, tol, iter, c->log.p, c->done.p, c->head.p);
     if (c->passes % 50 == 0) refresh(c, 0, c->n_local);
