@@ -410,66 +410,74 @@ __global__ void k_theta2_raster(const AgentDev* agents, int n_agents, int n)
 // theta2_p = sum a_p^2 lambda (icd.py:193-195) for the kSvBatch slots of each batch, and the
 // cross terms c_ij = sum_r a_ir a_jr lambda_r that couple two pixels of a batch through shared
 // rows (k_sv.cuh).  Depends on lambda only, so it is recomputed per data load.
+template <int K, int NG>
 __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n_items, const uint32_t* queue,
-                                                   int n_side, int S, int K, int nb, int W)
+                                                   int n_side, int S, int nb, int W)
 {
     const int lane = threadIdx.x & 31;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    const int SS = S * S, h = S / 2, per_class = h * h, bpc = (per_class + 3) / 4;
-    for (int item = gw; item < n_items; item += nw) {
-        const uint32_t code = queue[item];
-        const AgentDev& A = agents[code >> kAgentShift];
-        const int sv = (int)(code & kSvMask);
-        const int r0 = (sv / A.n_sv_side) * S, c0 = (sv % A.n_sv_side) * S;
-        const int2* bt = A.band + (size_t)sv * A.V;
-        int start[4];
-        for (int g = 0; g < 4; ++g) {
-            const int j = 32 * g + lane;
-            start[g] = (g < A.ng && j < A.V) ? bt[j].x : 0;
-            if (g < A.ng) {  // the band's lambda rows, laid out as the kernel's shared-memory plane
-                const int cnt = j < A.V ? bt[j].y : 0;
-                float* lb = A.lb + (((size_t)sv * A.ng + g) * W) * 32 + lane;
-                for (int o = 0; o < W; ++o) lb[o * 32] = o < cnt ? A.lam[start[g] + o] : 0.f;
+    const long task = (long)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);  // one warp per (item, batch)
+    if (task >= (long)n_items * nb) return;
+    const int item = (int)(task / nb), b = (int)(task % nb);
+    const int h = S / 2, per_class = h * h, bpc = (per_class + 3) / 4;
+    const int recw = NG * 32 * K + 32;
+    const uint32_t code = queue[item];
+    const AgentDev& A = agents[code >> kAgentShift];
+    const int sv = (int)(code & kSvMask);
+    const int r0 = (sv / A.n_sv_side) * S, c0 = (sv % A.n_sv_side) * S;
+    const int2* bt = A.band + (size_t)sv * A.V;
+    int start[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        const int j = 32 * g + lane;
+        const int2 bj = j < A.V ? bt[j] : make_int2(0, 0);
+        start[g] = bj.x;
+        if (b == 0) {  // the band's lambda rows, laid out as the kernel's shared-memory plane
+            float* lb = A.lb + (((size_t)sv * NG + g) * W) * 32 + lane;
+            for (int o = 0; o < W; ++o) lb[o * 32] = o < bj.y ? A.lam[bj.x + o] : 0.f;
+        }
+    }
+    const uint32_t* rb = A.rec + ((size_t)sv * nb + b) * 4 * recw;
+    float t2[4] = {0.f, 0.f, 0.f, 0.f}, cx[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        float a[4][K], l[4][K];
+        int o[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const uint32_t* r = rb + (size_t)p * recw;
+            o[p] = (int)((r[NG * 32 * K + lane] >> (8 * g)) & 0xffu);
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+                a[p][q] = __uint_as_float(r[(g * 32 + lane) * K + q]);
+                l[p][q] = a[p][q] != 0.f ? A.lam[start[g] + o[p] + q] : 0.f;
+                t2[p] = fmaf(a[p][q] * a[p][q], l[p][q], t2[p]);
             }
         }
-        for (int b = 0; b < nb; ++b) {
-            const uint32_t* rb = A.rec + ((size_t)sv * nb + b) * 4 * A.rec_words;
-            float t2[4] = {0.f, 0.f, 0.f, 0.f}, cx[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            for (int g = 0; g < A.ng; ++g) {
-                float a[4][4];
-                int o[4];
-                for (int p = 0; p < 4; ++p) {
-                    const uint32_t* r = rb + (size_t)p * A.rec_words;
-                    o[p] = (int)((r[A.ng * 32 * K + lane] >> (8 * g)) & 0xffu);
-                    for (int q = 0; q < K; ++q) a[p][q] = __uint_as_float(r[(g * 32 + lane) * K + q]);
-                }
-                for (int p = 0; p < 4; ++p)
-                    for (int q = 0; q < K; ++q)
-                        if (a[p][q] != 0.f) t2[p] = fmaf(a[p][q] * a[p][q], A.lam[start[g] + o[p] + q], t2[p]);
-                int x = 0;
-                for (int i = 0; i < 4; ++i)
-                    for (int j = i + 1; j < 4; ++j, ++x)
-                        for (int q = 0; q < K; ++q) {  // row o_i + q of pixel i is row q - (o_j - o_i) of j
-                            const int qj = q - (o[j] - o[i]);
-                            if (qj >= 0 && qj < K && a[i][q] != 0.f && a[j][qj] != 0.f)
-                                cx[x] = fmaf(a[i][q] * a[j][qj], A.lam[start[g] + o[i] + q], cx[x]);
-                        }
-            }
-            for (int p = 0; p < 4; ++p) t2[p] = warp_sum(t2[p]);
-            for (int x = 0; x < 6; ++x) cx[x] = warp_sum(cx[x]);
-            float* out = A.bc + ((size_t)sv * nb + b) * 16;
-            if (lane < 4) out[lane] = t2[lane];
-            else if (lane < 10) out[lane] = cx[lane - 4];
-            else if (lane < 16) out[lane] = 0.f;
-            if (lane < 4) {  // theta2 image (cost kernels, diagnostics)
-                const int i = (b % bpc) * 4 + lane, cls = b / bpc;
-                if (i < per_class) {
-                    const int lr = (cls >> 1) + 2 * (i / h), lc = (cls & 1) + 2 * (i % h);
-                    if (r0 + lr < n_side && c0 + lc < n_side && lr * S + lc < SS)
-                        A.th[(size_t)(r0 + lr) * n_side + c0 + lc] = t2[lane];
-                }
-            }
+        int x = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = i + 1; j < 4; ++j, ++x)
+#pragma unroll
+                for (int q = 0; q < K; ++q)
+#pragma unroll
+                    for (int qj = 0; qj < K; ++qj)  // row o_i + q of pixel i is row o_j + qj of pixel j
+                        if (o[i] + q == o[j] + qj) cx[x] = fmaf(a[i][q] * a[j][qj], l[i][q], cx[x]);
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) t2[p] = warp_sum(t2[p]);
+#pragma unroll
+    for (int x = 0; x < 6; ++x) cx[x] = warp_sum(cx[x]);
+    float v = 0.f;
+#pragma unroll
+    for (int k = 0; k < 10; ++k)
+        if (lane == k) v = k < 4 ? t2[k & 3] : cx[(k - 4) % 6];
+    if (lane < 16) A.bc[((size_t)sv * nb + b) * 16 + lane] = v;
+    if (lane < 4) {  // theta2 image (cost kernels, diagnostics)
+        const int i = (b % bpc) * 4 + lane, cls = b / bpc;
+        if (i < per_class) {
+            const int lr = (cls >> 1) + 2 * (i / h), lc = (cls & 1) + 2 * (i % h);
+            if (r0 + lr < n_side && c0 + lc < n_side) A.th[(size_t)(r0 + lr) * n_side + c0 + lc] = v;
         }
     }
 }

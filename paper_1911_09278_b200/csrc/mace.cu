@@ -304,9 +304,24 @@ static void compute_theta2(Ctx* c)
     if (c->schedule == 1) {
         k_theta2_raster<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_agents.p, c->n_local, (int)c->n);
     } else {
-        // one warp per (agent, tile) item
-        k_sv_consts<<<std::max(1, (c->n_items + 3) / 4), 128, 0, c->stream>>>(
-            c->d_agents.p, c->n_items, c->queue.p, c->n_side, c->S, c->sv_K, sv_batches(c->S), c->sv_wcap);
+        // one warp per (item, batch)
+        const int nb = sv_batches(c->S);
+        const long blocks = std::max(1L, ((long)c->n_items * nb + 3) / 4);
+        auto go = [&](auto kern) {
+            kern<<<(unsigned)blocks, 128, 0, c->stream>>>(c->d_agents.p, c->n_items, c->queue.p, c->n_side, c->S, nb,
+                                                          c->sv_wcap);
+        };
+        const int key = c->sv_K * 10 + c->sv_ng;
+        switch (key) {
+            case 21: go(k_sv_consts<2, 1>); break;
+            case 22: go(k_sv_consts<2, 2>); break;
+            case 23: go(k_sv_consts<2, 3>); break;
+            case 24: go(k_sv_consts<2, 4>); break;
+            case 41: go(k_sv_consts<4, 1>); break;
+            case 42: go(k_sv_consts<4, 2>); break;
+            case 43: go(k_sv_consts<4, 3>); break;
+            default: go(k_sv_consts<4, 4>); break;
+        }
     }
     CK(cudaGetLastError());
 }
