@@ -282,6 +282,27 @@ struct FPParams {
     int n_ch;
 };
 
+// sum over one CSR row of vals[k] * x[cols[k]], lanes strided, four independent accumulators
+// (loads of four chunks in flight); fixed order -> deterministic
+__device__ __forceinline__ float row_dot(const FPParams& F, int64_t k0, int64_t k1, const float* __restrict__ x,
+                                        int lane)
+{
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int64_t k = k0 + lane;
+    for (; k + 96 < k1; k += 128) {
+        const int c0 = __ldcs(F.cols + k), c1 = __ldcs(F.cols + k + 32), c2 = __ldcs(F.cols + k + 64),
+                  c3 = __ldcs(F.cols + k + 96);
+        const float v0 = __ldcs(F.vals + k), v1 = __ldcs(F.vals + k + 32), v2 = __ldcs(F.vals + k + 64),
+                    v3 = __ldcs(F.vals + k + 96);
+        a0 = fmaf(v0, __ldcg(x + c0), a0);
+        a1 = fmaf(v1, __ldcg(x + c1), a1);
+        a2 = fmaf(v2, __ldcg(x + c2), a2);
+        a3 = fmaf(v3, __ldcg(x + c3), a3);
+    }
+    for (; k < k1; k += 32) a0 = fmaf(__ldcs(F.vals + k), __ldcg(x + __ldcs(F.cols + k)), a0);
+    return warp_sum((a0 + a1) + (a2 + a3));
+}
+
 // agent owning concatenated row `wr`: last a with row_base[a] <= wr (row_base ascending)
 __device__ __forceinline__ int agent_of_row(const int* row_base, int n_agents, int wr)
 {
@@ -308,9 +329,7 @@ __global__ void k_fp_agents(FPParams F, const AgentDev* agents, const int* row_b
         if (r >= A.R) continue;  // alignment padding between agents
         const int j = r / F.n_ch, ch = r % F.n_ch;
         const int64_t g = (int64_t)A.views[j] * F.n_ch + ch;
-        float acc = 0.f;
-        for (int64_t k = F.rp[g] + lane; k < F.rp[g + 1]; k += 32) acc = fmaf(F.vals[k], __ldcg(A.z + F.cols[k]), acc);
-        acc = warp_sum(acc);
+        const float acc = row_dot(F, F.rp[g], F.rp[g + 1], A.z, lane);
         if (lane == 0) A.e[r] = A.y[r] - acc;
     }
 }
@@ -324,9 +343,7 @@ __global__ void k_fp_rows(FPParams F, int n_rows, const float* x, float* out, co
     const int nw = (gridDim.x * blockDim.x) >> 5;
     double loc = 0.0;
     for (int g = gw; g < n_rows; g += nw) {
-        float acc = 0.f;
-        for (int64_t k = F.rp[g] + lane; k < F.rp[g + 1]; k += 32) acc = fmaf(F.vals[k], x[F.cols[k]], acc);
-        acc = warp_sum(acc);
+        const float acc = row_dot(F, F.rp[g], F.rp[g + 1], x, lane);
         if (lane == 0) {
             if (out) out[g] = acc;
             if (part) {
