@@ -155,13 +155,16 @@ def run_ours(args):
 
     cfg = gen.CONFIGS[args.config]
     N, iters = cfg["n_agents"], args.iters or cfg["iters"]
+    pnp = args.config == 3  # config 3: PnP MACE with the 17-layer CNN denoiser (K5) as the prior agent
     t0 = time.time()
     geom, mats, phantom, y, lam = gen.make_scan(args.config)
     t_scan = time.time() - t0
     prior = mb.PriorParams("qggmrf", beta=cfg["beta"], p=2.0, q=1.2, T=1.0, sigma_x=0.01)
     prob = mb.ReconProblem(geom, mats, y, lam, prior)
     mcfg = mb.MaceConfig(n_subsets=N, rho=0.8, sigma=cfg["sigma"], max_outer=iters, tol=1e-300,
-                         residuals="none", schedule=args.schedule, sv_side=args.sv, device=local)
+                         residuals="none", schedule=args.schedule, sv_side=args.sv, device=local,
+                         **({"mode": "pnp", "denoiser": mb.DenoiserSpec("identity")} if pnp else {}))
+    den = mb.denoisers.CnnDenoiser(geom.n_side, seed=0, device=local) if pnp else None
     comm = True if world > 1 else None
     subsets = mb.partition_views(geom.n_views, N)
     local_agents = [i for i in range(N) if i % world == rank]
@@ -179,20 +182,27 @@ def run_ours(args):
             plan.local_sum()
             mb.mace._resolve_comm(True).allreduce(*plan.comm_arrays()[:1])
             plan.mean_from_sum(N)
-        plan.states_from(0)
+        if pnp:
+            den.device_apply(plan)  # g = H(wbar)
+        plan.states_from(1 if pnp else 0)
         if world == 1:
-            plan.iterate(iters, 0, 0.8, False, 1e-300, N, False)
+            plan.iterate(iters, 0, 0.8, pnp, 1e-300, N, False, device_denoise=pnp)
         else:
             c = mb.mace._resolve_comm(True)
             for k in range(iters):
-                plan.iterate_local(0.8, False)
+                plan.iterate_local(0.8, pnp)
                 c.allreduce(*plan.comm_arrays())
                 plan.iterate_finish(N, 1e-300, k)
+                if pnp:
+                    den.device_apply(plan)
 
     # resident inputs
     plan.load_data(y, lam)
     plan.set_prior(prior)
-    plan.set_agent_params(-1, prior.beta / N, 1.0 / cfg["sigma"] ** 2, False)
+    if pnp:  # agents carry only data terms at sqrt(N) sigma (mace.py:263-265)
+        plan.set_agent_params(-1, 0.0, 1.0 / (N * cfg["sigma"] ** 2), False)
+    else:
+        plan.set_agent_params(-1, prior.beta / N, 1.0 / cfg["sigma"] ** 2, False)
 
     def barrier():
         torch.cuda.synchronize(local)
@@ -222,11 +232,11 @@ def run_ours(args):
 
     # ---- end to end through the public API (host numpy in, host numpy out)
     for _ in range(1):
-        _solve_api(mb, prob, mcfg, comm)
+        _solve_api(mb, prob, mcfg, comm, den)
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        res = _solve_api(mb, prob, mcfg, comm)
+        res = _solve_api(mb, prob, mcfg, comm, den)
     barrier()
     e2e_s = time.perf_counter() - t0
     if world > 1:
@@ -265,7 +275,26 @@ def run_ours(args):
         "clocks": clocks,
         "setup_s": {"scan": t_scan, "plan": t_plan},
     }
-    if world == 1 and args.ttr_iters > 0:
+    if pnp:  # K5 alone: 17-layer CNN on the consensus image, CUDA events on the library stream
+        reps = 20
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            den.device_apply(plan)
+        e1.record(stream)
+        barrier()
+        k5_ms = e0.elapsed_time(e1) / reps
+        flop = 2.0 * geom.n_pixels * 9 * (64 + 15 * 64 * 64 + 64)
+        line["k5"] = {"kernel": "k_conv64_tc (tcgen05, 15 layers) + first/last layers", "ms_per_denoise": k5_ms,
+                      "flop_per_denoise": flop, "achieved_tflops": flop / (k5_ms / 1e3) / 1e12,
+                      "peak_tflops": pk.get("bf16_tflops"), "peak_source": "MEASURED_PEAKS bf16_tflops (burst: "
+                      "timed alone)", "frac": flop / (k5_ms / 1e3) / 1e12 / pk.get("bf16_tflops", 1.0),
+                      "frac_of_sustained": flop / (k5_ms / 1e3) / 1e12 / pk.get("bf16_tflops_sustained", 1.0),
+                      "share_of_step": k5_ms * iters / (ms / args.steps)}
+        line["config"]["workload"] = line["config"]["workload"].replace("qGGMRF beta", "PnP CNN denoiser (K5); beta")
+        line["config"]["prior"] = "PnP: 17-layer 64-ch 3x3 CNN, He-normal(seed 0) x 0.1 weights in bf16, x - net(x)"
+    if world == 1 and args.ttr_iters > 0 and not pnp:
         line["time_to_rmse_1e-3"] = time_to_rmse(plan, args.config, N, n, args.ttr_iters)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.config, mats, y, lam, sample_iters=args.cpu_iters)
@@ -312,8 +341,10 @@ def plan_stream(plan):
     return s.value
 
 
-def _solve_api(mb, prob, cfg, comm):
+def _solve_api(mb, prob, cfg, comm, denoiser=None):
     try:
+        if denoiser is not None:
+            return mb.mace_pnp_solve(prob, cfg, comm=comm, denoiser=denoiser)
         return mb.mace_solve(prob, cfg, comm=comm)
     except mb.ConvergenceError as err:
         return err.last_iterate

@@ -100,6 +100,8 @@ int mace_states_from(void* ctx, int which);
 int mace_get_image(void* ctx, int which, float* out);
 int mace_set_image(void* ctx, int which, const float* img);
 int mace_get_stack(void* ctx, float* w);
+/* use_g: 0 MACE (G = average); 1 PnP, g = H(wbar) supplied between calls (host denoiser or
+ * mace_cnn_apply); 2 PnP with the K5 denoiser applied on the device after every iteration */
 int mace_iterate(void* ctx, int iters, int iter0, double rho, int use_g, double tol, int n_total, int with_ref,
                  float* ms_out);
 int mace_iterate_local(void* ctx, double rho, int use_g);

@@ -1005,6 +1005,17 @@ int mace_get_stack(void* p, float* w)
 
 // Single-rank device loop: iters x [K2 pass of all agents -> K4 average/norms -> stop test];
 // use_g: v = 2 g - w with g set by the caller (PnP), else v = 2 wbar - w.  No host sync inside.
+// g = H(wbar) per slice with the K5 denoiser
+static void cnn_all_slices(Ctx* c)
+{
+    if (!c->cnn.ready) throw std::runtime_error("denoiser weights not loaded (mace_cnn_set_weights)");
+    for (int s = 0; s < c->n_slices; ++s)
+        c->cnn.apply(c->wbar.p + (size_t)s * c->n, c->g.p + (size_t)s * c->n, c->n_side, c->n_side, c->stream,
+                     c->num_sms, nullptr);
+}
+
+// use_g: 0 = MACE (G = average), 1 = PnP with g supplied between calls, 2 = PnP with the K5
+// denoiser applied on the device after every iteration (no host round trip)
 int mace_iterate(void* p, int iters, int iter0, double rho, int use_g, double tol, int n_total, int with_ref,
                  float* ms_out)
 {
@@ -1022,6 +1033,7 @@ int mace_iterate(void* p, int iters, int iter0, double rho, int use_g, double to
         k_finish<<<1, 1, 0, c->stream>>>(c->sums5.p, with_ref && !use_g ? c->ref_norm2 : 0.0, tol, iter0 + k,
                                          c->log.p, c->done.p, c->head.p);
         if (c->passes % 50 == 0) refresh(c, 0, c->n_local);  // icd.py:29,280-282
+        if (use_g == 2) cnn_all_slices(c);                    // g = H(wbar) on the device (mace.py:105-108)
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(c->ev1, c->stream));
@@ -1291,7 +1303,7 @@ int mace_cnn_apply(void* p)
 {
     API_BEGIN
     Ctx* c = C(p);
-    c->cnn.apply(c->wbar.p, c->g.p, c->n_side, c->n_side, c->stream, c->num_sms, nullptr);
+    cnn_all_slices(c);
     API_END
 }
 

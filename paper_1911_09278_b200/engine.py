@@ -249,9 +249,12 @@ class AgentPlan(_Context):
     def set_ref(self, ref):
         self.call("mace_set_ref", N.ptr(None if ref is None else N.f32(ref)))
 
-    def iterate(self, iters, iter0, rho, use_g, tol, n_total, with_ref) -> float:
+    def iterate(self, iters, iter0, rho, use_g, tol, n_total, with_ref, device_denoise=False) -> float:
+        """`iters` MACE iterations on the device; use_g: PnP (v from g).  device_denoise: apply the
+        loaded K5 denoiser g = H(wbar) inside the loop after every iteration."""
         ms = ctypes.c_float(0.0)
-        self.call("mace_iterate", int(iters), int(iter0), float(rho), int(bool(use_g)), float(tol), int(n_total),
+        mode = 2 if (use_g and device_denoise) else int(bool(use_g))
+        self.call("mace_iterate", int(iters), int(iter0), float(rho), mode, float(tol), int(n_total),
                   int(bool(with_ref)), ctypes.byref(ms))
         return float(ms.value)
 

@@ -28,8 +28,9 @@ CONFIGS = {
             beta=25.0, sigma=3.5e-4),
     2: dict(n_side=1024, n_views=1440, n_channels=1450, n_agents=16, iters=50, I0=5e3, n_ellipses=40, slices=1,
             beta=4.0, sigma=3.5e-4),
+    # PnP agents run at sqrt(N) sigma (mace.py:263-265): sigma = 3.5e-4 / sqrt(8) keeps them at c1's margin
     3: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=40, I0=1e4, n_ellipses=10, slices=1,
-            beta=25.0, sigma=3.5e-4),
+            beta=25.0, sigma=1.24e-4),
     4: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=30, I0=1e4, n_ellipses=10, slices=64,
             beta=25.0, sigma=3.5e-4),
 }

@@ -347,11 +347,14 @@ def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=
         chunk = config.max_outer
         while it < config.max_outer and done[0] == 0:
             k = min(chunk, config.max_outer - it)
-            if pnp:  # device denoiser: one iteration per call, H applied on the device in between
+            in_loop = pnp and hasattr(denoiser, "_load")  # the K5 CNN: H inside the device loop
+            if pnp and (ref_image is not None or not in_loop):  # per-iteration host step
                 k = 1
-            ms = plan.iterate(k, it, config.rho, pnp, config.tol, N, ref32 is not None)
+            if in_loop:
+                denoiser._load(plan)
+            ms = plan.iterate(k, it, config.rho, pnp, config.tol, N, ref32 is not None, device_denoise=in_loop)
             device_ms += ms
-            if pnp:
+            if pnp and not in_loop:
                 _apply_denoiser(plan, denoiser)
             it += k
             lg, done = plan.read_log(it)

@@ -103,7 +103,7 @@ class CpuPlan:
         elif rel < tol:
             self.done = (1, it + 1)
 
-    def iterate(self, iters, iter0, rho, use_g, tol, n_total, with_ref):
+    def iterate(self, iters, iter0, rho, use_g, tol, n_total, with_ref, device_denoise=False):
         for k in range(iters):
             if self.done[0]:
                 break
