@@ -180,7 +180,7 @@ def run_ours(args):
         plan.stack_init(None, N if world == 1 else 0)
         if world > 1:
             plan.local_sum()
-            mb.mace._resolve_comm(True).allreduce(*plan.comm_arrays()[:1])
+            mb.mace._resolve_comm(True).allreduce(*plan.comm_arrays()[:1], stream=plan.torch_stream())
             plan.mean_from_sum(N)
         if pnp:
             den.device_apply(plan)  # g = H(wbar)
@@ -191,7 +191,7 @@ def run_ours(args):
             c = mb.mace._resolve_comm(True)
             for k in range(iters):
                 plan.iterate_local(0.8, pnp)
-                c.allreduce(*plan.comm_arrays())
+                c.allreduce(*plan.comm_arrays(), stream=plan.torch_stream())
                 plan.iterate_finish(N, 1e-300, k)
                 if pnp:
                     den.device_apply(plan)

@@ -234,14 +234,27 @@ class AgentPlan(_Context):
         self.call("mace_mean_from_sum", int(n_total))
 
     def comm_arrays(self):
-        """(stack sum [n] float32, norm sums [5] float64) as torch CUDA tensors over the context's buffers."""
+        """(stack sum [n] float32, norm sums [5] float64) as torch CUDA tensors over the context's
+        buffers.  No host synchronisation: reduce them on `torch_stream()`, which orders the
+        collective after the kernels that produced them and before the ones that consume them."""
         import torch
 
-        wsum, sums = ctypes.c_void_p(), ctypes.c_void_p()
-        self.call("mace_comm_buffers", ctypes.byref(wsum), ctypes.byref(sums))
-        self.call("mace_sync")
-        return (torch.as_tensor(_DevArray(wsum.value, (self.n,), "<f4"), device=f"cuda:{self.device}"),
-                torch.as_tensor(_DevArray(sums.value, (5,), "<f8"), device=f"cuda:{self.device}"))
+        if getattr(self, "_comm_t", None) is None:
+            wsum, sums = ctypes.c_void_p(), ctypes.c_void_p()
+            self.call("mace_comm_buffers", ctypes.byref(wsum), ctypes.byref(sums))
+            self._comm_t = (torch.as_tensor(_DevArray(wsum.value, (self.n,), "<f4"), device=f"cuda:{self.device}"),
+                            torch.as_tensor(_DevArray(sums.value, (5,), "<f8"), device=f"cuda:{self.device}"))
+        return self._comm_t
+
+    def torch_stream(self):
+        """The library stream as a torch stream (collectives enqueued on it need no host sync)."""
+        import torch
+
+        if getattr(self, "_tstream", None) is None:
+            s = ctypes.c_void_p()
+            self.call("mace_ctx_stream", ctypes.byref(s))
+            self._tstream = torch.cuda.ExternalStream(s.value, device=f"cuda:{self.device}")
+        return self._tstream
 
     def states_from(self, which):
         self.call("mace_states_from", int(which))
@@ -267,9 +280,7 @@ class AgentPlan(_Context):
         self.call("mace_iterate_local", float(rho), int(bool(use_g)))
 
     def iterate_finish(self, n_total, tol, it):
-        import torch
-
-        torch.cuda.synchronize(self.device)
+        """after the all-reduce of comm_arrays() on torch_stream() (stream-ordered, no host sync)"""
         self.call("mace_iterate_finish", int(n_total), float(tol), int(it))
 
     def read_log(self, n):

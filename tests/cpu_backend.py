@@ -78,6 +78,8 @@ class CpuPlan:
 
     # -- iterations
     def iterate_local(self, rho, use_g):
+        if self.done[0]:  # like the device kernels: no-ops once the stop test has fired
+            return
         g = self.g if use_g else self.wbar
         dsq = dw2 = wn2 = wo2 = 0.0
         for i, a in enumerate(self.agents):
@@ -94,6 +96,8 @@ class CpuPlan:
         self.sums[:] = torch.tensor([dsq, dw2, wn2, wo2, 0.0], dtype=torch.float64)
 
     def iterate_finish(self, n_total, tol, it):
+        if self.done[0]:
+            return
         self.wbar = self.wsum.numpy() / n_total
         dsq, dw2, wn2, wo2, _ = self.sums.tolist()
         rel = np.sqrt(dw2) / max(np.sqrt(wo2), 1e-300)

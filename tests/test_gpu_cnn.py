@@ -106,3 +106,30 @@ def test_mace_pnp_with_cnn_denoiser_vs_oracle_loop():
     agents = O.build_agents(mats, y, lam, N, sigma, O.Prior("qggmrf", 25.0, 2.0, 1.2, 1.0, 0.01), ns, pnp=True)
     run = O.mace_run(agents, iters, 0.8, denoiser=lambda v: cnn_apply(v, w, ns))
     assert rel(res.image, run.image) < 1e-4
+
+
+def test_pnp_denoiser_in_device_loop_matches_host_steps():
+    """mace_iterate(use_g=2) applies the CNN inside the device loop; the same CNN driven as a plain
+    host callable (one iteration per call, H on the host boundary) must give the same iterates."""
+    ns, nv, nc, N = 64, 90, 91, 4
+    pitch = 128.0 / ns
+    geom = mb.Geometry(ns, pitch, nv, nc, pitch)
+    mats = mb.build_system_matrix(geom)
+    ph = gen.ellipse_phantom(ns, pitch, 10, seed=2)
+    y, lam = gen.poisson_sinogram(gen.host_forward_project(mats, ph), 1e4, seed=3)
+    prob = mb.ReconProblem(geom, mats, y, lam, mb.PriorParams("qggmrf", 25.0, 2.0, 1.2, 1.0, 0.01))
+    w = cnn_weights(5, scale=0.5)
+    H = CnnDenoiser(ns, weights=w)
+    cfg = mb.MaceConfig(n_subsets=N, rho=0.8, sigma=2e-4, mode="pnp", denoiser=mb.DenoiserSpec("identity"),
+                        max_outer=15, tol=1e-300, residuals="none", schedule="raster")
+
+    def solve(den):
+        try:
+            return mb.mace_pnp_solve(prob, cfg, denoiser=den)
+        except mb.ConvergenceError as err:
+            return err.last_iterate
+
+    dev = solve(H)
+    host = solve(lambda v: H(v))  # no device hooks: host round trip every iteration
+    assert rel(dev.image, host.image) < 1e-6
+    assert rel(dev.stack, host.stack) < 1e-6
