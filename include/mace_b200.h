@@ -92,6 +92,9 @@ int mace_pass(void* ctx, int local, const float* v, int n_passes, int64_t s_begi
 
 int mace_forward_project(void* ctx, const float* x, float* out);
 int mace_cost(void* ctx, const float* x, double beta, double* like, double* prior);
+/* gradient of the MAP cost (models.py:235-278) at x: norms[3] = |grad|, |data part|, |prior part|;
+ * grad_out[n] optional (fp64).  A fixed-point certificate where no converged oracle exists. */
+int mace_gradient(void* ctx, const float* x, double beta, double* grad_out, double* norms);
 
 /* ---- MACE outer loop */
 int mace_stack_init(void* ctx, const float* w0, int n_total);

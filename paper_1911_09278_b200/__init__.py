@@ -13,6 +13,6 @@ from .icd import (REFRESH_EVERY, AgentWorkspace, ConvergenceError, icd_map_solve
 from .mace import (ConvergenceLog, EquitCounter, MaceConfig, MaceResult, ResidualReport, WorkerPool, average,
                    consensus_G, consensus_GH, equilibrium_residuals, mace_pnp_solve, mace_solve, mann_step,
                    new_stack, nrmse, reflect_G, mace_solve_batch)
-from .models import QGGMRF, QUADRATIC, PriorParams, ReconProblem, book_to_reference_beta, map_cost, neighbor_table
+from .models import QGGMRF, QUADRATIC, PriorParams, ReconProblem, book_to_reference_beta, map_cost, map_gradient, neighbor_table
 
 __version__ = "0.1.0"

@@ -49,6 +49,7 @@ _SIGS = {
     "mace_pass": (c_int, [P, c_int, P, c_int, c_int64, c_int64, P]),
     "mace_forward_project": (c_int, [P, P, P]),
     "mace_cost": (c_int, [P, P, c_double, P, P]),
+    "mace_gradient": (c_int, [P, P, c_double, P, P]),
     "mace_stack_init": (c_int, [P, P, c_int]),
     "mace_set_ref": (c_int, [P, P]),
     "mace_states_from": (c_int, [P, c_int]),

@@ -374,6 +374,49 @@ __device__ __forceinline__ double qg_potential_d(double d, const PriorC& P)
     return (pow(ad, P.p) / (P.p * pow(P.sx, P.p))) * (um / (1.0 + um));
 }
 
+// rho'(d) in fp64 (icd.py:45-64 _qg_influence, reference convention)
+__device__ __forceinline__ double qg_influence_d(double d, const PriorC& P)
+{
+    const double ad = fabs(d);
+    const double u = ad / (P.T * P.sx);
+    if (!(u > 0.0)) return 0.0;
+    const double um = pow(u, P.q - P.p);
+    const double g = pow(ad, P.p - 1.0) / pow(P.sx, P.p) * um * (P.q / P.p + um) / ((1.0 + um) * (1.0 + um));
+    return d < 0.0 ? -g : g;
+}
+
+// MAP-cost gradient, data part: grad[s] -= sum_rows a_rs lambda_r (y_r - (Ax)_r)  (one warp per row)
+__global__ void k_bp_rows(FPParams F, int n_rows, const float* Ax, const float* y, const float* lam, double* grad)
+{
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int g = gw; g < n_rows; g += nw) {
+        const double r = (double)lam[g] * ((double)y[g] - (double)Ax[g]);
+        if (r == 0.0) continue;
+        for (int64_t k = F.rp[g] + lane; k < F.rp[g + 1]; k += 32) atomicAdd(grad + F.cols[k], -(double)F.vals[k] * r);
+    }
+}
+
+// MAP-cost gradient, prior part: grad[s] += beta sum_k w_k rho'(x_s - x_k) (+ 2 beta eps x_s, quadratic)
+__global__ void k_prior_grad(const float* x, int n_side, PriorC P, double beta, double* grad)
+{
+    const size_t N = (size_t)n_side * n_side;
+    for (size_t s = blockIdx.x * (size_t)blockDim.x + threadIdx.x; s < N; s += (size_t)gridDim.x * blockDim.x) {
+        const int r = (int)(s / n_side), c = (int)(s % n_side);
+        const double xs = x[s];
+        double acc = 0.0;
+        for (int k = 0; k < 8; ++k) {
+            const int rr = r + c_dr[k], cc = c + c_dc[k];
+            if (rr < 0 || rr >= n_side || cc < 0 || cc >= n_side) continue;
+            const double d = xs - (double)x[(size_t)rr * n_side + cc];
+            acc += (double)c_nw[k] * (P.kind == 0 ? d : qg_influence_d(d, P));
+        }
+        if (P.kind == 0) acc += 2.0 * P.eps * xs;
+        grad[s] += beta * acc;
+    }
+}
+
 __global__ void k_prior_cost(const float* x, int n_side, PriorC P, double* part)
 {
     const size_t N = (size_t)n_side * n_side;

@@ -931,6 +931,45 @@ int mace_cost(void* p, const float* x, double beta, double* like, double* prior)
     API_END
 }
 
+// gradient of the MAP cost f = likelihood + beta prior (models.py:235-278) at x (host), fp64
+// accumulation; norms = [|grad|, |grad_data|, |grad_prior|]; grad_out (host, n) optional.
+// The fixed-point certificate for configurations the CPU oracle cannot converge.
+int mace_gradient(void* p, const float* x, double beta, double* grad_out, double* norms)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    const int rows = c->n_views * c->n_ch;
+    DBuf<float> dx, ax;
+    DBuf<double> g;
+    dx.alloc(c->n);
+    ax.alloc(rows);
+    g.alloc(c->n);
+    CK(cudaMemcpyAsync(dx.p, x, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(g.p, 0, sizeof(double) * c->n, c->stream));
+    const int b1 = std::max(1, std::min(c->num_sms * 8, (rows + 7) / 8));
+    FPParams F{c->rp.p, c->cols.p, c->vals.p, c->n_ch};
+    k_fp_rows<<<b1, 256, 0, c->stream>>>(F, rows, dx.p, ax.p, nullptr, nullptr, nullptr);
+    k_bp_rows<<<b1, 256, 0, c->stream>>>(F, rows, ax.p, c->y.p, c->lam.p, g.p);
+    CK(cudaGetLastError());
+    std::vector<double> gd(c->n), gt(c->n);
+    CK(cudaMemcpyAsync(gd.data(), g.p, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    k_prior_grad<<<c->num_sms * 8, 256, 0, c->stream>>>(dx.p, c->n_side, c->prior, beta, g.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(gt.data(), g.p, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    double n2 = 0, d2 = 0, p2 = 0;
+    for (size_t i = 0; i < c->n; ++i) {
+        n2 += gt[i] * gt[i];
+        d2 += gd[i] * gd[i];
+        p2 += (gt[i] - gd[i]) * (gt[i] - gd[i]);
+    }
+    norms[0] = std::sqrt(n2);
+    norms[1] = std::sqrt(d2);
+    norms[2] = std::sqrt(p2);
+    if (grad_out) std::memcpy(grad_out, gt.data(), sizeof(double) * c->n);
+    API_END
+}
+
 // ------------------------------------------------------------------ MACE outer loop (mace.py:276-365)
 int mace_stack_init(void* p, const float* w0, int n_total)
 {

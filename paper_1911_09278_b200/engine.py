@@ -106,6 +106,16 @@ class DeviceOperator(_Context):
         self.call("mace_cost", N.ptr(x), float(prior.beta), ctypes.byref(like), ctypes.byref(pri))
         return like.value, pri.value
 
+    def gradient(self, y, weights, x, prior, want_grad=True):
+        """grad f(x) (fp64, length n or None) and [|grad|, |data part|, |prior part|]"""
+        self.load_data(y, weights)
+        self.set_prior(prior)
+        x = N.f32(x)
+        norms = np.zeros(3, np.float64)
+        g = np.zeros(x.shape[0], np.float64) if want_grad else None
+        self.call("mace_gradient", N.ptr(x), float(prior.beta), N.ptr(g), N.ptr(norms))
+        return g, norms
+
 
 _CACHE: "OrderedDict[tuple, object]" = OrderedDict()
 _CACHE_LOCK = threading.Lock()

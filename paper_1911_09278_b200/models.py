@@ -15,7 +15,7 @@ import numpy as np
 
 from .geometry import Geometry
 
-__all__ = ["QUADRATIC", "QGGMRF", "PriorParams", "ReconProblem", "neighbor_table", "map_cost",
+__all__ = ["QUADRATIC", "QGGMRF", "PriorParams", "ReconProblem", "neighbor_table", "map_cost", "map_gradient",
            "likelihood_cost", "prior_cost", "book_to_reference_beta"]
 
 QUADRATIC = "quadratic-mrf"
@@ -113,6 +113,16 @@ def map_cost(problem, x, beta: float | None = None) -> float:
     """f(x; beta) = 1/2 ||y - Ax||^2_Lambda + beta h(x) on the GPU (models.py:273-278)."""
     like, prior = _costs(problem, x, beta)
     return like + prior
+
+
+def map_gradient(problem, x, beta: float | None = None):
+    """grad f(x; beta) on the GPU (fp64 accumulation) and its norms [total, data, prior]: the
+    stationarity certificate of a fixed point (0 at the MAP)."""
+    from .engine import operator_for
+
+    op = operator_for(problem.matrices)
+    params = problem.prior if beta is None else problem.prior.with_beta(beta)
+    return op.gradient(problem.y, problem.weights, x, params)
 
 
 def likelihood_cost(problem, x) -> float:
