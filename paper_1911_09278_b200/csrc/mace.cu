@@ -261,7 +261,9 @@ static void run_pass(Ctx* c, int mode, float rho, const float* gimg, int a0, int
         switch (c->NV) {
             case 1: launch_raster<1>(c, P, na, a0); break;
             case 2: launch_raster<2>(c, P, na, a0); break;
-            default: launch_raster<4>(c, P, na, a0); break;
+            case 4: launch_raster<4>(c, P, na, a0); break;
+            case 8: launch_raster<8>(c, P, na, a0); break;
+            default: launch_raster<16>(c, P, na, a0); break;
         }
         k2_end(c, ev);
         return;
@@ -694,8 +696,10 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
         A.inv_s2 = m.inv_s2;
         A.clamp = m.clamp;
     }
-    c->NV = max_col <= 128 ? 1 : (max_col <= 256 ? 2 : 4);
-    if (max_col > 512) throw std::runtime_error("column longer than 512 entries");
+    // raster pass: one warp per column, 4 entries per lane per chunk of 128
+    c->NV = 1;
+    while (c->NV < 16 && 128 * c->NV < max_col) c->NV *= 2;
+    if (max_col > 128 * 16) throw std::runtime_error("column longer than 2048 entries");
     if (schedule == 0) {
         std::vector<uint32_t> q = build_queue(n_agents, n_sv_side, colours, n_slices);
         c->queue.alloc(q.size());

@@ -145,6 +145,9 @@ def operator_for(matrices, device: int = 0) -> DeviceOperator:
     return _cached(("op", id(matrices), device), lambda: DeviceOperator(matrices, device), matrices)
 
 
+SV_MAX_VIEWS = 128  # lane-per-view layout: 4 groups of 32 views per agent
+
+
 class AgentPlan(_Context):
     """Context with the layouts of ``agent_views`` (one tuple of view indices per local agent)."""
 
@@ -153,9 +156,13 @@ class AgentPlan(_Context):
         super().__init__(device)
         if schedule not in SCHEDULES:
             raise ValueError(f"schedule must be one of {sorted(SCHEDULES)}")
-        self.schedule = schedule
         self.load_matrix(matrices)
         self.agent_views = [tuple(int(v) for v in vs) for vs in agent_views]
+        if schedule == "sv" and max(len(v) for v in self.agent_views) > SV_MAX_VIEWS and int(n_slices) == 1:
+            # the lane-per-view super-voxel layout holds at most 4 x 32 views per agent;
+            # agents with more views (few agents over many views, centralized ICD) run the raster pass
+            schedule = "raster"
+        self.schedule = schedule
         counts = np.array([len(v) for v in self.agent_views], np.int32)
         flat = np.array([v for vs in self.agent_views for v in vs], np.int32)
         sv_eff = sv
