@@ -441,16 +441,25 @@ __global__ void __launch_bounds__(32, MACE_K2_MINB) k_icd_sv(PassParams P)
             step(b + 1, nxt, cur);
         }
 
-        // -- 5. fold the band's net change into global e; prefetch the next tile's e windows;
-        // write z, Mann, partial norms
+        // -- 5. fold the band's net change into global e (vector red.add over the window's aligned
+        // 16-byte span: rows outside the window add +0); write z, Mann, partial norms
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
-            const int cnt = myb[g].y;
-            float* ep = eg + myb[g].x;
+            const int st = myb[g].x, cnt = myb[g].y, s0 = st & 3;
+            float* ep = eg + (st - s0);
             const float* d = sb + g * W * U + lane;
-            for (int o = 0; o < cnt; ++o) {
-                const float dv = d[o * U] - d[o * U + 64];
-                if (dv != 0.f) asm volatile("red.global.add.f32 [%0], %1;" ::"l"(ep + o), "f"(dv) : "memory");
+            const int nv = (cnt + s0 + 3) >> 2;
+            for (int v = 0; v < nv; ++v) {
+                float dv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int o = 4 * v + i - s0;
+                    dv[i] = (o >= 0 && o < cnt) ? d[o * U] - d[o * U + 64] : 0.f;
+                }
+                if (dv[0] != 0.f || dv[1] != 0.f || dv[2] != 0.f || dv[3] != 0.f)
+                    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(ep + 4 * v), "f"(dv[0]),
+                                 "f"(dv[1]), "f"(dv[2]), "f"(dv[3])
+                                 : "memory");
             }
         }
 
