@@ -31,10 +31,13 @@ namespace {
 
 constexpr int kC = 64;             // channels
 constexpr int kTileX = 128;        // output pixels per tile (one row segment)
-constexpr int kHaloX = kTileX + 2;  // 130
+// halo row in shared memory: 18 chunks of 8 px from x0 - 8 (TMA moves whole 128-byte chunks;
+// the 3x3 window spans pixels x0 - 1 .. x0 + 128, i.e. slot pixels 7 .. 136)
+constexpr int kHaloX = kTileX + 16;  // 144
+constexpr int kHaloOff = 7;         // pixel of the slot that holds x0 - 1
 constexpr int kSlots = 6;          // ring of halo rows (TMA runs up to 3 rows ahead)
 constexpr int kAcc = 4;            // TMEM accumulators (4 x 64 fp32 columns)
-constexpr int kSlotBytes = 8 * kHaloX * 16;         // 16,640
+constexpr int kSlotBytes = 8 * kHaloX * 16;         // 18,432
 constexpr int kWBytes = 9 * kC * kC * 2;            // 73,728
 constexpr int kSmem = kWBytes + kSlots * kSlotBytes + 1024;
 
@@ -61,7 +64,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity)
 }
 __device__ __forceinline__ void tma_row(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar)
 {
-    // 4-D box {8 ch, 130 px, 1 row, 8 groups} at (0, x, y, 0)
+    // 4-D box {64 = 8 px x 8 ch, 18 chunks, 1 row, 8 groups} at (0, x chunk, y, 0)
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
         "[%6];" ::"r"(s_u32(dst)),
@@ -117,9 +120,15 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar)
 //   warps 2..5         epilogue:     tcgen05.ld -> ReLU -> bf16 -> blocked stores, acc_empty
 // (warp i may only touch TMEM lanes 32*(i%4)..+31, so warps 2..5 cover all 128 rows.)
 // Grid: one CTA per (128-px strip, run of rows), one CTA per SM.
+#ifdef K5_TRACE  // profiling builds only (tools/micro/k5_trace.cu): per-CTA clock64 timeline of a layer
+__device__ long long g_k5_trace[148][64];  // [0] start, [1] weights landed, [2+2t] tile t issued, [3+2t] tile t stored
+#define K5T(i) g_k5_trace[blockIdx.x][(i)] = clock64()
+#else
+#define K5T(i)
+#endif
 __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CUtensorMap amap,
                                                       const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* out,
-                                                      int H, int W, int rows_per_cta)
+                                                      int H, int W, int Wp, int rows_per_cta)
 {
     extern __shared__ __align__(1024) unsigned char sm[];
     unsigned char* sw = sm;                     // weights: [tap 9][ic-group 8][oc 64][8 ic]
@@ -133,6 +142,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kAcc);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) K5T(0);
     const int strips = (W + kTileX - 1) / kTileX;
     const int strip = blockIdx.x % strips;
     const int x0 = strip * kTileX;
@@ -172,13 +182,14 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
                 const int q = r - rbase, s = q % kSlots, u = q / kSlots;
                 if (u >= 1) mbar_wait(sempty + s, (uint32_t)((u - 1) & 1));
                 mbar_expect(sfull + s, kSlotBytes);
-                tma_row(slots + s * kSlotBytes, &amap, x0 - 1, r, sfull + s);
+                tma_row(slots + s * kSlotBytes, &amap, x0 / 8 - 1, r, sfull + s);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer
             const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
             mbar_wait(wbar, 0);
+            K5T(1);
             for (int y = y0; y < y1; ++y) {
                 const int t = y - y0, b = t % kAcc, ub = t / kAcc;
                 if (ub >= 1) mbar_wait(aempty + b, (uint32_t)((ub - 1) & 1));
@@ -198,7 +209,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
                     for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
-                            const uint64_t a = a0 + (uint64_t)((dx * 16 + 2 * j * (kHaloX * 16)) >> 4);
+                            const uint64_t a = a0 + (uint64_t)(((kHaloOff + dx) * 16 + 2 * j * (kHaloX * 16)) >> 4);
                             const uint64_t bd = b0 + (uint64_t)(((dy * 3 + dx) * (kC * kC * 2) + 2 * j * (kC * 16)) >> 4);
                             umma(d, a, bd, (dy | dx | j) != 0);
                         }
@@ -206,6 +217,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
                 }
                 umma_commit(afull + b);
                 umma_commit(sempty + (y - 1 - rbase) % kSlots);  // row y-1: last reader was tile y
+                K5T(2 + 2 * t);
             }
         }
     } else {  // ---- epilogue warps 2..5
@@ -227,9 +239,9 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(aempty + b)) : "memory");
             const int px = x0 + quad * 32 + lane;
             if (px < W) {
-                // channel-blocked output [group][H][W][8]: each store is 512 B contiguous per warp
-                uint4* dst = reinterpret_cast<uint4*>(out) + ((size_t)y * W + px);
-                const size_t gstride = (size_t)H * W;
+                // channel-blocked output [group][H][Wp][8]: each store is 512 B contiguous per warp
+                uint4* dst = reinterpret_cast<uint4*>(out) + ((size_t)y * Wp + px);
+                const size_t gstride = (size_t)H * Wp;
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     uint32_t pk[4];
@@ -243,6 +255,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
                     dst[q * gstride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
             }
+            if (warp == 2 && lane == 0) K5T(3 + 2 * t);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -253,7 +266,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
 
 // layer 1: x (fp32, rounded to bf16) -> 64 ch, ReLU, bf16 blocked [8][H][W][8].  w1: [9 taps][64 oc] fp32
 __global__ void k_conv_first(const float* __restrict__ x, const float* __restrict__ w1, __nv_bfloat16* out, int H,
-                             int W)
+                             int W, int Wp)
 {
     __shared__ float ws[9 * kC];
     for (int i = threadIdx.x; i < 9 * kC; i += blockDim.x) ws[i] = w1[i];
@@ -267,8 +280,8 @@ __global__ void k_conv_first(const float* __restrict__ x, const float* __restric
         const int sy = yy + t / 3 - 1, sx = xx + t % 3 - 1;
         in[t] = (sy >= 0 && sy < H && sx >= 0 && sx < W) ? __bfloat162float(__float2bfloat16_rn(x[sy * W + sx])) : 0.f;
     }
-    uint4* dst = reinterpret_cast<uint4*>(out) + p;  // channel-blocked [group][H][W][8]
-    const size_t gstride = (size_t)H * W;
+    uint4* dst = reinterpret_cast<uint4*>(out) + ((size_t)yy * Wp + xx);  // channel-blocked [group][H][Wp][8]
+    const size_t gstride = (size_t)H * Wp;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         uint32_t pk[4];
@@ -290,7 +303,7 @@ __global__ void k_conv_first(const float* __restrict__ x, const float* __restric
 
 // layer 17 + residual: out = x - sum_taps sum_ic h[ic] w17[tap][ic]  (fp32)
 __global__ void k_conv_last(const __nv_bfloat16* __restrict__ h, const float* __restrict__ w17,
-                            const float* __restrict__ x, float* out, int H, int W)
+                            const float* __restrict__ x, float* out, int H, int W, int Wp)
 {
     __shared__ float ws[9 * kC];
     for (int i = threadIdx.x; i < 9 * kC; i += blockDim.x) ws[i] = w17[i];
@@ -298,13 +311,13 @@ __global__ void k_conv_last(const __nv_bfloat16* __restrict__ h, const float* __
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= H * W) return;
     const int yy = p / W, xx = p % W;
-    const size_t gstride = (size_t)H * W;
+    const size_t gstride = (size_t)H * Wp;
     float acc = 0.f;
 #pragma unroll
     for (int t = 0; t < 9; ++t) {
         const int sy = yy + t / 3 - 1, sx = xx + t % 3 - 1;
         if (sy < 0 || sy >= H || sx < 0 || sx >= W) continue;
-        const uint4* src = reinterpret_cast<const uint4*>(h) + ((size_t)sy * W + sx);  // [group][H][W][8]
+        const uint4* src = reinterpret_cast<const uint4*>(h) + ((size_t)sy * Wp + sx);  // [group][H][Wp][8]
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const uint4 v = __ldg(src + q * gstride);
@@ -338,14 +351,16 @@ EncodeTiledFn encode_fn()
     return fn;
 }
 
-// 4-D view of a channel-blocked [8][H][W][8] bf16 image: (ch-in-group 8, x, y, group 8), box {8, 130, 1, 8}
-CUtensorMap make_act_map(void* base, int H, int W)
+// 4-D view of a channel-blocked [8][H][Wp][8] bf16 image (row pitch Wp = W rounded up to 8 px,
+// padding columns zero) in 8-pixel chunks: (64 elements = 8 px x 8 ch, x chunk, y, group 8),
+// box {64, 18, 1, 8}: every TMA row is 128 B
+CUtensorMap make_act_map(void* base, int H, int Wp)
 {
     CUtensorMap m;
-    const cuuint64_t dims[4] = {8, (cuuint64_t)W, (cuuint64_t)H, 8};
-    // channel-blocked global layout [group 8][H][W][8 ch]: a halo row of one group is 130 x 16 B contiguous
-    const cuuint64_t strides[3] = {16, (cuuint64_t)W * 16, (cuuint64_t)H * W * 16};  // bytes, dims 1..3
-    const cuuint32_t box[4] = {8, (cuuint32_t)kHaloX, 1, 8};
+    const cuuint64_t dims[4] = {64, (cuuint64_t)Wp / 8, (cuuint64_t)H, 8};
+    // a halo row of one group is 144 x 16 B contiguous
+    const cuuint64_t strides[3] = {128, (cuuint64_t)Wp * 16, (cuuint64_t)H * Wp * 16};  // bytes, dims 1..3
+    const cuuint32_t box[4] = {64, (cuuint32_t)(kHaloX / 8), 1, 8};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -361,6 +376,10 @@ CUtensorMap make_act_map(void* base, int H, int W)
         cudaError_t e_ = (x);                                                                              \
         if (e_ != cudaSuccess) throw std::runtime_error(std::string(#x) + ": " + cudaGetErrorString(e_)); \
     } while (0)
+
+#ifdef K5_TRACE
+void k5_trace_copy(long long* host) { cudaMemcpyFromSymbol(host, g_k5_trace, sizeof(g_k5_trace)); }
+#endif
 
 void Cnn::set_weights(const uint16_t* bf16, int layers, int channels)
 {
@@ -404,10 +423,13 @@ void Cnn::ensure(int h, int w)
     if (h == H && w == W && act0.p) return;
     H = h;
     W = w;
-    act0.alloc((size_t)H * W * kC);
-    act1.alloc((size_t)H * W * kC);
-    map0 = make_act_map(act0.p, H, W);
-    map1 = make_act_map(act1.p, H, W);
+    Wp = (w + 7) & ~7;
+    act0.alloc((size_t)H * Wp * kC);
+    act1.alloc((size_t)H * Wp * kC);
+    CKC(cudaMemset(act0.p, 0, (size_t)H * Wp * kC * 2));  // padding columns stay zero (never written)
+    CKC(cudaMemset(act1.p, 0, (size_t)H * Wp * kC * 2));
+    map0 = make_act_map(act0.p, H, Wp);
+    map1 = make_act_map(act1.p, H, Wp);
     CKC(cudaFuncSetAttribute(k_conv64_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
 }
 
@@ -416,7 +438,7 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
     if (!ready) throw std::runtime_error("denoiser weights not set");
     ensure(h, w);
     const int npx = H * W;
-    k_conv_first<<<(npx + 255) / 256, 256, 0, s>>>(x, w_first.p, act0.p, H, W);
+    k_conv_first<<<(npx + 255) / 256, 256, 0, s>>>(x, w_first.p, act0.p, H, W, Wp);
     // one CTA per (128-px strip, run of rows); one CTA per SM (140 KB smem)
     const int strips = (W + kTileX - 1) / kTileX;
     const int ctas_y = std::max(1, num_sms / strips);
@@ -425,10 +447,10 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
     for (int l = 0; l < 15; ++l) {
         const CUtensorMap& m = (l & 1) ? map1 : map0;
         __nv_bfloat16* dst = (l & 1) ? act0.p : act1.p;
-        k_conv64_tc<<<ctas, 192, kSmem, s>>>(m, w_mid.p + (size_t)l * 9 * kC * kC, dst, H, W, per);
+        k_conv64_tc<<<ctas, 192, kSmem, s>>>(m, w_mid.p + (size_t)l * 9 * kC * kC, dst, H, W, Wp, per);
     }
     // 15 middle layers: the last one wrote act1 (l = 14 even -> dst act1)
-    k_conv_last<<<(npx + 255) / 256, 256, 0, s>>>(act1.p, w_last.p, x, out, H, W);
+    k_conv_last<<<(npx + 255) / 256, 256, 0, s>>>(act1.p, w_last.p, x, out, H, W, Wp);
     CKC(cudaGetLastError());
     if (launches) *launches += 17;
 }
