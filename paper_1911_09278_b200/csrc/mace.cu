@@ -176,9 +176,28 @@ template <int S, int K, int NG>
 static void launch_sv(Ctx* c, const PassParams& P, int items, int agents_in_queue)
 {
     auto kern = k_icd_sv<S, K, NG>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sv_smem));
-    int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSvThreads, c->sv_smem));
+    // occupancy of this instantiation at this shared-memory size, queried once per (device, size);
+    // the kernel's dynamic shared-memory limit only ever grows (per device)
+    static thread_local std::vector<std::pair<std::pair<int, size_t>, int>> occ;
+    static thread_local std::vector<std::pair<int, size_t>> limit;
+    size_t* lim = nullptr;
+    for (auto& e : limit)
+        if (e.first == c->device) lim = &e.second;
+    if (!lim) {
+        limit.push_back({c->device, 0});
+        lim = &limit.back().second;
+    }
+    if (c->sv_smem > *lim) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sv_smem));
+        *lim = c->sv_smem;
+    }
+    int nb = -1;
+    for (auto& e : occ)
+        if (e.first.first == c->device && e.first.second == c->sv_smem) nb = e.second;
+    if (nb < 0) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSvThreads, c->sv_smem));
+        occ.push_back({{c->device, c->sv_smem}, nb});
+    }
     if (nb < 1) throw std::runtime_error("super-voxel kernel does not fit on an SM (band too large)");
     // Concurrency bound: at most a fraction `sv_frac` of an agent's tiles are in flight at once
     // (bounded staleness), never fewer than one tile per agent, never more than
