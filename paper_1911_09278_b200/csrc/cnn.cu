@@ -143,6 +143,9 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) K5T(0);
+    // programmatic dependent launch: the next layer may start its prologue (TMEM, barriers,
+    // weights) as soon as SMs free up; it waits for this grid before touching activations
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int strips = (W + kTileX - 1) / kTileX;
     const int strip = blockIdx.x % strips;
     const int x0 = strip * kTileX;
@@ -178,6 +181,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
         if (lane == 0) {  // ---- TMA producer
             mbar_expect(wbar, kWBytes);
             bulk_copy(sw, wts, kWBytes, wbar);
+            asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous layer's activations
             for (int r = y0 - 1; r <= y1; ++r) {
                 const int q = r - rbase, s = q % kSlots, u = q / kSlots;
                 if (u >= 1) mbar_wait(sempty + s, (uint32_t)((u - 1) & 1));
@@ -269,6 +273,7 @@ __global__ void k_conv_first(const float* __restrict__ x, const float* __restric
                              int W, int Wp)
 {
     __shared__ float ws[9 * kC];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int i = threadIdx.x; i < 9 * kC; i += blockDim.x) ws[i] = w1[i];
     __syncthreads();
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -307,6 +312,7 @@ __global__ void k_conv_last(const __nv_bfloat16* __restrict__ h, const float* __
 {
     __shared__ float ws[9 * kC];
     for (int i = threadIdx.x; i < 9 * kC; i += blockDim.x) ws[i] = w17[i];
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the last 64-channel layer
     __syncthreads();
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= H * W) return;
@@ -444,13 +450,35 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
     const int ctas_y = std::max(1, num_sms / strips);
     const int per = (H + ctas_y - 1) / ctas_y;  // rows per CTA
     const int ctas = strips * ((H + per - 1) / per);
+    // layers 2..17 are launched with programmatic stream serialization (PDL): each one's prologue
+    // overlaps the previous layer's tail; griddepcontrol.wait orders the activation reads
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
     for (int l = 0; l < 15; ++l) {
         const CUtensorMap& m = (l & 1) ? map1 : map0;
         __nv_bfloat16* dst = (l & 1) ? act0.p : act1.p;
-        k_conv64_tc<<<ctas, 192, kSmem, s>>>(m, w_mid.p + (size_t)l * 9 * kC * kC, dst, H, W, Wp, per);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(ctas);
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = kSmem;
+        cfg.stream = s;
+        cfg.attrs = pdl;
+        cfg.numAttrs = 1;
+        CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc, m, (const __nv_bfloat16*)(w_mid.p + (size_t)l * 9 * kC * kC), dst,
+                               H, W, Wp, per));
     }
     // 15 middle layers: the last one wrote act1 (l = 14 even -> dst act1)
-    k_conv_last<<<(npx + 255) / 256, 256, 0, s>>>(act1.p, w_last.p, x, out, H, W, Wp);
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((npx + 255) / 256);
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cfg.attrs = pdl;
+        cfg.numAttrs = 1;
+        CKC(cudaLaunchKernelEx(&cfg, k_conv_last, (const __nv_bfloat16*)act1.p, (const float*)w_last.p, x, out, H, W,
+                               Wp));
+    }
     CKC(cudaGetLastError());
     if (launches) *launches += 17;
 }
