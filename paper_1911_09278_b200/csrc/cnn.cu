@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
                 const int q = r - rbase, s = q % kSlots, u = q / kSlots;
                 if (u >= 1) mbar_wait(sempty + s, (uint32_t)((u - 1) & 1));
                 mbar_expect(sfull + s, kSlotBytes);
+                if (q < 16) K5T(32 + q);  // TMA issue time of ring row q
                 tma_row(slots + s * kSlotBytes, &amap, x0 / 8 - 1, r, sfull + s);
             }
         }
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
                 for (int r = y - 1; r <= y + 1; ++r) {
                     const int q = r - rbase;
                     mbar_wait(sfull + q % kSlots, (uint32_t)((q / kSlots) & 1));
+                    if (r == y + 1 && q < 16) K5T(48 + q);  // ring row q landed (as seen by the MMA issuer)
                 }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t d = tmem + (uint32_t)(b * 64);

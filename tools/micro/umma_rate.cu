@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(128, 1) k(int iters, long long* out)
     __shared__ __align__(8) uint64_t bar;
     const int warp = threadIdx.x >> 5;
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(&tslot)), "n"(256));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(&tslot)), "n"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (threadIdx.x == 32) {
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(128, 1) k(int iters, long long* out)
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
 
 template <int N, int MODE>
@@ -105,6 +105,7 @@ int main()
     run<64, 3>(sms);
     run<128, 2>(sms);
     run<128, 3>(sms);
+    run<192, 2>(sms);
     run<128, 0>(sms);
     run<128, 1>(sms);
     run<256, 0>(sms);
