@@ -269,3 +269,46 @@ def test_agents_with_many_views_take_the_raster_pass():
     agents = O.build_agents(mats, y, lam, 2, sigma, O.Prior("qggmrf", 50.0, 2.0, 1.2, 1.0, 0.01), ns)
     run = O.mace_run(agents, iters, 0.8)
     assert rel(res.image, run.image) < 1e-4
+
+
+def _clamp_problem():
+    """Low-count scan of a sparse phantom: the unconstrained iterates go negative in the background,
+    so the non-negativity clamp (icd.py:130-134, clamp_nonneg) is active on many pixels."""
+    ns, nv, nc = 32, 45, 47
+    pitch = 4.0
+    geom = mb.Geometry(ns, pitch, nv, nc, pitch)
+    mats = mb.build_system_matrix(geom)
+    ph = gen.ellipse_phantom(ns, pitch, 3, seed=21) * 0.3
+    y, lam = gen.poisson_sinogram(gen.host_forward_project(mats, ph), 300.0, seed=22)
+    prior = mb.PriorParams("qggmrf", 5.0, 2.0, 1.2, 1.0, 0.01)
+    return geom, mats, y, lam, mb.ReconProblem(geom, mats, y, lam, prior), O.Prior("qggmrf", 5.0, 2.0, 1.2, 1.0, 0.01)
+
+
+def test_clamped_mace_raster_matches_oracle():
+    geom, mats, y, lam, prob, oprior = _clamp_problem()
+    iters, sigma, N = 80, 3e-4, 4
+    cfg = mb.MaceConfig(n_subsets=N, rho=0.8, sigma=sigma, max_outer=iters, tol=1e-300, residuals="none",
+                        schedule="raster", clamp_nonneg=True)
+    res = _fixed(mb.mace_solve, prob, cfg)
+    run = O.mace_run(O.build_agents(mats, y, lam, N, sigma, oprior, geom.n_side, clamp=True), iters, 0.8)
+    assert rel(res.image, run.image) < 1e-4
+    free = O.mace_run(O.build_agents(mats, y, lam, N, sigma, oprior, geom.n_side), iters, 0.8)
+    assert free.image.min() < -1e-4  # the clamp was active
+
+
+def test_clamped_mace_sv_reaches_the_clamped_map():
+    """super-voxel schedule (4-pixel batches, clamp inside the exact in-batch recurrence) converges to
+    the fixed point of the clamped centralized ICD"""
+    geom, mats, y, lam, prob, oprior = _clamp_problem()
+    cfg = mb.MaceConfig(n_subsets=4, rho=0.8, sigma=3e-4, max_outer=10000, tol=1e-300, residuals="none",
+                        schedule="sv", sv_side=4, clamp_nonneg=True)
+    res = _fixed(mb.mace_solve, prob, cfg)
+    ag = O.Agent(mats, y, lam, range(geom.n_views), 1, None, oprior, geom.n_side, clamp=True)
+    v = np.zeros(ag.n)
+    for _ in range(5000):
+        dsq = ag.run_range(v, 0, ag.n)
+        if np.sqrt(dsq) < 1e-11 * max(np.linalg.norm(ag.state), 1e-300):
+            break
+    assert ag.state.min() >= 0.0
+    assert res.image.min() >= -1e-9  # the consensus average of the stack, non-negative up to rounding
+    assert rel(res.image, ag.state) < 2e-3
