@@ -489,7 +489,11 @@ def run_batch(args):
                 "note": "mace_solve_batch() on host arrays"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                      "frac": achieved / pk.get("hbm_gbs"), "traffic": None, "kernel": "k_icd_sv (K2), slices batched",
-                     "bytes_per_launch": alg, "k2_avg_ms": k2_avg, "k2_share": k2_ms / ms},
+                     "bytes_per_launch": alg, "k2_avg_ms": k2_avg, "k2_share": k2_ms / ms,
+                     "note": "SURVEY 8(d) counts A once per launch for the 64 slices that share it (B_upd = 8c/64 + "
+                             "16 + 12 R/n), so the HBM fraction is nominal; per slice the kernel streams the A "
+                             "records from L2 and is bound by the L1 data pipe like config 1 (k2_ms_per_slice)",
+                     "k2_ms_per_slice": k2_avg / S},
         "gpu_launches": (3 + 4 * iters) * args.steps, "clocks": clk.summary(),
         "setup_s": {"scan": t_scan, "plan": t_plan},
     }
