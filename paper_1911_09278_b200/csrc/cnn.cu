@@ -308,27 +308,40 @@ __global__ void k_conv_first(const float* __restrict__ x, const float* __restric
     }
 }
 
-// layer 17 + residual: out = x - sum_taps sum_ic h[ic] w17[tap][ic]  (fp32)
-__global__ void k_conv_last(const __nv_bfloat16* __restrict__ h, const float* __restrict__ w17,
-                            const float* __restrict__ x, float* out, int H, int W, int Wp)
+// layer 17 + residual: out = x - sum_taps sum_ic h[ic] w17[tap][ic]  (fp32).  16 x 16 output pixels
+// per block; the 18 x 18 x 64-channel input tile is staged once in shared memory (coalesced 16-byte
+// loads, zero outside the image), then every pixel reads its 9 taps from there.
+constexpr int kLastT = 16;
+__global__ void __launch_bounds__(kLastT * kLastT) k_conv_last(const __nv_bfloat16* __restrict__ h,
+                                                                const float* __restrict__ w17,
+                                                                const float* __restrict__ x, float* out, int H, int W,
+                                                                int Wp)
 {
+    constexpr int TT = kLastT + 2;
     __shared__ float ws[9 * kC];
-    for (int i = threadIdx.x; i < 9 * kC; i += blockDim.x) ws[i] = w17[i];
+    __shared__ uint4 tile[8][TT][TT];  // [channel group][row][col], 41.5 KB
+    const int tid = threadIdx.x;
+    for (int i = tid; i < 9 * kC; i += blockDim.x) ws[i] = w17[i];
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the last 64-channel layer
-    __syncthreads();
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= H * W) return;
-    const int yy = p / W, xx = p % W;
+    const int bx = blockIdx.x * kLastT, by = blockIdx.y * kLastT;
     const size_t gstride = (size_t)H * Wp;
+    for (int i = tid; i < 8 * TT * TT; i += blockDim.x) {
+        const int g = i / (TT * TT), r = (i / TT) % TT, c = i % TT;
+        const int sy = by + r - 1, sx = bx + c - 1;
+        tile[g][r][c] = (sy >= 0 && sy < H && sx >= 0 && sx < W)
+                            ? __ldg(reinterpret_cast<const uint4*>(h) + g * gstride + (size_t)sy * Wp + sx)
+                            : make_uint4(0u, 0u, 0u, 0u);
+    }
+    __syncthreads();
+    const int tx = tid % kLastT, ty = tid / kLastT;
+    const int xx = bx + tx, yy = by + ty;
+    if (xx >= W || yy >= H) return;
     float acc = 0.f;
 #pragma unroll
     for (int t = 0; t < 9; ++t) {
-        const int sy = yy + t / 3 - 1, sx = xx + t % 3 - 1;
-        if (sy < 0 || sy >= H || sx < 0 || sx >= W) continue;
-        const uint4* src = reinterpret_cast<const uint4*>(h) + ((size_t)sy * Wp + sx);  // [group][H][Wp][8]
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const uint4 v = __ldg(src + q * gstride);
+            const uint4 v = tile[q][ty + t / 3][tx + t % 3];
             const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -339,6 +352,7 @@ __global__ void k_conv_last(const __nv_bfloat16* __restrict__ h, const float* __
             }
         }
     }
+    const size_t p = (size_t)yy * W + xx;
     out[p] = x[p] - acc;
 }
 
@@ -473,8 +487,8 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
     // 15 middle layers: the last one wrote act1 (l = 14 even -> dst act1)
     {
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((npx + 255) / 256);
-        cfg.blockDim = dim3(256);
+        cfg.gridDim = dim3((W + kLastT - 1) / kLastT, (H + kLastT - 1) / kLastT);
+        cfg.blockDim = dim3(kLastT * kLastT);
         cfg.stream = s;
         cfg.attrs = pdl;
         cfg.numAttrs = 1;
