@@ -51,6 +51,10 @@ int mace_abi_version(void);
 int mace_sysmat_trace(int n_side, double pixel_pitch, int n_views, int n_channels, const double* ux,
                       const double* uy, const double* ex, const double* ey, const double* offsets, int n_threads,
                       void** handle);
+/* MACEMAT1 file (save_system_matrix's cache format, geometry.py:293-342) -> the same per-view
+ * handle as mace_sysmat_trace; dims3 = n_views, n_channels, n_pixels.  Replaces
+ * load_system_matrix (geometry.py:316-342) without per-row Python parsing. */
+int mace_sysmat_read(const char* path, int64_t* dims3, void** handle);
 int64_t mace_sysmat_view_nnz(void* handle, int view);
 /* copies view `view` out (row_ptr: n_channels+1 int64, cols: nnz int32, lens: nnz float64) and frees it */
 int mace_sysmat_take_view(void* handle, int view, int64_t* row_ptr, int32_t* cols, double* lens);
@@ -91,6 +95,8 @@ int mace_refresh(void* ctx, int local);
 int mace_pass(void* ctx, int local, const float* v, int n_passes, int64_t s_begin, int64_t s_end, double* dsq);
 
 int mace_forward_project(void* ctx, const float* x, float* out);
+/* out[n] (fp64) = A^T sino: back_project geometry.py:273-282, the exact transpose of forward_project */
+int mace_back_project(void* ctx, const float* sino, double* out);
 int mace_cost(void* ctx, const float* x, double beta, double* like, double* prior);
 /* gradient of the MAP cost (models.py:235-278) at x: norms[3] = |grad|, |data part|, |prior part|;
  * grad_out[n] optional (fp64).  A fixed-point certificate where no converged oracle exists. */

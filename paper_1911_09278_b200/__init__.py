@@ -6,8 +6,8 @@ kernels in ``libmace_b200.so`` (see include/mace_b200.h).
 """
 
 from .denoisers import DenoiserSpec, denoise, make_denoiser
-from .geometry import (Geometry, SparseViewMatrix, ViewSubset, build_system_matrix, forward_project,
-                       partition_views)
+from .geometry import (Geometry, SparseViewMatrix, ViewSubset, back_project, build_system_matrix, forward_project,
+                       load_system_matrix, partition_views, roi_mask, save_system_matrix)
 from .icd import (REFRESH_EVERY, AgentWorkspace, ConvergenceError, icd_map_solve, partial_update_prox,
                   pixel_update, prox_solve)
 from .mace import (ConvergenceLog, EquitCounter, MaceConfig, MaceResult, ResidualReport, WorkerPool, average,

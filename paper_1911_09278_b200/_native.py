@@ -27,6 +27,7 @@ _SIGS = {
     "mace_abi_version": (c_int, []),
     "mace_sysmat_trace": (c_int, [c_int, c_double, c_int, c_int, P, P, P, P, P, c_int, ctypes.POINTER(c_void_p)]),
     "mace_sysmat_view_nnz": (c_int64, [P, c_int]),
+    "mace_sysmat_read": (c_int, [ctypes.c_char_p, P, ctypes.POINTER(c_void_p)]),
     "mace_sysmat_take_view": (c_int, [P, c_int, P, P, P]),
     "mace_sysmat_free": (None, [P]),
     "mace_ctx_create": (c_int, [c_int, ctypes.POINTER(c_void_p)]),
@@ -50,6 +51,7 @@ _SIGS = {
     "mace_forward_project": (c_int, [P, P, P]),
     "mace_cost": (c_int, [P, P, c_double, P, P]),
     "mace_gradient": (c_int, [P, P, c_double, P, P]),
+    "mace_back_project": (c_int, [P, P, P]),
     "mace_stack_init": (c_int, [P, P, c_int]),
     "mace_set_ref": (c_int, [P, P]),
     "mace_states_from": (c_int, [P, c_int]),

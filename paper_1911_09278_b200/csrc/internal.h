@@ -22,6 +22,7 @@ struct SysMat {
 };
 SysMat* sysmat_trace(int n_side, double pitch, int n_views, int n_ch, const double* ux, const double* uy,
                      const double* ex, const double* ey, const double* offsets, int n_threads);
+SysMat* sysmat_read(const char* path, int64_t* n_pixels);  // MACEMAT1 file
 
 // ---- per-agent device layouts (built on the host from the global CSR)
 //

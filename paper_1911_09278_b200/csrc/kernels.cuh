@@ -398,6 +398,19 @@ __global__ void k_bp_rows(FPParams F, int n_rows, const float* Ax, const float* 
     }
 }
 
+// back-projection out[s] += sum_rows a_rs sino_r (geometry.py:273-282), one warp per row, fp64 atomics
+__global__ void k_bp_sino(FPParams F, int n_rows, const float* sino, double* out)
+{
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int g = gw; g < n_rows; g += nw) {
+        const double r = (double)sino[g];
+        if (r == 0.0) continue;
+        for (int64_t k = F.rp[g] + lane; k < F.rp[g + 1]; k += 32) atomicAdd(out + F.cols[k], (double)F.vals[k] * r);
+    }
+}
+
 // MAP-cost gradient, prior part: grad[s] += beta sum_k w_k rho'(x_s - x_k) (+ 2 beta eps x_s, quadratic)
 __global__ void k_prior_grad(const float* x, int n_side, PriorC P, double beta, double* grad)
 {

@@ -416,6 +416,18 @@ int mace_sysmat_trace(int n_side, double pixel_pitch, int n_views, int n_channel
     API_END
 }
 
+int mace_sysmat_read(const char* path, int64_t* dims3, void** handle)
+{
+    API_BEGIN
+    int64_t n = 0;
+    SysMat* m = sysmat_read(path, &n);
+    dims3[0] = m->n_views;
+    dims3[1] = m->n_ch;
+    dims3[2] = n;
+    *handle = m;
+    API_END
+}
+
 int64_t mace_sysmat_view_nnz(void* handle, int view)
 {
     SysMat* s = static_cast<SysMat*>(handle);
@@ -951,6 +963,26 @@ int mace_cost(void* p, const float* x, double beta, double* like, double* prior)
     for (int i = 0; i < b2; ++i) P += h[b1 + i];
     *like = L;
     *prior = beta * P;
+    API_END
+}
+
+// out = A^T sino (fp64 accumulation), the exact transpose of mace_forward_project (geometry.py:273-282)
+int mace_back_project(void* p, const float* sino, double* out)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    const int rows = c->n_views * c->n_ch;
+    DBuf<float> ds;
+    DBuf<double> dout;
+    ds.alloc(rows);
+    dout.alloc(c->n);
+    CK(cudaMemcpyAsync(ds.p, sino, sizeof(float) * rows, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(dout.p, 0, sizeof(double) * c->n, c->stream));
+    FPParams F{c->rp.p, c->cols.p, c->vals.p, c->n_ch};
+    k_bp_sino<<<std::max(1, std::min(c->num_sms * 8, (rows + 7) / 8)), 256, 0, c->stream>>>(F, rows, ds.p, dout.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, dout.p, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
     API_END
 }
 

@@ -10,7 +10,11 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -179,6 +183,53 @@ SysMat* sysmat_trace(int n_side, double pitch, int n_views, int n_ch, const doub
     for (int t = 0; t < n_threads; ++t) th.emplace_back(worker);
     for (auto& t : th) t.join();
     return sm;
+}
+
+// MACEMAT1 reader (format of save_system_matrix, geometry.py:293-342): ASCII "MACEMAT1",
+// ASCII "n_views n_channels n", then per view, per row: uint32 LE count, count x (uint32 LE pixel,
+// float32 LE length).  Lengths come back as float64 (the file holds float32, like the reference's
+// load_system_matrix).  One sequential pass into the per-view CSR, no per-row Python work.
+SysMat* sysmat_read(const char* path, int64_t* n_pixels)
+{
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) throw std::runtime_error(std::string("cannot open ") + path);
+    std::unique_ptr<std::FILE, int (*)(std::FILE*)> guard(f, &std::fclose);
+    char line[256];
+    if (!std::fgets(line, sizeof line, f) || std::string(line).rfind("MACEMAT1", 0) != 0 ||
+        (line[8] != '\n' && line[8] != '\r'))
+        throw std::invalid_argument("bad matrix file magic");
+    long long nv = 0, nc = 0, n = 0;
+    if (!std::fgets(line, sizeof line, f) || std::sscanf(line, "%lld %lld %lld", &nv, &nc, &n) != 3 || nv < 1 ||
+        nc < 1 || n < 1 || n > INT32_MAX)
+        throw std::invalid_argument("bad matrix file header");
+    auto m = std::make_unique<SysMat>();
+    m->n_views = (int)nv;
+    m->n_ch = (int)nc;
+    const long long side = (long long)std::llround(std::sqrt((double)n));
+    m->n_side = side * side == n ? (int)side : 0;
+    m->views.resize(nv);
+    std::vector<uint32_t> rec;
+    for (long long k = 0; k < nv; ++k) {
+        SysMatView& V = m->views[k];
+        V.row_ptr.assign(nc + 1, 0);
+        for (long long d = 0; d < nc; ++d) {
+            uint32_t cnt = 0;
+            if (std::fread(&cnt, 4, 1, f) != 1) throw std::invalid_argument("truncated matrix file");
+            rec.resize(2 * (size_t)cnt);
+            if (cnt && std::fread(rec.data(), 8, cnt, f) != cnt) throw std::invalid_argument("truncated matrix file");
+            for (uint32_t e = 0; e < cnt; ++e) {
+                const uint32_t col = rec[2 * e];
+                float len;
+                std::memcpy(&len, &rec[2 * e + 1], 4);
+                if ((long long)col >= n) throw std::invalid_argument("pixel index out of range in matrix file");
+                V.cols.push_back((int32_t)col);
+                V.lens.push_back((double)len);
+            }
+            V.row_ptr[d + 1] = V.row_ptr[d] + cnt;
+        }
+    }
+    *n_pixels = n;
+    return m.release();
 }
 
 }  // namespace mace

@@ -94,6 +94,12 @@ class DeviceOperator(_Context):
         self.call("mace_forward_project", N.ptr(x), N.ptr(out))
         return out
 
+    def back_project(self, sino) -> np.ndarray:
+        s32 = N.f32(sino)
+        out = np.empty(self.n_side * self.n_side, np.float64)
+        self.call("mace_back_project", N.ptr(s32), N.ptr(out))
+        return out
+
     def load_data(self, y, weights):
         y32, w32 = N.f32(y), N.f32(weights)
         self.call("mace_load_data", N.ptr(y32), N.ptr(w32))

@@ -25,7 +25,14 @@ __all__ = [
     "build_system_matrix",
     "forward_project",
     "global_csr",
+    "save_system_matrix",
+    "load_system_matrix",
+    "back_project",
+    "roi_mask",
+    "MATRIX_MAGIC",
 ]
+
+MATRIX_MAGIC = "MACEMAT1"
 
 
 @dataclass(frozen=True)
@@ -146,6 +153,78 @@ def build_system_matrix(geom: Geometry, n_threads: int = 0) -> list[SparseViewMa
     finally:
         L.mace_sysmat_free(h)
     return out
+
+
+def back_project(matrices, sinogram, device: int = 0) -> np.ndarray:
+    """Exact transpose of forward_project (geometry.py:273-282) on the GPU, fp64 accumulation
+    (float32 operands, like forward_project)."""
+    from .engine import operator_for
+
+    sinogram = np.asarray(sinogram, dtype=np.float64)
+    expected = (len(matrices), matrices[0].n_channels)
+    if sinogram.shape != expected:
+        raise ValueError(f"sinogram must have shape {expected}, got {sinogram.shape}")
+    return operator_for(matrices, device=device).back_project(sinogram)
+
+
+def roi_mask(geom: Geometry) -> np.ndarray:
+    """Pixels whose centres fall in the inscribed circle (geometry.py:285-290)."""
+    half = 0.5 * geom.image_width
+    c = (np.arange(geom.n_side) + 0.5) * geom.pixel_pitch - half
+    xx, yy = np.meshgrid(c, c)
+    return ((xx**2 + yy**2) <= half**2).ravel()
+
+
+def _take_views(L, h, n_views, n_channels, n_pixels) -> list[SparseViewMatrix]:
+    out = []
+    for k in range(n_views):
+        nnz = L.mace_sysmat_view_nnz(h, k)
+        rp = np.empty(n_channels + 1, np.int64)
+        cols = np.empty(nnz, np.int32)
+        lens = np.empty(nnz, np.float64)
+        N.check(L.mace_sysmat_take_view(h, k, N.ptr(rp), N.ptr(cols), N.ptr(lens)), "sysmat_take_view")
+        out.append(SparseViewMatrix(k, n_channels, n_pixels, rp, cols, lens))
+    return out
+
+
+def save_system_matrix(path, matrices: list[SparseViewMatrix]) -> None:
+    """Write the MACEMAT1 cache (geometry.py:293-313): ASCII magic line, ASCII "n_views n_channels n",
+    then per view, per row a uint32 LE count and (uint32 LE pixel, float32 LE length) pairs.  One
+    vectorised record block per view (byte-identical to the reference's per-row writer)."""
+    with open(path, "wb") as fh:
+        fh.write(f"{MATRIX_MAGIC}\n".encode("ascii"))
+        fh.write(f"{len(matrices)} {matrices[0].n_channels} {matrices[0].n_pixels}\n".encode("ascii"))
+        for mat in matrices:
+            rp = np.asarray(mat.row_ptr, np.int64)
+            counts = np.diff(rp).astype("<u4")
+            nnz = int(rp[-1] - rp[0])
+            words = np.empty(mat.n_channels + 2 * nnz, "<u4")
+            # word position of row d's count: d + 2 * (entries before row d)
+            pos = np.arange(mat.n_channels) + 2 * (rp[:-1] - rp[0])
+            words[pos] = counts
+            entry_row = np.repeat(np.arange(mat.n_channels), counts)
+            epos = entry_row + 1 + 2 * np.arange(nnz)
+            words[epos] = np.asarray(mat.cols[rp[0]:rp[-1]], "<u4")
+            words[epos + 1] = np.asarray(mat.lens[rp[0]:rp[-1]], "<f4").view("<u4")
+            fh.write(words.tobytes())
+
+
+def load_system_matrix(path) -> list[SparseViewMatrix]:
+    """Read a MACEMAT1 file (geometry.py:316-342; float32 lengths returned as float64) with the
+    native reader: one sequential pass in C++ into the per-view CSR."""
+    L = N.lib()
+    dims = np.zeros(3, np.int64)
+    h = ctypes.c_void_p()
+    rc = L.mace_sysmat_read(os.fsencode(path), N.ptr(dims), ctypes.byref(h))
+    if rc != 0:
+        msg = L.mace_last_error().decode(errors="replace")
+        if "cannot open" in msg:
+            raise OSError(msg)
+        raise ValueError(msg)  # bad magic / header, truncated file, index out of range
+    try:
+        return _take_views(L, h, int(dims[0]), int(dims[1]), int(dims[2]))
+    finally:
+        L.mace_sysmat_free(h)
 
 
 def global_csr(matrices) -> tuple[np.ndarray, np.ndarray, np.ndarray]:

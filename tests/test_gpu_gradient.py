@@ -52,3 +52,23 @@ def test_gradient_vanishes_at_the_map(golden):
     _, at_map = mb.map_gradient(prob, golden["ell_central"].astype(np.float32))
     # float32 image of a float64 fixed point: only rounding of x is left
     assert at_map[0] < 1e-4 * at0[0]
+
+
+def test_back_project_is_the_transpose_of_forward_project():
+    ns, nv, nc = 32, 45, 47
+    geom = mb.Geometry(ns, 4.0, nv, nc, 4.0)
+    mats = mb.build_system_matrix(geom)
+    rng = np.random.default_rng(11)
+    s = rng.standard_normal((nv, nc))
+    x = rng.standard_normal(ns * ns)
+    bp = mb.back_project(mats, s)
+    want = sum(O.view_csr(m).T @ s[k] for k, m in enumerate(mats))
+    s32 = s.astype(np.float32).astype(np.float64)
+    want32 = sum(O.view_csr(m).astype(np.float32).astype(np.float64).T @ s32[k] for k, m in enumerate(mats))
+    assert np.linalg.norm(bp - want32) <= 1e-12 * np.linalg.norm(want32) * 10
+    assert np.linalg.norm(bp - want) <= 1e-6 * np.linalg.norm(want)
+    # adjointness <A x, s> = <x, A^T s> (the reference's own check, tests/test_geometry.py)
+    lhs = float(np.sum(mb.forward_project(mats, x) * s))
+    assert lhs == pytest.approx(float(x @ bp), rel=1e-5)
+    with pytest.raises(ValueError):
+        mb.back_project(mats, s[:, :-1])
