@@ -175,10 +175,20 @@ def run_ours(args):
     n = geom.n_pixels
     stream = torch.cuda.ExternalStream(plan_stream(plan), device=f"cuda:{local}")
 
+    peer = world > 1 and args.comm == "peer"
+    if peer:
+        pcomm = mb.PeerComm()
+        pcomm.attach(plan)
+        comm = pcomm  # the e2e solves use the same exchange
+        if pnp:
+            den._load(plan)
+
     def solve_device():
         """one step with inputs resident: stack init, X0 = average(w0), refresh e, `iters` iterations"""
         plan.stack_init(None, N if world == 1 else 0)
-        if world > 1:
+        if peer:
+            plan.peer_mean(N)
+        elif world > 1:
             plan.local_sum()
             mb.mace._resolve_comm(True).allreduce(*plan.comm_arrays()[:1], stream=plan.torch_stream())
             plan.mean_from_sum(N)
@@ -187,6 +197,8 @@ def run_ours(args):
         plan.states_from(1 if pnp else 0)
         if world == 1:
             plan.iterate(iters, 0, 0.8, pnp, 1e-300, N, False, device_denoise=pnp)
+        elif peer:  # consensus over NVLink peer memory, the whole loop on the device
+            plan.iterate_peer(iters, 0, 0.8, pnp, 1e-300, N, device_denoise=pnp)
         else:
             c = mb.mace._resolve_comm(True)
             for k in range(iters):
@@ -261,7 +273,8 @@ def run_ours(args):
         "config": {"workload": f"BASELINE config {args.config}: {geom.n_side}^2, {geom.n_views} views x "
                    f"{geom.n_channels} ch, N={N} agents, {iters} iterations, rho=0.8, qGGMRF beta={cfg['beta']}, "
                    f"sigma={cfg['sigma']}", "schedule": args.schedule, "sv_side": args.sv,
-                   "parallelism": f"agents {N} over {world} GPU(s)", "l2": "inputs > L2 (A stream 1.4 GB/iter)",
+                   "parallelism": f"agents {N} over {world} GPU(s)" + (f", consensus: {args.comm}" if world > 1 else ""),
+                   "l2": "inputs > L2 (A stream 1.4 GB/iter)",
                    "final_relnorm": float(lg[-1, 0]) if len(lg) else None},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "note": "mace_solve() on host float64 y/weights; includes H2D, solve, D2H image+stack"},
@@ -514,6 +527,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ttr-iters", type=int, default=3000, help="iterations for time-to-RMSE (0: skip)")
     ap.add_argument("--slices", type=int, default=0, help="config 4: number of slices (default 64)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1: consensus by an NCCL all-reduce on the library stream, or by the library's own "
+                         "push/reduce kernels over NVLink peer memory (PeerComm)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -118,6 +118,14 @@ int mace_comm_buffers(void* ctx, void** wsum, void** sums5);
 int mace_local_sum(void* ctx);
 int mace_mean_from_sum(void* ctx, int n_total);
 int mace_iterate_finish(void* ctx, int n_total, double tol, int iter);
+/* the same loop with the consensus exchanged over NVLink peer memory (k_peer.cuh) instead of a
+ * collective: bytes of the symmetric buffer each rank allocates; setup with every rank's buffer
+ * pointer; stack-average initialisation; `iters` iterations entirely on the device. */
+int mace_peer_bytes(void* ctx, int world, size_t* bytes);
+int mace_peer_setup(void* ctx, int world, int rank, const uint64_t* bufs);
+int mace_peer_mean(void* ctx, int n_total);
+int mace_iterate_peer(void* ctx, int iters, int iter0, double rho, int use_g, double tol, int n_total,
+                      float* ms_out);
 int mace_read_log(void* ctx, int n, double* log, int* done2);
 /* ---- K5: the PnP denoiser agent (17-layer 3x3 conv net, 64 ch, ReLU, out = x - net(x),
  * bf16 weights/activations, tcgen05 implicit GEMM); replaces the `denoiser` callable of

@@ -10,7 +10,7 @@ from .geometry import (Geometry, SparseViewMatrix, ViewSubset, back_project, bui
                        load_system_matrix, partition_views, roi_mask, save_system_matrix)
 from .icd import (REFRESH_EVERY, AgentWorkspace, ConvergenceError, icd_map_solve, partial_update_prox,
                   pixel_update, prox_solve)
-from .mace import (ConvergenceLog, EquitCounter, MaceConfig, MaceResult, ResidualReport, WorkerPool, average,
+from .mace import (ConvergenceLog, EquitCounter, MaceConfig, MaceResult, PeerComm, ResidualReport, WorkerPool, average,
                    consensus_G, consensus_GH, equilibrium_residuals, mace_pnp_solve, mace_solve, mann_step,
                    new_stack, nrmse, reflect_G, mace_solve_batch)
 from .models import QGGMRF, QUADRATIC, PriorParams, ReconProblem, book_to_reference_beta, map_cost, map_gradient, neighbor_table

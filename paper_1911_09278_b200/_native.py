@@ -52,6 +52,10 @@ _SIGS = {
     "mace_cost": (c_int, [P, P, c_double, P, P]),
     "mace_gradient": (c_int, [P, P, c_double, P, P]),
     "mace_back_project": (c_int, [P, P, P]),
+    "mace_peer_bytes": (c_int, [P, c_int, P]),
+    "mace_peer_setup": (c_int, [P, c_int, c_int, P]),
+    "mace_peer_mean": (c_int, [P, c_int]),
+    "mace_iterate_peer": (c_int, [P, c_int, c_int, c_double, c_int, c_double, c_int, P]),
     "mace_stack_init": (c_int, [P, P, c_int]),
     "mace_set_ref": (c_int, [P, P]),
     "mace_states_from": (c_int, [P, c_int]),

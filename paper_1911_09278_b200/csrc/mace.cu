@@ -22,6 +22,7 @@
 #include "kernels.cuh"
 #include "k_sv.cuh"
 #include "k_sweep64.cuh"
+#include "k_peer.cuh"
 #include "cnn.cuh"
 #include "mace_b200.h"
 
@@ -120,6 +121,11 @@ struct Ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // K5 PnP denoiser (cnn.cu)
     Cnn cnn;
+    // consensus across ranks over NVLink peer memory (k_peer.cuh), set up by mace_peer_setup
+    bool peer_on = false;
+    PeerArgs peer{};
+    uint32_t epoch = 0;
+    DBuf<unsigned> peer_counter;
     // optional per-launch timing of K2 (bench roofline): event pairs on the launch stream
     bool time_k2 = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k2ev;
@@ -1150,6 +1156,94 @@ int mace_iterate_local(void* p, double rho, int use_g)
     k_norms<<<kNormBlocks, 256, 0, c->stream>>>(c->part.p, c->n_items, nullptr, 0, c->norm_scratch.p, c->sums5.p,
                                                 c->norm_counter.p, c->done.p);
     CK(cudaGetLastError());
+    API_END
+}
+
+// ------------------------------------------------------------------ consensus over peer memory
+int mace_peer_bytes(void* p, int world, size_t* bytes)
+{
+    API_BEGIN
+    if (world < 1 || world > kMaxPeers) throw std::runtime_error("1..8 ranks per node");
+    *bytes = peer_bytes(world, C(p)->n);
+    API_END
+}
+
+// bufs[world]: every rank's symmetric buffer as seen from this process (device pointers, bufs[rank]
+// local).  Zeroes this rank's flags; the caller barriers before the first exchange.
+int mace_peer_setup(void* p, int world, int rank, const uint64_t* bufs)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world) throw std::runtime_error("bad rank layout");
+    if (c->n_slices != 1) throw std::runtime_error("peer consensus: one slice per context");
+    c->peer = PeerArgs{};
+    for (int r = 0; r < world; ++r) c->peer.buf[r] = reinterpret_cast<unsigned char*>(bufs[r]);
+    c->peer.world = world;
+    c->peer.rank = rank;
+    c->epoch = 0;
+    c->peer_counter.alloc(1);
+    CK(cudaMemsetAsync(c->peer_counter.p, 0, sizeof(unsigned), c->stream));
+    CK(cudaMemsetAsync(c->peer.buf[rank], 0, peer_norm_off(), c->stream));  // flags
+    sync(c);
+    c->peer_on = true;
+    API_END
+}
+
+// one exchange: this rank's local tree sum + c->sums5 (local norms) -> wbar = (sum over ranks) / scale,
+// c->sums5 = the global norms
+static void peer_exchange(Ctx* c, float scale)
+{
+    if (!c->peer_on) throw std::runtime_error("mace_peer_setup first");
+    c->peer.epoch = ++c->epoch;
+    c->peer.parity = (int)(c->epoch & 1u);
+    const int blocks = kRefBlocks;
+    switch (c->n_real) {
+        case 1: k_peer_push<1><<<blocks, 256, 0, c->stream>>>(c->W.p, 1, c->n, c->sums5.p, c->peer, c->peer_counter.p, c->done.p); break;
+        case 2: k_peer_push<2><<<blocks, 256, 0, c->stream>>>(c->W.p, 2, c->n, c->sums5.p, c->peer, c->peer_counter.p, c->done.p); break;
+        case 4: k_peer_push<4><<<blocks, 256, 0, c->stream>>>(c->W.p, 4, c->n, c->sums5.p, c->peer, c->peer_counter.p, c->done.p); break;
+        case 8: k_peer_push<8><<<blocks, 256, 0, c->stream>>>(c->W.p, 8, c->n, c->sums5.p, c->peer, c->peer_counter.p, c->done.p); break;
+        default:
+            k_peer_push<0><<<blocks, 256, 0, c->stream>>>(c->W.p, c->n_real, c->n, c->sums5.p, c->peer, c->peer_counter.p,
+                                                          c->done.p);
+    }
+    k_peer_reduce<<<blocks, 256, 0, c->stream>>>(c->peer, c->n, scale, c->wbar.p, c->sums5.p, c->done.p);
+    CK(cudaGetLastError());
+}
+
+// stack initialisation across ranks: wbar = average of every rank's w0 (mace.py:286 with agents spread)
+int mace_peer_mean(void* p, int n_total)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    CK(cudaMemsetAsync(c->sums5.p, 0, 5 * sizeof(double), c->stream));
+    peer_exchange(c, (float)n_total);
+    API_END
+}
+
+// `iters` MACE iterations with agents on several GPUs, entirely on the device: K2 -> local norms ->
+// push/reduce over peer memory -> stop test (-> K5 if use_g == 2); no host step per iteration.
+int mace_iterate_peer(void* p, int iters, int iter0, double rho, int use_g, double tol, int n_total, float* ms_out)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    ensure_log(c, iter0 + iters);
+    CK(cudaEventRecord(c->ev0, c->stream));
+    for (int k = 0; k < iters; ++k) {
+        run_pass(c, 1, (float)rho, use_g ? c->g.p : c->wbar.p, 0, c->n_local);
+        c->passes++;
+        k_norms<<<kNormBlocks, 256, 0, c->stream>>>(c->part.p, c->n_items, nullptr, 0, c->norm_scratch.p, c->sums5.p,
+                                                    c->norm_counter.p, c->done.p);
+        peer_exchange(c, (float)n_total);
+        k_finish<<<1, 1, 0, c->stream>>>(c->sums5.p, 0.0, tol, iter0 + k, c->log.p, c->done.p, c->head.p);
+        if (c->passes % 50 == 0) refresh(c, 0, c->n_local);
+        if (use_g == 2) cnn_all_slices(c);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(c->ev1, c->stream));
+    if (ms_out) {
+        CK(cudaEventSynchronize(c->ev1));
+        CK(cudaEventElapsedTime(ms_out, c->ev0, c->ev1));
+    }
     API_END
 }
 

@@ -299,6 +299,26 @@ class AgentPlan(_Context):
         self.call("mace_k2_timing", int(bool(enable)), ctypes.byref(ms), ctypes.byref(n))
         return ms.value, n.value
 
+    # ---- consensus over NVLink peer memory (k_peer.cuh)
+    def peer_bytes(self, world) -> int:
+        b = ctypes.c_size_t(0)
+        self.call("mace_peer_bytes", int(world), ctypes.byref(b))
+        return int(b.value)
+
+    def peer_setup(self, world, rank, ptrs):
+        ptrs = np.ascontiguousarray(ptrs, np.uint64)
+        self.call("mace_peer_setup", int(world), int(rank), N.ptr(ptrs))
+
+    def peer_mean(self, n_total):
+        self.call("mace_peer_mean", int(n_total))
+
+    def iterate_peer(self, iters, iter0, rho, use_g, tol, n_total, device_denoise=False) -> float:
+        ms = ctypes.c_float(0.0)
+        mode = 2 if (use_g and device_denoise) else int(bool(use_g))
+        self.call("mace_iterate_peer", int(iters), int(iter0), float(rho), mode, float(tol), int(n_total),
+                  ctypes.byref(ms))
+        return float(ms.value)
+
     def iterate_local(self, rho, use_g):
         self.call("mace_iterate_local", float(rho), int(bool(use_g)))
 

@@ -28,7 +28,7 @@ from .engine import DEFAULT_COLOURS, DEFAULT_SV, plan_for
 from .geometry import partition_views
 from .icd import AgentWorkspace, ConvergenceError, prox_solve
 
-__all__ = ["MaceConfig", "MaceResult", "ConvergenceLog", "ResidualReport", "WorkerPool", "new_stack", "average",
+__all__ = ["PeerComm", "MaceConfig", "MaceResult", "ConvergenceLog", "ResidualReport", "WorkerPool", "new_stack", "average",
            "consensus_G", "reflect_G", "consensus_GH", "mann_step", "mace_solve", "mace_pnp_solve",
            "equilibrium_residuals", "EquitCounter", "nrmse", "mace_solve_batch"]
 
@@ -285,6 +285,29 @@ def _plan_stream(plan):
     return ts() if ts is not None else None
 
 
+class PeerComm(_Comm):
+    """Agents on several GPUs of one node with the consensus exchanged over NVLink peer memory by
+    the library's own kernels (k_peer.cuh: local tree sum pushed into every rank's symmetric
+    buffer, flag, rank-ordered sum) instead of a collective; the whole MACE loop stays on the
+    device.  torch.distributed's symmetric memory provides the buffers and their peer mappings."""
+
+    def attach(self, plan):
+        if getattr(plan, "_peer_comm", None) is self:
+            return
+        import torch
+        import torch.distributed._symmetric_memory as symm
+
+        nbytes = plan.peer_bytes(self.world)
+        buf = symm.empty(nbytes, dtype=torch.uint8, device=f"cuda:{plan.device}")
+        group = self.group if self.group is not None else self.dist.group.WORLD
+        hdl = symm.rendezvous(buf, group)
+        ptrs = np.array(list(hdl.buffer_ptrs), np.uint64)
+        plan.peer_setup(self.world, self.rank, ptrs)
+        plan._peer_keep = (buf, hdl)
+        plan._peer_comm = self
+        self.dist.barrier(group=self.group)  # every rank's flags are zero before the first exchange
+
+
 def _resolve_comm(comm):
     if comm is None or comm is False:
         return None
@@ -331,8 +354,13 @@ def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=
         w_local = np.ascontiguousarray(w0[local], np.float32)
     else:
         w_local = None
+    peer = isinstance(comm, PeerComm)
     if comm is None:
         plan.stack_init(w_local, N)
+    elif peer:
+        comm.attach(plan)
+        plan.stack_init(w_local, 0)
+        plan.peer_mean(N)
     else:
         plan.stack_init(w_local, 0)
         plan.local_sum()
@@ -357,7 +385,9 @@ def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=
     rows = []  # (relnorm, nrmse, wall)
     done = (0, 0)
     it = 0
-    host_loop = comm is not None or (pnp and not device_g)
+    if peer and pnp and not device_g:
+        raise ValueError("the peer-memory consensus needs a device denoiser (CnnDenoiser) or none")
+    host_loop = (comm is not None and not peer) or (pnp and not device_g)
     if not host_loop:
         chunk = config.max_outer
         while it < config.max_outer and done[0] == 0:
@@ -367,7 +397,10 @@ def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=
                 k = 1
             if in_loop:
                 denoiser._load(plan)
-            ms = plan.iterate(k, it, config.rho, pnp, config.tol, N, ref32 is not None, device_denoise=in_loop)
+            if peer:
+                ms = plan.iterate_peer(k, it, config.rho, pnp, config.tol, N, device_denoise=in_loop)
+            else:
+                ms = plan.iterate(k, it, config.rho, pnp, config.tol, N, ref32 is not None, device_denoise=in_loop)
             device_ms += ms
             if pnp and not in_loop:
                 _apply_denoiser(plan, denoiser)

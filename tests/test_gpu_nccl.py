@@ -57,3 +57,43 @@ def test_nccl_stream_ordered_loop_matches_device_loop():
     r_ref = [r["relnorm"] for r in ref.log.rows]
     r_got = [r["relnorm"] for r in got.log.rows]
     assert np.allclose(r_got, r_ref, rtol=1e-5)
+
+
+def test_peer_memory_consensus_matches_device_loop():
+    """PeerComm: the consensus pushed into every rank's symmetric buffer by the library's kernels
+    (k_peer.cuh) and reduced in rank order, the whole loop on the device.  One rank holding every
+    agent must reproduce the single-context loop bit for bit (a one-term rank sum is exact)."""
+    import torch
+    import torch.distributed as dist
+
+    ns, nv, nc, N = 64, 90, 91, 4
+    pitch = 128.0 / ns
+    geom = mb.Geometry(ns, pitch, nv, nc, pitch)
+    mats = mb.build_system_matrix(geom)
+    ph = gen.ellipse_phantom(ns, pitch, 10, seed=6)
+    y, lam = gen.poisson_sinogram(gen.host_forward_project(mats, ph), 1e4, seed=7)
+    prob = mb.ReconProblem(geom, mats, y, lam, mb.PriorParams("qggmrf", 25.0, 2.0, 1.2, 1.0, 0.01))
+    # raster schedule: deterministic, so the two paths can be compared bit for bit
+    cfg = mb.MaceConfig(n_subsets=N, rho=0.8, sigma=2e-4, max_outer=150, tol=1e-300, residuals="none",
+                        schedule="raster")
+
+    def solve(comm):
+        try:
+            return mb.mace_solve(prob, cfg, comm=comm)
+        except mb.ConvergenceError as err:
+            return err.last_iterate
+
+    ref = solve(None)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", world_size=1, rank=0,
+                            device_id=torch.device("cuda:0"))
+    try:
+        got = solve(mb.PeerComm())
+        again = solve(mb.PeerComm())  # a second solve on the same plan re-attaches cleanly
+    finally:
+        dist.destroy_process_group()
+    assert got.iterations == ref.iterations == 150
+    assert np.array_equal(got.image, ref.image)
+    assert np.array_equal(got.stack, ref.stack)
+    assert np.array_equal(again.image, ref.image)
+    assert [r["relnorm"] for r in got.log.rows] == [r["relnorm"] for r in ref.log.rows]
