@@ -122,6 +122,7 @@ struct Ctx {
     // K5 PnP denoiser (cnn.cu)
     Cnn cnn;
     // consensus across ranks over NVLink peer memory (k_peer.cuh), set up by mace_peer_setup
+    bool stack_zero = false;  // the stack was initialised to zero (states_from(0) needs no SpMV)
     bool peer_on = false;
     PeerArgs peer{};
     uint32_t epoch = 0;
@@ -273,6 +274,7 @@ static PassParams base_params(Ctx* c)
 // One pass of every agent in [a0, a0 + na) (or all local agents if na == n_local via the combined queue).
 static void run_pass(Ctx* c, int mode, float rho, const float* gimg, int a0, int na, long s0 = 0, long s1 = -1)
 {
+    c->stack_zero = false;  // states and (in MACE mode) the stack move
     PassParams P = base_params(c);
     P.mode = mode;
     P.rho = rho;
@@ -1038,6 +1040,7 @@ int mace_stack_init(void* p, const float* w0, int n_total)
     Ctx* c = C(p);
     if (w0) CK(cudaMemcpyAsync(c->W.p, w0, sizeof(float) * c->n * c->n_local, cudaMemcpyHostToDevice, c->stream));
     else CK(cudaMemsetAsync(c->W.p, 0, sizeof(float) * c->n * c->n_local, c->stream));
+    c->stack_zero = (w0 == nullptr);  // (every rank passes w0 or none: the same MaceConfig)
     CK(cudaMemsetAsync(c->done.p, 0, 2 * sizeof(int), c->stream));
     c->passes = 0;
     if (n_total > 0) consensus(c, (float)n_total, c->wbar.p, false);  // single rank: wbar = average(w)
@@ -1069,7 +1072,10 @@ int mace_states_from(void* p, int which)
     k_broadcast_state<<<c->num_sms * 4, 256, 0, c->stream>>>(c->d_agents.p, c->n_local, which ? c->g.p : c->wbar.p, c->n);
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(c->done.p, 0, 2 * sizeof(int), c->stream));
-    refresh(c, 0, c->n_local);
+    if (which == 0 && c->stack_zero)  // X0 = average(0) = 0 exactly: e = y - A 0 = y (icd.py:200) without the SpMV
+        CK(cudaMemcpyAsync(c->E.p, c->Y.p, sizeof(float) * c->total_rows, cudaMemcpyDeviceToDevice, c->stream));
+    else
+        refresh(c, 0, c->n_local);
     sync(c);
     API_END
 }
@@ -1088,6 +1094,7 @@ int mace_set_image(void* p, int which, const float* img)
 {
     API_BEGIN
     Ctx* c = C(p);
+    c->stack_zero = false;
     CK(cudaMemcpyAsync(which ? c->g.p : c->wbar.p, img, sizeof(float) * c->n * c->n_slices, cudaMemcpyHostToDevice,
                        c->stream));
     sync(c);

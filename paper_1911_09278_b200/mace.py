@@ -279,6 +279,16 @@ class _Comm:
         return out
 
 
+def _f64(a: np.ndarray) -> np.ndarray:
+    """float32 -> float64 result arrays (the reference returns float64) with torch's multi-threaded
+    CPU conversion: a 2M-element stack converts ~5x faster than ndarray.astype."""
+    if a.size < (1 << 16):
+        return a.astype(np.float64)
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).to(torch.float64).numpy()
+
+
 def _plan_stream(plan):
     """the plan's stream as a torch stream (GPU plans), None for host-side test backends"""
     ts = getattr(plan, "torch_stream", None)
@@ -449,8 +459,8 @@ def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=
     iterations = len(rows)
     converged = done[0] == 1
     _fill_log(log, rows, counter, N, n)
-    image = plan.get_image(1 if pnp else 0).astype(np.float64)
-    w_loc = plan.get_stack().reshape(len(local), n).astype(np.float64)
+    image = _f64(plan.get_image(1 if pnp else 0))
+    w_loc = _f64(plan.get_stack().reshape(len(local), n))
     if comm is None:
         stack = w_loc
     else:
@@ -554,8 +564,8 @@ def mace_solve_batch(problems, config: MaceConfig) -> list:
     if done[0] == 2:
         raise ConvergenceError(f"MACE diverged at iteration {done[1]} (reduce sigma)", last_iterate=None)
     iters = done[1] if done[0] == 1 else config.max_outer
-    images = plan.get_image(0).reshape(S, n).astype(np.float64)
-    stacks = plan.get_stack().reshape(S, N, n).astype(np.float64)
+    images = _f64(plan.get_image(0).reshape(S, n))
+    stacks = _f64(plan.get_stack().reshape(S, N, n))
     log = ConvergenceLog()
     counter = EquitCounter(n, N)
     _fill_log(log, [(lg[j, 0], None, wall * (j + 1) / max(iters, 1)) for j in range(iters)], counter, N, n)
