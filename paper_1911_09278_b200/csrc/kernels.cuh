@@ -69,7 +69,7 @@ struct PassParams {
     int n_items;
     unsigned* head;
     double* part;  // [n_items * 4]: sum alpha^2, sum (w'-w)^2, sum w'^2, sum w^2
-    int ng, wcap, view_cap;  // shared-memory band geometry (max over agents)
+    int ng, wcap;  // shared-memory band geometry (max over agents)
     const int* done;
     long s_begin, s_end;  // raster passes: pixel range [s_begin, s_end) (icd.py:222-246)
 };

@@ -110,7 +110,7 @@ struct Ctx {
     DBuf<float> wbar, g, ref, wsum;
     DBuf<double> refpart;
     double ref_norm2 = 0.0;
-    int sv_ng = 1, sv_wcap = 1, sv_K = 2, view_cap = 0;  // lane-per-view band geometry (max over agents)
+    int sv_ng = 1, sv_wcap = 1, sv_K = 2;  // lane-per-view band geometry (max over agents)
     size_t sv_smem = 0;
     int sv_grid = 0, sv_warps = 0;
     double sv_frac = 1.0 / 16.0;  // max fraction of an agent's tiles in flight
@@ -264,7 +264,6 @@ static PassParams base_params(Ctx* c)
     P.S = c->S;
     P.ng = c->sv_ng;
     P.wcap = c->sv_wcap;
-    P.view_cap = c->view_cap;
     P.head = c->head.p;
     P.part = c->part.p;
     P.done = c->done.p;
@@ -744,9 +743,6 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
         c->queue.alloc(q.size());
         CK(cudaMemcpy(c->queue.p, q.data(), sizeof(uint32_t) * q.size(), cudaMemcpyHostToDevice));
         c->n_items = (int)q.size();
-        int vmax = 0;
-        for (int a = 0; a < n_agents; ++a) vmax = std::max(vmax, (int)c->am[a]->views.size());
-        c->view_cap = (vmax + 1) & ~1;
         for (int a = 0; a < n_agents; ++a)
             if (c->am[a]->K != c->sv_K) throw std::runtime_error("agents with different (pixel, view) slot widths");
         c->sv_smem = (kSvThreads / 32) * sv_warp_bytes(c->S, c->sv_ng, c->sv_wcap);
