@@ -716,6 +716,100 @@ __global__ void k_finish(const double* sums5, double ref_norm2, double tol, int 
     *head = 0u;
 }
 
+// The tail of one single-context MACE iteration in one launch: the consensus average (K4 tree,
+// optionally the NRMSE partials against ref), the per-item norm partials of K2 folded per block, and
+// in the last block to finish a fixed-order fold of the block sums followed by the stop test and log
+// row (k_finish).  Same arithmetic order as k_consensus + k_norms + k_finish; gridDim <= 256.
+template <int NL>
+__global__ void __launch_bounds__(256) k_tail(const float* W, int n_local, size_t n, float scale, float* out,
+                                              const float* ref, const double* part, int n_items, double* scratch,
+                                              unsigned* counter, double* sums5, double ref_norm2, double tol,
+                                              int iter, double* log, int* done, unsigned* head, int n_groups)
+{
+    if (*done) return;
+    __shared__ double sh[5][256];
+    __shared__ bool last;
+    double a[5] = {0, 0, 0, 0, 0};
+    for (size_t gs = blockIdx.x * (size_t)blockDim.x + threadIdx.x; gs < n * n_groups;
+         gs += (size_t)gridDim.x * blockDim.x) {
+        const size_t grp = gs / n, s = gs % n;
+        const float* Wg = W + grp * n_local * n;
+        float v;
+        if constexpr (NL > 0) {
+            float acc[NL];
+#pragma unroll
+            for (int i = 0; i < NL; ++i) acc[i] = __ldcg(Wg + (size_t)i * n + s);
+            v = tree_sum<NL>(acc) / scale;
+        } else {
+            float acc[64];
+            for (int i = 0; i < n_local; ++i) acc[i] = Wg[(size_t)i * n + s];
+            int m = n_local;
+            while (m > 1) {
+                const int half = m / 2;
+                for (int i = 0; i < half; ++i) acc[i] += acc[half + i];
+                if (m % 2) {
+                    acc[half] = acc[2 * half];
+                    m = half + 1;
+                } else {
+                    m = half;
+                }
+            }
+            v = acc[0] / scale;
+        }
+        out[gs] = v;
+        if (ref && grp == 0) {
+            const double d = (double)v - (double)ref[s];
+            a[4] += d * d;
+        }
+    }
+    const int chunk = (n_items + gridDim.x - 1) / gridDim.x;
+    const int i0 = blockIdx.x * chunk, i1 = min(n_items, i0 + chunk);
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x)
+        for (int k = 0; k < 4; ++k) a[k] += part[(size_t)i * 4 + k];
+    for (int k = 0; k < 5; ++k) sh[k][threadIdx.x] = a[k];
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if ((int)threadIdx.x < o)
+            for (int k = 0; k < 5; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 5; ++k) scratch[5 * blockIdx.x + k] = sh[k][0];
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    for (int k = 0; k < 5; ++k)
+        sh[k][threadIdx.x] = (int)threadIdx.x < (int)gridDim.x ? __ldcg(scratch + 5 * threadIdx.x + k) : 0.0;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if ((int)threadIdx.x < o)
+            for (int k = 0; k < 5; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 5; ++k) sums5[k] = sh[k][0];
+        *counter = 0u;
+        const double dw2 = sh[1][0], wn2 = sh[2][0], wo2 = sh[3][0];
+        const double nn = sqrt(wn2);
+        const double rel = sqrt(dw2) / fmax(sqrt(wo2), 1e-300);
+        double* L = log + (size_t)iter * 4;
+        L[0] = rel;
+        L[1] = nn;
+        L[2] = sh[0][0];
+        L[3] = ref_norm2 > 0.0 ? sqrt(sh[4][0] / ref_norm2) : -1.0;
+        if (!isfinite(nn)) {
+            done[0] = 2;
+            done[1] = iter + 1;
+        } else if (rel < tol) {
+            done[0] = 1;
+            done[1] = iter + 1;
+        }
+        *head = 0u;
+    }
+}
+
 __global__ void k_reset_head(unsigned* head) { *head = 0u; }
 
 __global__ void k_fill(float* p, size_t n, float v)

@@ -473,7 +473,7 @@ int mace_ctx_create(int device, void** out)
     c->head.alloc(1);
     c->done.alloc(2);
     c->sums5.alloc(5);
-    c->norm_scratch.alloc(5 * kNormBlocks);
+    c->norm_scratch.alloc(5 * std::max(kNormBlocks, kRefBlocks));  // k_norms and k_tail block sums
     c->norm_counter.alloc(1);
     CK(cudaMemset(c->norm_counter.p, 0, sizeof(unsigned)));
     CK(cudaMemset(c->head.p, 0, sizeof(unsigned)));
@@ -1108,6 +1108,27 @@ int mace_get_stack(void* p, float* w)
 
 // Single-rank device loop: iters x [K2 pass of all agents -> K4 average/norms -> stop test];
 // use_g: v = 2 g - w with g set by the caller (PnP), else v = 2 wbar - w.  No host sync inside.
+// consensus + norms + stop test of one single-context iteration (k_tail: one launch)
+static void iteration_tail(Ctx* c, float scale, bool with_ref, double tol, int iter)
+{
+    const float* rf = with_ref ? c->ref.p : nullptr;
+    const double rn2 = with_ref ? c->ref_norm2 : 0.0;
+#define MACE_TAIL(NL_)                                                                                             \
+    k_tail<NL_><<<kRefBlocks, 256, 0, c->stream>>>(c->W.p, c->n_real, c->n, scale, c->wbar.p, rf, c->part.p,        \
+                                                   c->n_items, c->norm_scratch.p, c->norm_counter.p, c->sums5.p, rn2, \
+                                                   tol, iter, c->log.p, c->done.p, c->head.p, c->n_slices)
+    switch (c->n_real) {
+        case 1: MACE_TAIL(1); break;
+        case 2: MACE_TAIL(2); break;
+        case 4: MACE_TAIL(4); break;
+        case 8: MACE_TAIL(8); break;
+        case 16: MACE_TAIL(16); break;
+        default: MACE_TAIL(0);
+    }
+#undef MACE_TAIL
+    CK(cudaGetLastError());
+}
+
 // g = H(wbar) per slice with the K5 denoiser
 static void cnn_all_slices(Ctx* c)
 {
@@ -1129,12 +1150,7 @@ int mace_iterate(void* p, int iters, int iter0, double rho, int use_g, double to
     for (int k = 0; k < iters; ++k) {
         run_pass(c, 1, (float)rho, use_g ? c->g.p : c->wbar.p, 0, c->n_local);
         c->passes++;
-        consensus(c, (float)n_total, c->wbar.p, with_ref && !use_g);
-        k_norms<<<kNormBlocks, 256, 0, c->stream>>>(c->part.p, c->n_items,
-                                                    with_ref && !use_g ? c->refpart.p : nullptr, kRefBlocks,
-                                                    c->norm_scratch.p, c->sums5.p, c->norm_counter.p, c->done.p);
-        k_finish<<<1, 1, 0, c->stream>>>(c->sums5.p, with_ref && !use_g ? c->ref_norm2 : 0.0, tol, iter0 + k,
-                                         c->log.p, c->done.p, c->head.p);
+        iteration_tail(c, (float)n_total, with_ref && !use_g, tol, iter0 + k);
         if (c->passes % 50 == 0) refresh(c, 0, c->n_local);  // icd.py:29,280-282
         if (use_g == 2) cnn_all_slices(c);                    // g = H(wbar) on the device (mace.py:105-108)
         CK(cudaGetLastError());
