@@ -197,8 +197,8 @@ class AgentPlan(_Context):
             N.check(self.L.mace_host_alloc(2 * rows * 4, ctypes.byref(p)), "host_alloc")
             self._pin = p
             self._pin_arr = np.ctypeslib.as_array((ctypes.c_float * (2 * rows)).from_address(p.value))
-        np.copyto(self._pin_arr[:rows], np.asarray(y).reshape(-1), casting="same_kind")
-        np.copyto(self._pin_arr[rows:], np.asarray(weights).reshape(-1), casting="same_kind")
+        _convert_into(self._pin_arr[:rows], np.asarray(y).reshape(-1))
+        _convert_into(self._pin_arr[rows:], np.asarray(weights).reshape(-1))
         self.call("mace_load_data", ctypes.c_void_p(self._pin.value), ctypes.c_void_p(self._pin.value + rows * 4))
 
     def close(self):
@@ -350,6 +350,16 @@ class AgentPlan(_Context):
         out = np.empty(shape, np.float32)
         self.call("mace_get_stack", N.ptr(out))
         return out
+
+
+def _convert_into(dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[:] = src (float64 -> float32 into pinned staging) with torch's multi-threaded CPU copy."""
+    if src.size < (1 << 16) or src.dtype.kind != "f":
+        np.copyto(dst, src, casting="same_kind")
+        return
+    import torch
+
+    torch.from_numpy(dst).copy_(torch.from_numpy(np.ascontiguousarray(src)))
 
 
 class _DevArray:
