@@ -65,7 +65,9 @@ int mace_ctx_create(int device, void** ctx);
 void mace_ctx_destroy(void* ctx);
 int mace_ctx_stream(void* ctx, void** stream);
 int mace_sync(void* ctx);
-int mace_ctx_info(void* ctx, int64_t* info8);
+/* info10: nnz, queue items, raster NV, K2 shared bytes per warp, K2 warps of the last pass, SMs,
+ * passes, tile side, weighted records (0/1), reserved */
+int mace_ctx_info(void* ctx, int64_t* info10);
 int mace_agent_info(void* ctx, int local, int64_t* info8);
 
 /* global CSR over all (view, channel) rows: row_ptr[n_views*n_ch + 1], cols/vals[nnz] */
@@ -83,8 +85,12 @@ int mace_setup_agents(void* ctx, int n_agents, const int* view_counts, const int
 int mace_set_schedule(void* ctx, double concurrency, int64_t max_warps);
 /* local < 0: every local agent */
 int mace_set_agent_params(void* ctx, int local, double beta_eff, double inv_sigma2, int clamp);
-/* global sinogram y and weights, n_views x n_ch float32; recomputes theta2 */
+/* global sinogram y and weights, n_views x n_ch float32; recomputes theta2.  Single-slice
+ * super-voxel contexts with every weight > 0 switch K2 to weighted records (a sqrt(lambda),
+ * error sinogram kept as sqrt(lambda) e; mace_get_error still returns e); refresh e afterwards. */
 int mace_load_data(void* ctx, const float* y, const float* lam);
+/* allow (1, default) or forbid (0) weighted records from the next mace_load_data on */
+int mace_set_weighting(void* ctx, int allow);
 
 int mace_set_state(void* ctx, int local, const float* x);
 int mace_get_state(void* ctx, int local, float* x);

@@ -42,6 +42,7 @@ _SIGS = {
     "mace_set_schedule": (c_int, [P, c_double, c_int64]),
     "mace_set_agent_params": (c_int, [P, c_int, c_double, c_double, c_int]),
     "mace_load_data": (c_int, [P, P, P]),
+    "mace_set_weighting": (c_int, [P, c_int]),
     "mace_set_state": (c_int, [P, c_int, P]),
     "mace_get_state": (c_int, [P, c_int, P]),
     "mace_get_error": (c_int, [P, c_int, P]),

@@ -11,6 +11,10 @@
 //  * The band windows of the lane's views (the error-sinogram rows the tile touches) live in the
 //    lane's own shared-memory bank (planes e, lambda and a copy e0 of e): every gather and
 //    scatter is bank-conflict free and lane-private.
+//  * Weighted records (kW, single-slice contexts with lambda > 0): the slot records hold
+//    a sqrt(lambda) and the error sinogram is kept as sqrt(lambda) e, so theta1 = sum a lambda e
+//    is a plain dot product and the scatter keeps its form (e' -= alpha a'); the band loses its
+//    lambda plane (two planes, 2/3 of the shared memory) and each gather is one load.
 //  * Pixels are visited in batches of four pixels of one parity class (internal.h): they are
 //    never 8-neighbours, so the four prior terms are computed at once on lanes 8p..8p+7, and the
 //    data terms theta1_p = sum a_p lambda e are gathered against the band as it stood before the
@@ -23,7 +27,8 @@
 //  * Epilogue: the band's net change e - e0 is folded into global e with red.add (tiles of the
 //    same agent that share rows run concurrently), then z, the Mann step and norm partials.
 #pragma once
-#include "kernels.cuh"
+#include "dev_common.cuh"
+#include "k2_launch.h"
 
 namespace mace {
 
@@ -40,12 +45,6 @@ __device__ __forceinline__ void cp_async_wait()
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// shared-memory bytes per warp: the band (per row unit u = g W + o: e, lambda and e0 as three
-// 32-word lane vectors at word 96 u), the state tile with halo, and per-pixel v and w
-__host__ __device__ constexpr size_t sv_warp_bytes(int S, int ng, int wcap)
-{
-    return 12 * (size_t)ng * wcap * 32 + 4 * (size_t)((((S + 2) * (S + 2)) + 3) & ~3) + 8 * (size_t)S * S;
-}
 __host__ __device__ constexpr int sv_rec_words(int ng, int K) { return ng * 32 * K + 32; }
 
 __device__ __forceinline__ float fast_exp2(float x)
@@ -142,19 +141,23 @@ __device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __
 #ifndef MACE_K2_MINB
 #define MACE_K2_MINB 12  // resident warps per SM the register budget is sized for
 #endif
-template <int S, int K, int NG>
-__global__ void __launch_bounds__(32, MACE_K2_MINB) k_icd_sv(PassParams P)
+#ifndef MACE_K2_MINB_W
+#define MACE_K2_MINB_W 12  // weighted records (16 fits the shared memory but spills registers: slower)
+#endif
+template <int S, int K, int NG, bool kW>
+__global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_sv(PassParams P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     if (P.done && *P.done) return;
     constexpr int SS = S * S, S2 = S + 2, T2 = S2 * S2, T2p = (T2 + 3) & ~3;
     constexpr int H = S / 2, PER_CLASS = H * H, BPC = (PER_CLASS + 3) / 4, NB = 4 * BPC;
     constexpr int RECW = sv_rec_words(NG, K);
-    constexpr int U = 96;  // words per band row unit: e | lambda | e0
+    constexpr int U = sv_unit_words(kW);  // words per band row unit: e | lambda | e0 (kW: e | e0)
+    constexpr int E0 = U - 32;            // e0 plane offset
     const int lane = threadIdx.x & 31;
     const int W = P.wcap;
-    unsigned char* base = smem + (threadIdx.x >> 5) * sv_warp_bytes(S, NG, W);
-    float* sb = reinterpret_cast<float*>(base);  // band: e at U u + lane, lambda +32, e0 +64
+    unsigned char* base = smem + (threadIdx.x >> 5) * sv_warp_bytes(S, NG, W, kW);
+    float* sb = reinterpret_cast<float*>(base);  // band: e at U u + lane, lambda +32, e0 +E0
     float* zt = sb + NG * W * U;
     float* svv = zt + T2p;
     float* swo = svv + SS;
@@ -201,14 +204,43 @@ __global__ void __launch_bounds__(32, MACE_K2_MINB) k_icd_sv(PassParams P)
             for (int v = 0; v < EV; ++v) ev4[g][v] = v < nv ? __ldcg(ep + v) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
     };
+    // tile state (z with its halo, w, and v = 2 G(w) - w or the explicit target), one tile ahead:
+    // loaded after the previous tile's write-back, like the e windows
+    constexpr int ZN = (T2 + 31) / 32, VN = (SS + 31) / 32;
+    auto state_of = [&](uint32_t cd, float (&zp)[ZN], float (&wp)[VN], float (&vp)[VN]) {
+        const AgentDev& An = P.agents[cd >> kAgentShift];
+        const int svn = (int)(cd & kSvMask), nsn = An.n_sv_side;
+        const int rn = (svn / nsn) * S, cn = (svn % nsn) * S;
+        const float* zn = An.z;
+#pragma unroll
+        for (int k = 0; k < ZN; ++k) {
+            const int i = 32 * k + lane;
+            const int rr = rn - 1 + i / S2, cc = cn - 1 + i % S2;
+            zp[k] = (i < T2 && rr >= 0 && rr < n && cc >= 0 && cc < n) ? __ldcg(zn + (size_t)rr * n + cc) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < VN; ++k) {
+            const int i = 32 * k + lane;
+            const int rr = rn + i / S, cc = cn + i % S;
+            wp[k] = 0.f;
+            vp[k] = 0.f;
+            if (i < SS && rr < n && cc < n) {
+                const size_t s = (size_t)rr * n + cc;
+                wp[k] = __ldcg(An.w + s);
+                vp[k] = P.mode ? 2.f * __ldg(P.g + (size_t)An.slice * n * n + s) - wp[k] : __ldg(An.vt + s);
+            }
+        }
+    };
     unsigned item = fetch_item();
     if (item >= (unsigned)P.n_items) return;
     uint32_t code = __ldg(P.queue + item);
     int2 myb[NG];
     float4 ew[NG][EV];
     int sh[NG];
+    float zpre[ZN], wpre[VN], vpre[VN];
     band_of(code, myb);
     ewin_of(code, myb, ew, sh);
+    state_of(code, zpre, wpre, vpre);
 
     for (;;) {
         const AgentDev& A = P.agents[code >> kAgentShift];
@@ -229,42 +261,27 @@ __global__ void __launch_bounds__(32, MACE_K2_MINB) k_icd_sv(PassParams P)
         const uint32_t ncode = more ? __ldg(P.queue + nitem) : 0u;
 
         // -- 1. band: lambda rows by one coalesced copy, e rows from the prefetched windows
-        {  // lambda: pre-arranged per tile (k_sv_consts) as [u][32]; 16-byte copies into the units
+        if constexpr (!kW) {  // lambda: pre-arranged per tile (k_sv_consts) as [u][32]; 16-byte copies into the units
             const float* lsrc = A.lb + (size_t)sv * NG * W * 32;
             for (int c = lane; c < NG * W * 8; c += 32) cp_async16(sb + (c >> 3) * U + 32 + 4 * (c & 7), lsrc + 4 * c);
+            cp_async_commit();
         }
-        cp_async_commit();
         // -- 2. first batch of records
         SvBatch<K, NG> cur, nxt;
         load_batch<K, NG>(cur, recs, lane);
         // batch constants (theta2 x4 | c01 c02 c03 c12 | c13 c23 - -), 1 KB per tile: into L1 now,
         // read per batch as broadcast loads
         if (lane < NB / 2) asm volatile("prefetch.global.L1 [%0];" ::"l"(bcs + 32 * lane));
-        // -- 3. tile state + halo, w and v = 2 G(w) - w
+        // -- 3. tile state + halo, w and v = 2 G(w) - w (prefetched)
 #pragma unroll
-        for (int i0 = 0; i0 < T2p; i0 += 32) {
-            const int i = i0 + lane;
-            if (i < T2) {
-                const int rr = r0 - 1 + i / S2, cc = c0 - 1 + i % S2;
-                zt[i] = (rr >= 0 && rr < n && cc >= 0 && cc < n) ? __ldcg(z + (size_t)rr * n + cc) : 0.f;
-            }
-        }
+        for (int k = 0; k < ZN; ++k)
+            if (32 * k + lane < T2) zt[32 * k + lane] = zpre[k];
 #pragma unroll
-        for (int i0 = 0; i0 < SS; i0 += 32) {
-            const int i = i0 + lane;
-            if (i < SS) {
-                const int rr = r0 + i / S, cc = c0 + i % S;
-                if (rr < n && cc < n) {
-                    const size_t s = (size_t)rr * n + cc;
-                    const float wo = w[s];
-                    swo[i] = wo;
-                    svv[i] = P.mode ? 2.f * __ldg(P.g + (size_t)A.slice * n * n + s) - wo : A.vt[s];
-                } else {
-                    svv[i] = 0.f;
-                    swo[i] = 0.f;
-                }
+        for (int k = 0; k < VN; ++k)
+            if (32 * k + lane < SS) {
+                swo[32 * k + lane] = wpre[k];
+                svv[32 * k + lane] = vpre[k];
             }
-        }
 
         // -- 4. batches of four same-parity pixels
         float dsq = 0.f;
@@ -283,7 +300,7 @@ __global__ void __launch_bounds__(32, MACE_K2_MINB) k_icd_sv(PassParams P)
                             const float xi = i == 0 ? ew[g][v].x : i == 1 ? ew[g][v].y : i == 2 ? ew[g][v].z : ew[g][v].w;
                             const float x = o < cnt ? xi : 0.f;
                             d[o * U] = x;
-                            d[o * U + 64] = x;
+                            d[o * U + E0] = x;
                         }
                     }
                 }
@@ -291,11 +308,11 @@ __global__ void __launch_bounds__(32, MACE_K2_MINB) k_icd_sv(PassParams P)
                 for (int o = 0; o < W; ++o) {
                     const float x = o < cnt ? __ldcg(eg + myb[g].x + o) : 0.f;
                     d[o * U] = x;
-                    d[o * U + 64] = x;
+                    d[o * U + E0] = x;
                 }
             }
         }
-        cp_async_wait<0>();  // this lane's lambda copies have landed
+        if constexpr (!kW) cp_async_wait<0>();  // this lane's lambda copies have landed
         __syncwarp();        // ... and every other lane's; band / zt / v / w stores visible
         auto step = [&](const int b, const SvBatch<K, NG>& C, SvBatch<K, NG>& Nx) {
             if (b + 1 < NB) load_batch<K, NG>(Nx, recs + (size_t)(b + 1) * 4 * RECW, lane);
@@ -330,10 +347,12 @@ __global__ void __launch_bounds__(32, MACE_K2_MINB) k_icd_sv(PassParams P)
                 for (int g = 0; g < NG; ++g)
 #pragma unroll
                     for (int q = 0; q < K; ++q) {
-                        const float ee = sb[ab[p][g] + q * U], ll = sb[ab[p][g] + q * U + 32];
+                        const float ee = sb[ab[p][g] + q * U];
                         if (p == 0) e0v[g][q] = ee;
-                        if (q & 1) a1 = fmaf(av[p][g][q] * ll, ee, a1);
-                        else a0 = fmaf(av[p][g][q] * ll, ee, a0);
+                        // kW: a' = a sqrt(lambda) against e' = sqrt(lambda) e
+                        const float al = kW ? av[p][g][q] : av[p][g][q] * sb[ab[p][g] + q * U + 32];
+                        if (q & 1) a1 = fmaf(al, ee, a1);
+                        else a0 = fmaf(al, ee, a0);
                     }
                 num[p] = a0 + a1;
             }
@@ -360,17 +379,26 @@ __global__ void __launch_bounds__(32, MACE_K2_MINB) k_icd_sv(PassParams P)
                         qg_term<false>(d, wk, PR, g, c);
                     }
                 }
-#pragma unroll
-                for (int p = 0; p < 4; ++p)
-                    if (pp == p) num[p] -= beta * g;
                 den_l = beta * c;
+                // theta1 of the four pixels by a splitting butterfly: after the xor-16 and xor-8
+                // stages lanes 8p..8p+7 hold partial sums of pixel p = lane >> 3 only (the pixel
+                // whose prior neighbour they own), which the xor-4/2/1 stages finish with the
+                // prior gradient folded in: 6 shuffles instead of 20
+                const bool h16 = lane & 16, h8 = lane & 8;
+                float k0 = h16 ? num[2] : num[0], k1 = h16 ? num[3] : num[1];
+                k0 += __shfl_xor_sync(FULL, h16 ? num[0] : num[2], 16);
+                k1 += __shfl_xor_sync(FULL, h16 ? num[1] : num[3], 16);
+                float kp = h8 ? k1 : k0;
+                kp += __shfl_xor_sync(FULL, h8 ? k0 : k1, 8);
+                kp -= beta * g;
+#pragma unroll
+                for (int o = 4; o; o >>= 1) {
+                    kp += __shfl_xor_sync(FULL, kp, o);
+                    den_l += __shfl_xor_sync(FULL, den_l, o);
+                }
+#pragma unroll
+                for (int p = 0; p < 4; ++p) num[p] = __shfl_sync(FULL, kp, 8 * p);
             }
-#pragma unroll
-            for (int o = 16; o; o >>= 1)
-#pragma unroll
-                for (int p = 0; p < 4; ++p) num[p] += __shfl_xor_sync(FULL, num[p], o);
-#pragma unroll
-            for (int o = 4; o; o >>= 1) den_l += __shfl_xor_sync(FULL, den_l, o);
             // the four 1-D solves (icd.py:128-134): everything but the coupling to earlier pixels of
             // the batch is independent across p; the reference skips pixels with den <= 0
             float nm[4], rd[4], zs[4];
@@ -449,7 +477,7 @@ __global__ void __launch_bounds__(32, MACE_K2_MINB) k_icd_sv(PassParams P)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int o = 4 * v + i - s0;
-                    dv[i] = (o >= 0 && o < cnt) ? d[o * U] - d[o * U + 64] : 0.f;
+                    dv[i] = (o >= 0 && o < cnt) ? d[o * U] - d[o * U + E0] : 0.f;
                 }
                 if (dv[0] != 0.f || dv[1] != 0.f || dv[2] != 0.f || dv[3] != 0.f)
                     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(ep + 4 * v), "f"(dv[0]),
@@ -494,6 +522,7 @@ __global__ void __launch_bounds__(32, MACE_K2_MINB) k_icd_sv(PassParams P)
         code = ncode;
         band_of(code, myb);
         ewin_of(code, myb, ew, sh);
+        state_of(code, zpre, wpre, vpre);
     }
 }
 

@@ -10,156 +10,11 @@
 //   K4  k_consensus / k_norms /   average (mace.py:71-90), relnorm and divergence test
 //       k_finish                  (mace.py:309-318), log row
 #pragma once
-#include <cuda_runtime.h>
-#include <stdint.h>
+#include "dev_common.cuh"
 
 namespace mace {
 
-constexpr unsigned FULL = 0xffffffffu;
-// work-queue item = (local agent << kAgentShift) | super-voxel index (layout.cpp build_queue)
-constexpr int kAgentShift = 22;
-constexpr uint32_t kSvMask = (1u << kAgentShift) - 1;
-
-struct PriorC {
-    int kind;  // 0 quadratic-mrf, 1 qggmrf  (models.py:43-44)
-    int p_is_2;
-    float eps2;      // 2 * eps_reg
-    float inv_Tsx;   // 1 / (T sigma_x)
-    float inv_sxp;   // sigma_x^-p
-    float qp;        // q / p
-    float qmp;       // q - p
-    float pm1, pm2;  // p - 1, p - 2
-    float floor_;    // 1e-9 T sigma_x
-    float inv_sx2;   // 1 / sigma_x^2
-    double p, q, T, sx, eps;  // double copies for the cost kernels
-};
-
-struct AgentDev {
-    float* e;          // [R] error sinogram y_i - A_i X_i (icd.py:200)
-    float* lam;        // [R] weights lambda
-    float* y;          // [R]
-    float* z;          // [n] agent state X_i
-    float* w;          // [n] stack component w_i
-    float* th;         // [n] theta2 data term, sum a^2 lambda (icd.py:193-195)
-    float* vt;         // [n] explicit proximal target (plain passes)
-    int slice;         // slice of a multi-slice batch (config 4); consensus images are [slice][n]
-    const int* views;  // [V] global view index of local view j
-    // super-voxel layout
-    const int2* band;      // [n_sv * V] {local row start, window rows}
-    const uint32_t* rec;   // [n_sv][nb][4][rec_words] slot records (layout.cpp, lane-per-view)
-    float* bc;             // [n_sv][nb][16] batch constants: theta2 x4, cross terms x6 (per local agent)
-    float* lb;             // [n_sv][ng][wcap][32] band lambda in shared-memory order (per local agent)
-    int ng, rec_words;     // view groups ceil(V / 32); words per slot record
-    // raster layout
-    const int2* rpix;   // [n]
-    const uint32_t* ridx;
-    const float* rval;
-    int R, V, n_sv_side;
-    float beta_eff, inv_s2;
-    int clamp;
-};
-
-struct PassParams {
-    const AgentDev* agents;
-    PriorC pr;
-    int n_side, S, mode;  // mode 0: v from vt; 1: MACE (v = 2 g - w, Mann epilogue)
-    const float* g;       // consensus image G(w) or G_H(w)
-    float rho;
-    const uint32_t* queue;
-    int n_items;
-    unsigned* head;
-    double* part;  // [n_items * 4]: sum alpha^2, sum (w'-w)^2, sum w'^2, sum w^2
-    int ng, wcap;  // shared-memory band geometry (max over agents)
-    const int* done;
-    long s_begin, s_end;  // raster passes: pixel range [s_begin, s_end) (icd.py:222-246)
-};
-
-__constant__ int c_dr[8] = {-1, -1, -1, 0, 0, 1, 1, 1};  // models.py:50
-__constant__ int c_dc[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
-__constant__ float c_nw[8];  // raw weight / (4 + 2 sqrt 2), models.py:51-52,107
-
-// ---- qGGMRF potential derivatives in fp32 (icd.py:45-64)
-__device__ __forceinline__ float pow_pos(float x, float e) { return exp2f(e * log2f(x)); }
-
-__device__ __forceinline__ float qg_influence(float d, const PriorC& P)
-{
-    const float ad = fabsf(d);
-    if (ad == 0.0f) return 0.0f;
-    const float um = pow_pos(ad * P.inv_Tsx, P.qmp);
-    const float base = P.p_is_2 ? ad : pow_pos(ad, P.pm1);
-    const float opu = 1.0f + um;
-    const float val = (base * P.inv_sxp) * um * (P.qp + um) / (opu * opu);
-    return d > 0.0f ? val : -val;
-}
-
-__device__ __forceinline__ float qg_coef(float d, const PriorC& P)
-{
-    float ad = fabsf(d);
-    if (ad <= P.floor_) {
-        if (P.p_is_2) return P.inv_sx2;
-        ad = P.floor_;
-    }
-    const float um = pow_pos(ad * P.inv_Tsx, P.qmp);
-    const float base = P.p_is_2 ? 1.0f : pow_pos(ad, P.pm2);
-    const float opu = 1.0f + um;
-    return (base * P.inv_sxp) * um * (P.qp + um) / (opu * opu);
-}
-
-__device__ __forceinline__ float warp_sum(float v)
-{
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
-}
-__device__ __forceinline__ double warp_sum_d(double v)
-{
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
-}
-
-// Neighbour term of one lane (lanes 0..7 own neighbour k = lane; models.py:50-52 order).
-__device__ __forceinline__ void prior_lane(int lane, float zs, float zr, bool valid, const PriorC& P,
-                                           float& g, float& c)
-{
-    g = 0.f;
-    c = 0.f;
-    if (lane < 8 && valid) {
-        const float wk = c_nw[lane];
-        if (P.kind == 0) {
-            g = wk * (zs - zr);
-            c = wk;
-        } else {
-            const float d = zs - zr;
-            g = wk * qg_influence(d, P);
-            c = wk * qg_coef(d, P);
-        }
-    }
-}
-
-// 1-D surrogate solve (icd.py:128-134); returns false where the reference `continue`s.
-__device__ __forceinline__ bool pixel_step(float t, float g, float c, float zs, float v, float th, float beta,
-                                           float inv_s2, int clamp, const PriorC& P, float& alpha)
-{
-    float gp = 0.f, cp = 0.f;
-    if (beta > 0.f) {
-        if (P.kind == 0) {
-            gp = beta * (g + P.eps2 * zs);
-            cp = beta * (c + P.eps2);
-        } else {
-            gp = beta * g;
-            cp = beta * c;
-        }
-    }
-    const float num = t - gp - inv_s2 * (zs - v);
-    const float den = th + cp + inv_s2;
-    if (!(den > 0.f)) return false;
-    alpha = num / den;
-    if (clamp && zs + alpha < 0.f) alpha = -zs;
-    return true;
-}
-
-// K2 super-voxel pass: see k_sv.cuh.
+// K2 super-voxel pass: see k_sv.cuh (compiled per tile side in k2_inst.cu).
 
 // ===========================================================================
 // K2 raster pass: the reference's exact visiting order (pixels 0..n-1), one
@@ -330,7 +185,7 @@ __global__ void k_fp_agents(FPParams F, const AgentDev* agents, const int* row_b
         const int j = r / F.n_ch, ch = r % F.n_ch;
         const int64_t g = (int64_t)A.views[j] * F.n_ch + ch;
         const float acc = row_dot(F, F.rp[g], F.rp[g + 1], A.z, lane);
-        if (lane == 0) A.e[r] = A.y[r] - acc;
+        if (lane == 0) A.e[r] = A.sq ? A.sq[r] * (A.y[r] - acc) : A.y[r] - acc;
     }
 }
 
@@ -483,7 +338,7 @@ __global__ void k_theta2_raster(const AgentDev* agents, int n_agents, int n)
 // theta2_p = sum a_p^2 lambda (icd.py:193-195) for the kSvBatch slots of each batch, and the
 // cross terms c_ij = sum_r a_ir a_jr lambda_r that couple two pixels of a batch through shared
 // rows (k_sv.cuh).  Depends on lambda only, so it is recomputed per data load.
-template <int K, int NG>
+template <int K, int NG, bool kW>
 __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n_items, const uint32_t* queue,
                                                    int n_side, int S, int nb, int W)
 {
@@ -504,12 +359,13 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
         const int j = 32 * g + lane;
         const int2 bj = j < A.V ? bt[j] : make_int2(0, 0);
         start[g] = bj.x;
-        if (b == 0) {  // the band's lambda rows, laid out as the kernel's shared-memory plane
+        if (!kW && b == 0) {  // the band's lambda rows, laid out as the kernel's shared-memory plane
             float* lb = A.lb + (((size_t)sv * NG + g) * W) * 32 + lane;
             for (int o = 0; o < W; ++o) lb[o * 32] = o < bj.y ? A.lam[bj.x + o] : 0.f;
         }
     }
-    const uint32_t* rb = A.rec + ((size_t)sv * nb + b) * 4 * recw;
+    const uint32_t* rb = A.rec0 + ((size_t)sv * nb + b) * 4 * recw;
+    uint32_t* wb = kW ? A.recw + ((size_t)sv * nb + b) * 4 * recw : nullptr;
     float t2[4] = {0.f, 0.f, 0.f, 0.f}, cx[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
@@ -518,11 +374,18 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
             const uint32_t* r = rb + (size_t)p * recw;
-            o[p] = (int)((r[NG * 32 * K + lane] >> (8 * g)) & 0xffu);
+            const uint32_t ow = r[NG * 32 * K + lane];
+            o[p] = (int)((ow >> (8 * g)) & 0xffu);
+            if (kW && g == 0) wb[(size_t)p * recw + NG * 32 * K + lane] = ow;
 #pragma unroll
             for (int q = 0; q < K; ++q) {
                 a[p][q] = __uint_as_float(r[(g * 32 + lane) * K + q]);
                 l[p][q] = a[p][q] != 0.f ? A.lam[start[g] + o[p] + q] : 0.f;
+                if (kW) {  // weighted record a sqrt(lambda): theta2 and the cross terms are its plain products
+                    a[p][q] *= sqrtf(l[p][q]);
+                    l[p][q] = 1.f;
+                    wb[(size_t)p * recw + (g * 32 + lane) * K + q] = __float_as_uint(a[p][q]);
+                }
                 t2[p] = fmaf(a[p][q] * a[p][q], l[p][q], t2[p]);
             }
         }
@@ -567,6 +430,7 @@ __global__ void k_gather_data(const AgentDev* agents, const int* row_base, int n
         const int64_t g = (int64_t)A.slice * slice_rows + (int64_t)A.views[r / n_ch] * n_ch + r % n_ch;
         A.y[r] = y[g];
         A.lam[r] = lam[g];
+        if (A.sq) A.sq[r] = sqrtf(lam[g]);
     }
 }
 
@@ -815,6 +679,13 @@ __global__ void k_reset_head(unsigned* head) { *head = 0u; }
 __global__ void k_fill(float* p, size_t n, float v)
 {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// out = a * b elementwise (weighted error sinogram of a zero state: sqrt(lambda) y)
+__global__ void k_mul(float* out, const float* a, const float* b, size_t n)
+{
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = a[i] * b[i];
 }
 
 // X_i = x[slice(i)] for every local (virtual) agent; x is [slice][n]

@@ -20,7 +20,7 @@
 
 #include "internal.h"
 #include "kernels.cuh"
-#include "k_sv.cuh"
+#include "k2_launch.h"
 #include "k_sweep64.cuh"
 #include "k_peer.cuh"
 #include "cnn.cuh"
@@ -67,6 +67,7 @@ struct AgentMem {
     DBuf<int2> band, rpix;
     DBuf<float> rval;
     DBuf<uint32_t> rec, ridx;
+    DBuf<uint32_t> recw;  // weighted records a sqrt(lambda) (k_sv_consts; single-slice contexts)
     int R = 0, n_sv_side = 0, n_sv = 0, max_col = 0;
     int wcap = 0, ng = 1, K = 2, nb = 0, rec_words = 0;  // lane-per-view layout geometry
     int64_t entries = 0, nnz = 0, duplicates = 0;
@@ -111,6 +112,9 @@ struct Ctx {
     DBuf<double> refpart;
     double ref_norm2 = 0.0;
     int sv_ng = 1, sv_wcap = 1, sv_K = 2;  // lane-per-view band geometry (max over agents)
+    bool weighted = false;                  // K2 on weighted records: e kept as sqrt(lambda) e (k_sv.cuh)
+    bool allow_weighted = true;             // mace_set_weighting
+    DBuf<float> SQ;                         // sqrt(lambda) per local agent row (weighted mode)
     size_t sv_smem = 0;
     int sv_grid = 0, sv_warps = 0;
     double sv_frac = 1.0 / 16.0;  // max fraction of an agent's tiles in flight
@@ -164,64 +168,9 @@ static void k2_end(Ctx* c, cudaEvent_t second)
 static const int kRefBlocks = 256;
 static const int kNormBlocks = 64;
 
-static void upload_prior_consts()
-{
-    const double raw[8] = {1 / std::sqrt(2.0), 1.0, 1 / std::sqrt(2.0), 1.0, 1.0, 1 / std::sqrt(2.0), 1.0,
-                           1 / std::sqrt(2.0)};
-    const double norm = 4.0 + 2.0 * std::sqrt(2.0);
-    float w[8];
-    for (int k = 0; k < 8; ++k) w[k] = (float)(raw[k] / norm);
-    CK(cudaMemcpyToSymbol(c_nw, w, sizeof(w)));
-}
-
 static void sync(Ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
 
 // ------------------------------------------------------------------ K2 launch helpers
-constexpr int kSvThreads = 32;
-
-template <int S, int K, int NG>
-static void launch_sv(Ctx* c, const PassParams& P, int items, int agents_in_queue)
-{
-    auto kern = k_icd_sv<S, K, NG>;
-    // occupancy of this instantiation at this shared-memory size, queried once per (device, size);
-    // the kernel's dynamic shared-memory limit only ever grows (per device)
-    static thread_local std::vector<std::pair<std::pair<int, size_t>, int>> occ;
-    static thread_local std::vector<std::pair<int, size_t>> limit;
-    size_t* lim = nullptr;
-    for (auto& e : limit)
-        if (e.first == c->device) lim = &e.second;
-    if (!lim) {
-        limit.push_back({c->device, 0});
-        lim = &limit.back().second;
-    }
-    if (c->sv_smem > *lim) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sv_smem));
-        *lim = c->sv_smem;
-    }
-    int nb = -1;
-    for (auto& e : occ)
-        if (e.first.first == c->device && e.first.second == c->sv_smem) nb = e.second;
-    if (nb < 0) {
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSvThreads, c->sv_smem));
-        occ.push_back({{c->device, c->sv_smem}, nb});
-    }
-    if (nb < 1) throw std::runtime_error("super-voxel kernel does not fit on an SM (band too large)");
-    // Concurrency bound: at most a fraction `sv_frac` of an agent's tiles are in flight at once
-    // (bounded staleness), never fewer than one tile per agent, never more than
-    // the resident warps of the whole GPU.
-    constexpr int wpb = kSvThreads / 32;
-    long warps = (long)nb * wpb * c->num_sms;
-    long cap = (long)std::floor(c->sv_frac * (double)items);
-    cap = std::max<long>(cap, agents_in_queue);
-    if (c->sv_max_warps > 0) cap = std::min<long>(cap, c->sv_max_warps);
-    warps = std::max(1L, std::min(warps, cap));
-    const int threads = warps >= wpb ? kSvThreads : (int)warps * 32;
-    const long grid = warps >= wpb ? warps / wpb : 1;
-    c->sv_grid = (int)grid;
-    c->sv_warps = (int)(grid * threads / 32);
-    kern<<<(int)grid, threads, c->sv_smem, c->stream>>>(P);
-    CK(cudaGetLastError());
-}
 
 template <int NV>
 static void launch_raster(Ctx* c, const PassParams& P, int n_agents, int agent_base)
@@ -230,29 +179,31 @@ static void launch_raster(Ctx* c, const PassParams& P, int n_agents, int agent_b
     CK(cudaGetLastError());
 }
 
-template <int K, int NG>
+// one super-voxel pass over P.queue (k2_inst.cu, one unit per tile side)
 static void dispatch_sv(Ctx* c, const PassParams& P, int na)
 {
+    SvLaunch L;
+    L.device = c->device;
+    L.stream = c->stream;
+    L.smem = c->sv_smem;
+    L.num_sms = c->num_sms;
+    L.frac = c->sv_frac;
+    L.max_warps = c->sv_max_warps;
+    L.agents_in_queue = na;
+    L.K = c->sv_K;
+    L.NG = c->sv_ng;
+    L.weighted = c->weighted;
     switch (c->S) {
-        case 2: launch_sv<2, K, NG>(c, P, P.n_items, na); break;
-        case 4: launch_sv<4, K, NG>(c, P, P.n_items, na); break;
-        case 6: launch_sv<6, K, NG>(c, P, P.n_items, na); break;
-        case 8: launch_sv<8, K, NG>(c, P, P.n_items, na); break;
-        case 12: launch_sv<12, K, NG>(c, P, P.n_items, na); break;
-        case 16: launch_sv<16, K, NG>(c, P, P.n_items, na); break;
+        case 2: sv_launch_s2(L, P); break;
+        case 4: sv_launch_s4(L, P); break;
+        case 6: sv_launch_s6(L, P); break;
+        case 8: sv_launch_s8(L, P); break;
+        case 12: sv_launch_s12(L, P); break;
+        case 16: sv_launch_s16(L, P); break;
         default: throw std::runtime_error("super-voxel side must be one of 2, 4, 6, 8, 12, 16");
     }
-}
-
-template <int K>
-static void dispatch_sv_ng(Ctx* c, const PassParams& P, int na)
-{
-    switch (c->sv_ng) {
-        case 1: dispatch_sv<K, 1>(c, P, na); break;
-        case 2: dispatch_sv<K, 2>(c, P, na); break;
-        case 3: dispatch_sv<K, 3>(c, P, na); break;
-        default: dispatch_sv<K, 4>(c, P, na); break;
-    }
+    c->sv_grid = L.grid;
+    c->sv_warps = L.warps;
 }
 
 static PassParams base_params(Ctx* c)
@@ -304,8 +255,7 @@ static void run_pass(Ctx* c, int mode, float rho, const float* gimg, int a0, int
         P.queue = c->am[a0]->queue.p;
         P.n_items = c->am[a0]->n_sv;
     }
-    if (c->sv_K <= 2) dispatch_sv_ng<2>(c, P, na);
-    else dispatch_sv_ng<4>(c, P, na);
+    dispatch_sv(c, P, na);
     k2_end(c, ev);
 }
 
@@ -339,16 +289,24 @@ static void compute_theta2(Ctx* c)
             kern<<<(unsigned)blocks, 128, 0, c->stream>>>(c->d_agents.p, c->n_items, c->queue.p, c->n_side, c->S, nb,
                                                           c->sv_wcap);
         };
-        const int key = c->sv_K * 10 + c->sv_ng;
+        const int key = c->sv_K * 10 + c->sv_ng + (c->weighted ? 100 : 0);
         switch (key) {
-            case 21: go(k_sv_consts<2, 1>); break;
-            case 22: go(k_sv_consts<2, 2>); break;
-            case 23: go(k_sv_consts<2, 3>); break;
-            case 24: go(k_sv_consts<2, 4>); break;
-            case 41: go(k_sv_consts<4, 1>); break;
-            case 42: go(k_sv_consts<4, 2>); break;
-            case 43: go(k_sv_consts<4, 3>); break;
-            default: go(k_sv_consts<4, 4>); break;
+            case 21: go(k_sv_consts<2, 1, false>); break;
+            case 22: go(k_sv_consts<2, 2, false>); break;
+            case 23: go(k_sv_consts<2, 3, false>); break;
+            case 24: go(k_sv_consts<2, 4, false>); break;
+            case 41: go(k_sv_consts<4, 1, false>); break;
+            case 42: go(k_sv_consts<4, 2, false>); break;
+            case 43: go(k_sv_consts<4, 3, false>); break;
+            case 44: go(k_sv_consts<4, 4, false>); break;
+            case 121: go(k_sv_consts<2, 1, true>); break;
+            case 122: go(k_sv_consts<2, 2, true>); break;
+            case 123: go(k_sv_consts<2, 3, true>); break;
+            case 124: go(k_sv_consts<2, 4, true>); break;
+            case 141: go(k_sv_consts<4, 1, true>); break;
+            case 142: go(k_sv_consts<4, 2, true>); break;
+            case 143: go(k_sv_consts<4, 3, true>); break;
+            default: go(k_sv_consts<4, 4, true>); break;
         }
     }
     CK(cudaGetLastError());
@@ -371,6 +329,38 @@ static void consensus(Ctx* c, float scale, float* out, bool with_ref)
                                                           c->n_slices);
     }
     CK(cudaGetLastError());
+}
+
+// Switch K2 between plain records (lambda plane in shared memory) and weighted records
+// a sqrt(lambda) with the error sinogram kept as sqrt(lambda) e (k_sv.cuh).  Called when data
+// are loaded; the caller refreshes e afterwards (mace_set_state / mace_states_from).
+static void set_weighted(Ctx* c, bool on)
+{
+    if (on && !c->SQ.p) {
+        c->SQ.alloc(c->total_rows);
+        CK(cudaMemset(c->SQ.p, 0, sizeof(float) * c->total_rows));
+    }
+    for (int a = 0; a < c->n_real && on; ++a) {
+        AgentMem& m = *c->am[a];
+        if (!m.recw.p) m.recw.alloc(m.rec.n);
+    }
+    const bool changed = on != c->weighted;
+    c->weighted = on;
+    std::vector<int> rb(c->n_local + 1, 0);
+    CK(cudaMemcpy(rb.data(), c->row_base.p, sizeof(int) * (c->n_local + 1), cudaMemcpyDeviceToHost));
+    for (int va = 0; va < c->n_local; ++va) {
+        AgentMem& m = *c->am[va % c->n_real];
+        AgentDev& A = c->h_agents[va];
+        A.rec0 = m.rec.p;
+        A.recw = on ? m.recw.p : nullptr;
+        A.rec = on ? m.recw.p : m.rec.p;
+        A.sq = on ? c->SQ.p + rb[va] : nullptr;
+    }
+    c->sv_smem = (kSvThreads / 32) * sv_warp_bytes(c->S, c->sv_ng, c->sv_wcap, on);
+    if (c->sv_smem > 227 * 1024) throw std::runtime_error("super-voxel band does not fit in shared memory");
+    CK(cudaMemcpyAsync(c->d_agents.p, c->h_agents.data(), sizeof(AgentDev) * c->n_local, cudaMemcpyHostToDevice,
+                       c->stream));
+    if (changed) sync(c);
 }
 
 static void ensure_log(Ctx* c, int n)
@@ -478,7 +468,6 @@ int mace_ctx_create(int device, void** out)
     CK(cudaMemset(c->norm_counter.p, 0, sizeof(unsigned)));
     CK(cudaMemset(c->head.p, 0, sizeof(unsigned)));
     CK(cudaMemset(c->done.p, 0, 2 * sizeof(int)));
-    upload_prior_consts();
     *out = c.release();
     API_END
 }
@@ -578,6 +567,8 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
     c->schedule = schedule;
     c->S = schedule == 0 ? svs : c->n_side;
     c->am.clear();
+    c->SQ.free();
+    c->weighted = false;
     int off = 0;
     for (int a = 0; a < n_agents; ++a) {
         auto m = std::make_unique<AgentMem>();
@@ -725,6 +716,9 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
         A.rval = m.rval.p;
         A.band = m.band.p;
         A.rec = m.rec.p;
+        A.rec0 = m.rec.p;
+        A.recw = nullptr;
+        A.sq = nullptr;
         A.bc = schedule == 0 ? c->BC.p + bcb[va] : nullptr;
         A.lb = schedule == 0 ? c->LB.p + lbb[va] : nullptr;
         A.ng = m.ng;
@@ -745,7 +739,8 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
         c->n_items = (int)q.size();
         for (int a = 0; a < n_agents; ++a)
             if (c->am[a]->K != c->sv_K) throw std::runtime_error("agents with different (pixel, view) slot widths");
-        c->sv_smem = (kSvThreads / 32) * sv_warp_bytes(c->S, c->sv_ng, c->sv_wcap);
+        c->weighted = false;
+        c->sv_smem = (kSvThreads / 32) * sv_warp_bytes(c->S, c->sv_ng, c->sv_wcap, false);
         if (c->sv_smem > 227 * 1024) throw std::runtime_error("super-voxel band does not fit in shared memory");
     } else {
         c->n_items = n_local;
@@ -778,7 +773,7 @@ int mace_agent_info(void* p, int local, int64_t* info /* [8] */)
     API_END
 }
 
-int mace_ctx_info(void* p, int64_t* info /* [8] */)
+int mace_ctx_info(void* p, int64_t* info /* [10] */)
 {
     API_BEGIN
     Ctx* c = C(p);
@@ -790,6 +785,8 @@ int mace_ctx_info(void* p, int64_t* info /* [8] */)
     info[5] = c->num_sms;
     info[6] = c->passes;
     info[7] = c->S;
+    info[8] = c->weighted ? 1 : 0;
+    info[9] = 0;
     API_END
 }
 
@@ -824,6 +821,13 @@ int mace_set_agent_params(void* p, int local, double beta_eff, double inv_sigma2
     API_END
 }
 
+int mace_set_weighting(void* p, int allow)
+{
+    API_BEGIN
+    C(p)->allow_weighted = allow != 0;
+    API_END
+}
+
 int mace_load_data(void* p, const float* y, const float* lam)
 {
     API_BEGIN
@@ -838,6 +842,11 @@ int mace_load_data(void* p, const float* y, const float* lam)
     CK(cudaMemcpyAsync(c->y.p, y, sizeof(float) * total, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->lam.p, lam, sizeof(float) * total, cudaMemcpyHostToDevice, c->stream));
     if (c->n_local) {
+        // weighted records need one lambda per record (a single slice) and lambda > 0 everywhere,
+        // so that e = e' / sqrt(lambda) stays recoverable (mace_get_error)
+        bool pos = true;
+        for (size_t i = 0; i < total && pos; ++i) pos = lam[i] > 0.f;
+        set_weighted(c, c->allow_weighted && c->schedule == 0 && c->n_slices == 1 && pos);
         k_gather_data<<<c->num_sms * 4, 256, 0, c->stream>>>(c->d_agents.p, c->row_base.p, c->n_local, c->total_rows,
                                                               c->n_ch, c->y.p, c->lam.p, (int64_t)rows);
         CK(cudaGetLastError());
@@ -874,7 +883,13 @@ int mace_get_error(void* p, int local, float* e)
     Ctx* c = C(p);
     const AgentDev& A = c->h_agents.at(local);
     CK(cudaMemcpyAsync(e, A.e, sizeof(float) * A.R, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<float> sq;
+    if (A.sq) {
+        sq.resize(A.R);
+        CK(cudaMemcpyAsync(sq.data(), A.sq, sizeof(float) * A.R, cudaMemcpyDeviceToHost, c->stream));
+    }
     sync(c);
+    for (size_t r = 0; r < sq.size(); ++r) e[r] /= sq[r];  // weighted mode: e = e' / sqrt(lambda)
     API_END
 }
 
@@ -1068,9 +1083,14 @@ int mace_states_from(void* p, int which)
     k_broadcast_state<<<c->num_sms * 4, 256, 0, c->stream>>>(c->d_agents.p, c->n_local, which ? c->g.p : c->wbar.p, c->n);
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(c->done.p, 0, 2 * sizeof(int), c->stream));
-    if (which == 0 && c->stack_zero)  // X0 = average(0) = 0 exactly: e = y - A 0 = y (icd.py:200) without the SpMV
-        CK(cudaMemcpyAsync(c->E.p, c->Y.p, sizeof(float) * c->total_rows, cudaMemcpyDeviceToDevice, c->stream));
-    else
+    if (which == 0 && c->stack_zero) {  // X0 = average(0) = 0 exactly: e = y - A 0 = y (icd.py:200) without the SpMV
+        if (c->weighted) {
+            k_mul<<<c->num_sms * 4, 256, 0, c->stream>>>(c->E.p, c->Y.p, c->SQ.p, (size_t)c->total_rows);
+            CK(cudaGetLastError());
+        } else {
+            CK(cudaMemcpyAsync(c->E.p, c->Y.p, sizeof(float) * c->total_rows, cudaMemcpyDeviceToDevice, c->stream));
+        }
+    } else
         refresh(c, 0, c->n_local);
     sync(c);
     API_END

@@ -61,9 +61,10 @@ class _Context:
         N.check(getattr(self.L, name)(self.h, *args), name)
 
     def info(self):
-        buf = np.zeros(8, np.int64)
+        buf = np.zeros(10, np.int64)
         self.call("mace_ctx_info", N.ptr(buf))
-        return dict(zip(["nnz", "n_items", "NV", "sv_smem", "sv_grid", "num_sms", "passes", "S"], buf.tolist()))
+        return dict(zip(["nnz", "n_items", "NV", "sv_smem", "sv_grid", "num_sms", "passes", "S", "weighted"],
+                        buf.tolist()))
 
     def load_matrix(self, matrices):
         self.n_side = _n_side_of(matrices)
@@ -182,6 +183,12 @@ class AgentPlan(_Context):
         self.n_agents = len(self.agent_views)
         self.n_local = self.n_agents * self.n_slices
         self.set_schedule(DEFAULT_CONCURRENCY, int(os.environ.get("MACE_SV_MAX_WARPS", "0")))
+        # weighted records (a sqrt(lambda), k_sv.cuh) where the data allow them; MACE_WEIGHTED=0 forbids
+        self.set_weighting(os.environ.get("MACE_WEIGHTED", "1") != "0")
+
+    def set_weighting(self, allow: bool):
+        """Allow or forbid K2's weighted records from the next ``load_data`` on."""
+        self.call("mace_set_weighting", int(bool(allow)))
 
     def agent_info(self, a):
         buf = np.zeros(8, np.int64)

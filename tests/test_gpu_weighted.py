@@ -1,0 +1,109 @@
+"""K2 weighted records (k_sv.cuh): slot records a sqrt(lambda) and the error sinogram kept as
+sqrt(lambda) e give the same super-voxel iterates as the plain records with a lambda plane, the
+error sinogram the host reads back is still y - A z, and data with a zero weight fall back to the
+plain records."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+import paper_1911_09278_b200 as mb
+from paper_1911_09278_b200 import engine
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b)) / max(float(np.linalg.norm(b)), 1e-300)
+
+
+def _ellipse_problem(golden):
+    ns, nv, nc = 32, 45, 47
+    geom = mb.Geometry(ns, 4.0, nv, nc, 4.0)
+    return mb.ReconProblem(geom, mb.build_system_matrix(geom), golden["ell_y"], golden["ell_w"],
+                           mb.PriorParams("qggmrf", 20.0, 2.0, 1.2, 1.0, 0.01))
+
+
+def _solve(prob, weighted, iters, monkeypatch, sigma=3e-4, sv_side=4):
+    monkeypatch.setenv("MACE_WEIGHTED", "1" if weighted else "0")
+    engine.clear_cache()
+    cfg = mb.MaceConfig(n_subsets=4, rho=0.8, sigma=sigma, max_outer=iters, tol=1e-300, residuals="none",
+                        schedule="sv", sv_side=sv_side)
+    try:
+        res = mb.mace_solve(prob, cfg)
+    except mb.ConvergenceError as err:  # tol = 1e-300: a fixed iteration budget
+        res = err.last_iterate
+    views = [tuple(s.view_indices) for s in mb.partition_views(prob.geom.n_views, 4)]
+    plan = engine.plan_for(prob.matrices, views, schedule="sv", sv=sv_side)
+    flag = plan.info()["weighted"]
+    engine.clear_cache()
+    return res, flag
+
+
+def test_weighted_and_plain_records_give_the_same_iterates(monkeypatch):
+    # the setting of test_gpu_parity::test_sv_schedule_deterministic_enough_and_reproducible (a
+    # strongly contracting iteration, where run-to-run float-atomic noise stays ~1e-6)
+    ns, nv, nc = 8, 16, 11
+    geom = mb.Geometry(ns, 1.0, nv, nc, ns / nc * 1.1)
+    rng = np.random.default_rng(31)
+    y = rng.standard_normal((nv, nc))
+    w = 0.5 + rng.random((nv, nc))
+    prob = mb.ReconProblem(geom, mb.build_system_matrix(geom), y, w, mb.PriorParams("qggmrf", 1.0, sigma_x=0.5))
+    rw, fw = _solve(prob, True, 50, monkeypatch, sigma=0.2, sv_side=8)
+    rp, fp = _solve(prob, False, 50, monkeypatch, sigma=0.2, sv_side=8)
+    assert (fw, fp) == (1, 0)
+    assert rel(rw.image, rp.image) < 1e-5
+    assert rel(rw.stack, rp.stack) < 1e-5
+
+
+def test_weighted_fixed_point_is_the_centralized_map(golden, monkeypatch):
+    prob = _ellipse_problem(golden)
+    res, flag = _solve(prob, True, 3000, monkeypatch)
+    assert flag == 1
+    assert rel(res.image, golden["ell_central"]) < 1e-3
+
+
+def test_weighted_error_sinogram_reads_back_as_residual(monkeypatch):
+    monkeypatch.setenv("MACE_WEIGHTED", "1")
+    ns, nv, nc = 16, 24, 23
+    geom = mb.Geometry(ns, 1.0, nv, nc, 1.0)
+    mats = mb.build_system_matrix(geom)
+    rng = np.random.default_rng(4)
+    y = rng.standard_normal((nv, nc))
+    w = 0.5 + 100.0 * rng.random((nv, nc))  # wide weight range: sqrt(lambda) from 0.7 to 10
+    prob = mb.ReconProblem(geom, mats, y, w, mb.PriorParams("qggmrf", 0.5, 2.0, 1.2, 1.0, 1.0))
+    sub = mb.partition_views(nv, 2)[1]
+    ws = mb.AgentWorkspace(prob, sub, 2, sigma=0.5, schedule="sv")
+    assert ws.plan.info()["weighted"] == 1
+    v = rng.standard_normal(ws.n)
+    for _ in range(mb.REFRESH_EVERY + 3):
+        mb.partial_update_prox(ws, v)
+    assert ws.error_drift() < 1e-5
+    # e read back = y_i - A_i z (icd.py:200), against the oracle's float64 forward projection
+    ref_mats = O.build_system_matrix(ns, 1.0, nv, nc, 1.0)
+    z = ws.state
+    ax = O.forward_project(ref_mats, z)
+    exact = np.concatenate([(y - ax)[j] for j in sub.view_indices])
+    assert rel(ws.error_sinogram, exact) < 1e-5
+
+
+def test_zero_weight_falls_back_to_plain_records(monkeypatch):
+    monkeypatch.setenv("MACE_WEIGHTED", "1")
+    ns, nv, nc = 16, 24, 23
+    geom = mb.Geometry(ns, 1.0, nv, nc, 1.0)
+    rng = np.random.default_rng(5)
+    y = rng.standard_normal((nv, nc))
+    w = 0.5 + rng.random((nv, nc))
+    w[3, 5] = 0.0
+    prob = mb.ReconProblem(geom, mb.build_system_matrix(geom), y, w, mb.PriorParams("qggmrf", 0.5, 2.0, 1.2, 1.0, 1.0))
+    sub = mb.partition_views(nv, 2)[0]
+    a = mb.AgentWorkspace(prob, sub, 2, sigma=0.5, schedule="sv")
+    b = mb.AgentWorkspace(prob, sub, 2, sigma=0.5, schedule="raster")
+    assert a.plan.info()["weighted"] == 0
+    v = rng.standard_normal(a.n)
+    za = mb.prox_solve(a, v, tol=1e-7, max_passes=3000)
+    zb = mb.prox_solve(b, v, tol=1e-7, max_passes=3000)
+    assert rel(za, zb) < 1e-4
