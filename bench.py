@@ -115,9 +115,12 @@ def algorithmic_bytes_per_pass(plan, n_agents_local) -> tuple[int, dict]:
     alg = 8 * nnz + 16 * n * n_agents_local + 12 * R
     # bytes the lane-per-view super-voxel layout streams per launch (layout.cpp): slot records
     # (ng*32*K lengths + 32 offset words per pixel slot, 4 slots per batch), 64 B of batch constants
-    # per batch, the tile's lambda band (ng x wcap x 32 floats) and z/v/w per pixel
+    # per batch, the tile's lambda band (ng x wcap x 32 floats; not with weighted records, whose
+    # lengths carry sqrt(lambda)) and z/v/w per pixel
     lay_bytes = 0
-    S = plan.info()["S"]
+    ci = plan.info()
+    S = ci["S"]
+    band = 0 if ci.get("weighted") else 128
     if S < plan.n_side:
         nb = 4 * (((S // 2) ** 2 + 3) // 4)
         for a in range(n_agents_local):
@@ -125,7 +128,7 @@ def algorithmic_bytes_per_pass(plan, n_agents_local) -> tuple[int, dict]:
             V = len(plan.agent_views[a]) if hasattr(plan, "agent_views") else None
             ng = -(-V // 32) if V else 3
             rec = ng * 64 + 32
-            lay_bytes += info["n_sv"] * (nb * (4 * rec * 4 + 64) + ng * info["ctx_wcap"] * 128)
+            lay_bytes += info["n_sv"] * (nb * (4 * rec * 4 + 64) + ng * info["ctx_wcap"] * band)
         lay_bytes += 16 * n * n_agents_local
     return alg, {"nnz": nnz, "layout_entries": ent, "rows": R, "layout_bytes": lay_bytes,
                  "c_mean": nnz / (n * n_agents_local)}
@@ -280,7 +283,7 @@ def run_ours(args):
                 "note": "mace_solve() on host float64 y/weights; includes H2D, solve, D2H image+stack"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                      "frac": achieved / pk.get("hbm_gbs"), "traffic": k2_traffic(args.config, args.sv),
-                     "kernel": "k_icd_sv (K2)",
+                     "kernel": "k_icd_sv (K2)", "records": "weighted" if plan.info().get("weighted") else "plain",
                      "bytes_per_launch": alg, "layout_bytes_per_launch": lay["layout_bytes"],
                      "k2_avg_ms": k2_avg_ms, "k2_share": k2_ms / ms, "c_mean": lay["c_mean"],
                      "peak_source": "MEASURED_PEAKS.json" if not pk.get("_fallback") else "fallback"},
