@@ -27,6 +27,7 @@
 //  * Epilogue: the band's net change e - e0 is folded into global e with red.add (tiles of the
 //    same agent that share rows run concurrently), then z, the Mann step and norm partials.
 #pragma once
+#include <type_traits>
 #include "dev_common.cuh"
 #include "k2_launch.h"
 
@@ -314,7 +315,10 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
         }
         if constexpr (!kW) cp_async_wait<0>();  // this lane's lambda copies have landed
         __syncwarp();        // ... and every other lane's; band / zt / v / w stores visible
-        auto step = [&](const int b, const SvBatch<K, NG>& C, SvBatch<K, NG>& Nx) {
+        // kFull: the tile lies inside the image (all but the last tile row / column), so no slot
+        // needs the image-edge test
+        auto step = [&](const int b, const SvBatch<K, NG>& C, SvBatch<K, NG>& Nx, auto full_tag) {
+            constexpr bool kFull = decltype(full_tag)::value;
             if (b + 1 < NB) load_batch<K, NG>(Nx, recs + (size_t)(b + 1) * 4 * RECW, lane);
             const float4 k0 = __ldg(reinterpret_cast<const float4*>(bcs + 16 * b));
             const float4 k1 = __ldg(reinterpret_cast<const float4*>(bcs + 16 * b) + 1);
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
             for (int p = 0; p < 4; ++p) {
                 kx[p] = (int)((kxw >> (8 * p)) & 0xffu);
                 ok[p] = (PER_CLASS % 4 == 0 || kx[p] != 0xff) &&
-                        (full || (r0 + kx[p] / S < n && c0 + kx[p] % S < n));
+                        (kFull || (r0 + kx[p] / S < n && c0 + kx[p] % S < n));
                 if (PER_CLASS % 4 != 0 && kx[p] == 0xff) kx[p] = 0;
             }
             // theta1 partials against the band as it stands before the batch
@@ -360,7 +364,7 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
             float den_l;
             {
                 int kl = (int)((kxw >> (8 * pp)) & 0xffu);
-                const bool okl = (PER_CLASS % 4 == 0 || kl != 0xff) && (full || (r0 + kl / S < n && c0 + kl % S < n));
+                const bool okl = (PER_CLASS % 4 == 0 || kl != 0xff) && (kFull || (r0 + kl / S < n && c0 + kl % S < n));
                 if (PER_CLASS % 4 != 0 && kl == 0xff) kl = 0;
                 float g = 0.f, c = 0.f;
                 if (okl && beta > 0.f) {
@@ -458,10 +462,18 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
                     for (int q = 0; q < K; ++q) sb[ab[p][g] + q * U] = fmaf(-alpha[p], av[p][g][q], ev[g][q]);
             }
         };
+        if (full) {
 #pragma unroll 1
-        for (int b = 0; b < NB; b += 2) {  // ping-pong record buffers (NB is a multiple of 4)
-            step(b, cur, nxt);
-            step(b + 1, nxt, cur);
+            for (int b = 0; b < NB; b += 2) {  // ping-pong record buffers (NB is a multiple of 4)
+                step(b, cur, nxt, std::true_type{});
+                step(b + 1, nxt, cur, std::true_type{});
+            }
+        } else {
+#pragma unroll 1
+            for (int b = 0; b < NB; b += 2) {
+                step(b, cur, nxt, std::false_type{});
+                step(b + 1, nxt, cur, std::false_type{});
+            }
         }
 
         // -- 5. fold the band's net change into global e (vector red.add over the window's aligned
