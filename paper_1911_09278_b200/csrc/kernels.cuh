@@ -364,30 +364,52 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
             for (int o = 0; o < W; ++o) lb[o * 32] = o < bj.y ? A.lam[bj.x + o] : 0.f;
         }
     }
-    const uint32_t* rb = A.rec0 + ((size_t)sv * nb + b) * 4 * recw;
-    uint32_t* wb = kW ? A.recw + ((size_t)sv * nb + b) * 4 * recw : nullptr;
+    const uint32_t* __restrict__ rb = A.rec0 + ((size_t)sv * nb + b) * 4 * recw;
+    uint32_t* __restrict__ wb = kW ? A.recw + ((size_t)sv * nb + b) * 4 * recw : nullptr;
+    // all loads first (records, then the lambda rows they touch), then the weighted records and
+    // the sums: no store sits between two loads, so the loads of a task overlap
+    uint32_t ow[4];
+    float a[4][NG][K], l[4][NG][K];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const uint32_t* r = rb + (size_t)p * recw;
+        ow[p] = __ldcs(r + NG * 32 * K + lane);
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+#pragma unroll
+            for (int q = 0; q < K; ++q) a[p][g][q] = __uint_as_float(__ldcs(r + (g * 32 + lane) * K + q));
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+                l[p][g][q] = a[p][g][q] != 0.f ? __ldg(A.lam + start[g] + (int)((ow[p] >> (8 * g)) & 0xffu) + q) : 0.f;
+    if (kW) {  // weighted record a sqrt(lambda): theta2 and the cross terms are its plain products
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            uint32_t* w = wb + (size_t)p * recw;
+            __stcs(w + NG * 32 * K + lane, ow[p]);
+#pragma unroll
+            for (int g = 0; g < NG; ++g)
+#pragma unroll
+                for (int q = 0; q < K; ++q) {
+                    a[p][g][q] *= sqrtf(l[p][g][q]);
+                    l[p][g][q] = 1.f;
+                    __stcs(w + (g * 32 + lane) * K + q, __float_as_uint(a[p][g][q]));
+                }
+        }
+    }
     float t2[4] = {0.f, 0.f, 0.f, 0.f}, cx[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
-        float a[4][K], l[4][K];
         int o[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            const uint32_t* r = rb + (size_t)p * recw;
-            const uint32_t ow = r[NG * 32 * K + lane];
-            o[p] = (int)((ow >> (8 * g)) & 0xffu);
-            if (kW && g == 0) wb[(size_t)p * recw + NG * 32 * K + lane] = ow;
+            o[p] = (int)((ow[p] >> (8 * g)) & 0xffu);
 #pragma unroll
-            for (int q = 0; q < K; ++q) {
-                a[p][q] = __uint_as_float(r[(g * 32 + lane) * K + q]);
-                l[p][q] = a[p][q] != 0.f ? A.lam[start[g] + o[p] + q] : 0.f;
-                if (kW) {  // weighted record a sqrt(lambda): theta2 and the cross terms are its plain products
-                    a[p][q] *= sqrtf(l[p][q]);
-                    l[p][q] = 1.f;
-                    wb[(size_t)p * recw + (g * 32 + lane) * K + q] = __float_as_uint(a[p][q]);
-                }
-                t2[p] = fmaf(a[p][q] * a[p][q], l[p][q], t2[p]);
-            }
+            for (int q = 0; q < K; ++q) t2[p] = fmaf(a[p][g][q] * a[p][g][q], l[p][g][q], t2[p]);
         }
         int x = 0;
 #pragma unroll
@@ -398,7 +420,7 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
                 for (int q = 0; q < K; ++q)
 #pragma unroll
                     for (int qj = 0; qj < K; ++qj)  // row o_i + q of pixel i is row o_j + qj of pixel j
-                        if (o[i] + q == o[j] + qj) cx[x] = fmaf(a[i][q] * a[j][qj], l[i][q], cx[x]);
+                        if (o[i] + q == o[j] + qj) cx[x] = fmaf(a[i][g][q] * a[j][g][qj], l[i][g][q], cx[x]);
     }
 #pragma unroll
     for (int p = 0; p < 4; ++p) t2[p] = warp_sum(t2[p]);
