@@ -197,18 +197,45 @@ class AgentPlan(_Context):
                         buf.tolist()))
 
     def load_data(self, y, weights):
-        """y / weights ([n_slices x] n_views x n_ch, any float dtype) -> pinned float32 staging -> device."""
+        """y / weights ([n_slices x] n_views x n_ch, any float dtype; or, for a batch, sequences of
+        n_slices per-slice arrays) -> pinned float32 staging -> device."""
         rows = self.n_views * self.n_ch * getattr(self, "n_slices", 1)
         if getattr(self, "_pin", None) is None:
             p = ctypes.c_void_p()
             N.check(self.L.mace_host_alloc(2 * rows * 4, ctypes.byref(p)), "host_alloc")
             self._pin = p
             self._pin_arr = np.ctypeslib.as_array((ctypes.c_float * (2 * rows)).from_address(p.value))
-        _convert_into(self._pin_arr[:rows], np.asarray(y).reshape(-1))
-        _convert_into(self._pin_arr[rows:], np.asarray(weights).reshape(-1))
+        for k, src in enumerate((y, weights)):
+            dst = self._pin_arr[k * rows:(k + 1) * rows]
+            if isinstance(src, (list, tuple)):  # per-slice arrays straight into their staging slots
+                per = rows // max(len(src), 1)
+                if len(src) * per != rows:
+                    raise ValueError("need one sinogram per slice")
+                for j, a in enumerate(src):
+                    _convert_into(dst[j * per:(j + 1) * per], np.asarray(a).reshape(-1))
+            else:
+                _convert_into(dst, np.asarray(src).reshape(-1))
         self.call("mace_load_data", ctypes.c_void_p(self._pin.value), ctypes.c_void_p(self._pin.value + rows * 4))
 
+    def _pinned_out(self, count) -> np.ndarray:
+        """a pinned float32 host buffer for results (D2H at full PCIe rate); valid until the next call"""
+        if getattr(self, "_pout", None) is None or self._pout_n < count:
+            self._free_pout()
+            p = ctypes.c_void_p()
+            N.check(self.L.mace_host_alloc(count * 4, ctypes.byref(p)), "host_alloc")
+            self._pout, self._pout_n = p, count
+            self._pout_arr = np.ctypeslib.as_array((ctypes.c_float * count).from_address(p.value))
+        return self._pout_arr[:count]
+
+    def _free_pout(self):
+        if getattr(self, "_pout", None) is not None:
+            if getattr(self, "h", None):
+                self.L.mace_sync(self.h)
+            self.L.mace_host_free(self._pout)
+            self._pout = None
+
     def close(self):
+        self._free_pout()
         if getattr(self, "_pin", None) is not None:
             if getattr(self, "h", None):
                 self.L.mace_sync(self.h)
@@ -339,9 +366,11 @@ class AgentPlan(_Context):
         self.call("mace_read_log", int(n), N.ptr(lg), N.ptr(done))
         return lg[:n], (int(done[0]), int(done[1]))
 
-    def get_image(self, which) -> np.ndarray:
-        """wbar (which=0) or G_H(w) (which=1): shape (n,), or (n_slices, n) for a batch."""
-        out = np.empty((self.n_slices, self.n) if self.n_slices > 1 else self.n, np.float32)
+    def get_image(self, which, pinned=False) -> np.ndarray:
+        """wbar (which=0) or G_H(w) (which=1): shape (n,), or (n_slices, n) for a batch.  pinned: a
+        view of the plan's pinned result buffer (overwritten by the next pinned read)."""
+        shape = (self.n_slices, self.n) if self.n_slices > 1 else (self.n,)
+        out = self._pinned_out(int(np.prod(shape))).reshape(shape) if pinned else np.empty(shape, np.float32)
         self.call("mace_get_image", int(which), N.ptr(out))
         return out
 
@@ -351,10 +380,10 @@ class AgentPlan(_Context):
             raise ValueError("image size mismatch")
         self.call("mace_set_image", int(which), N.ptr(img))
 
-    def get_stack(self) -> np.ndarray:
-        """(n_local, n) for one slice, (n_slices, n_agents, n) for a batch."""
+    def get_stack(self, pinned=False) -> np.ndarray:
+        """(n_local, n) for one slice, (n_slices, n_agents, n) for a batch (pinned: as get_image)."""
         shape = (self.n_slices, self.n_agents, self.n) if self.n_slices > 1 else (self.n_local, self.n)
-        out = np.empty(shape, np.float32)
+        out = self._pinned_out(int(np.prod(shape))).reshape(shape) if pinned else np.empty(shape, np.float32)
         self.call("mace_get_stack", N.ptr(out))
         return out
 

@@ -18,6 +18,7 @@ never calls them.
 
 from __future__ import annotations
 
+import inspect
 import time
 from dataclasses import dataclass, field
 
@@ -289,6 +290,15 @@ def _f64(a: np.ndarray) -> np.ndarray:
     return torch.from_numpy(np.ascontiguousarray(a)).to(torch.float64).numpy()
 
 
+def _pinned_get(plan, name, *args):
+    """result read through the plan's pinned buffer when it has one (host-side test backends do not);
+    the caller converts it (_f64) before the next read"""
+    fn = getattr(plan, name)
+    if "pinned" in inspect.signature(fn).parameters:
+        return fn(*args, pinned=True)
+    return fn(*args)
+
+
 def _plan_stream(plan):
     """the plan's stream as a torch stream (GPU plans), None for host-side test backends"""
     ts = getattr(plan, "torch_stream", None)
@@ -459,8 +469,8 @@ def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=
     iterations = len(rows)
     converged = done[0] == 1
     _fill_log(log, rows, counter, N, n)
-    image = _f64(plan.get_image(1 if pnp else 0))
-    w_loc = _f64(plan.get_stack().reshape(len(local), n))
+    image = _f64(_pinned_get(plan, "get_image", 1 if pnp else 0))
+    w_loc = _f64(_pinned_get(plan, "get_stack").reshape(len(local), n))
     if comm is None:
         stack = w_loc
     else:
@@ -551,7 +561,7 @@ def mace_solve_batch(problems, config: MaceConfig) -> list:
                     sv=getattr(config, "sv_side", DEFAULT_SV), colours=getattr(config, "colours", DEFAULT_COLOURS),
                     device=getattr(config, "device", 0), n_slices=S)
     beta = p0.prior.beta if config.beta is None else config.beta
-    plan.load_data(np.stack([p.y for p in problems]), np.stack([p.weights for p in problems]))
+    plan.load_data([p.y for p in problems], [p.weights for p in problems])
     plan.set_prior(p0.prior)
     plan.set_agent_params(-1, beta / N, 1.0 / (config.sigma * config.sigma), config.clamp_nonneg)
     plan.stack_init(None, N)
@@ -564,8 +574,8 @@ def mace_solve_batch(problems, config: MaceConfig) -> list:
     if done[0] == 2:
         raise ConvergenceError(f"MACE diverged at iteration {done[1]} (reduce sigma)", last_iterate=None)
     iters = done[1] if done[0] == 1 else config.max_outer
-    images = _f64(plan.get_image(0).reshape(S, n))
-    stacks = _f64(plan.get_stack().reshape(S, N, n))
+    images = _f64(plan.get_image(0, pinned=True).reshape(S, n))
+    stacks = _f64(plan.get_stack(pinned=True).reshape(S, N, n))
     log = ConvergenceLog()
     counter = EquitCounter(n, N)
     _fill_log(log, [(lg[j, 0], None, wall * (j + 1) / max(iters, 1)) for j in range(iters)], counter, N, n)
