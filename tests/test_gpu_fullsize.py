@@ -49,3 +49,34 @@ def test_fixed_point_matches_cpu_oracle_map(config, iters):
     cost = mb.map_cost(prob, res.image)
     assert cost == pytest.approx(float(ref["cost"]), rel=1e-4)
     assert cost >= float(ref["cost"]) * (1 - 1e-5)
+
+
+def test_config4_batch_reaches_each_slice_fixed_point():
+    """Config 4's batched path at full size (512^2, 720 x 725, N=8): four slices share one operator;
+    slice 0 is config 1's scan, so its fixed point is the CPU-oracle MAP central_c1, and slice 1
+    must land where an unbatched solve of the same slice lands."""
+    c = gen.CONFIGS[4]
+    ref = np.load(os.path.join(GOLDEN, "central_c1.npz"))
+    geom, mats, _, y0, lam0 = gen.make_scan(1)
+    scans = [(y0, lam0)] + [gen.make_scan(4, slice_index=s, matrices=mats)[3:] for s in (1, 2, 3)]
+    prior = mb.PriorParams("qggmrf", c["beta"], 2.0, 1.2, 1.0, 0.01)
+    probs = [mb.ReconProblem(geom, mats, y, lam, prior) for y, lam in scans]
+    iters = 3000
+    cfg = mb.MaceConfig(n_subsets=c["n_agents"], rho=0.8, sigma=c["sigma"], max_outer=iters, tol=1e-300,
+                        residuals="none")
+    try:
+        res = mb.mace_solve_batch(probs, cfg)
+    except mb.ConvergenceError as err:
+        res = err.last_iterate
+    assert len(res) == 4 and res[0].iterations == iters
+    x_star = ref["image"].astype(np.float64)
+    nr0 = float(np.linalg.norm(res[0].image - x_star) / np.linalg.norm(x_star))
+    print(f"config 4 batch: slice 0 NRMSE vs the CPU-oracle MAP after {iters} iterations = {nr0:.2e}")
+    assert nr0 <= 1e-3
+    try:
+        single = mb.mace_solve(probs[1], cfg)
+    except mb.ConvergenceError as err:
+        single = err.last_iterate
+    d1 = float(np.linalg.norm(res[1].image - single.image) / np.linalg.norm(single.image))
+    print(f"config 4 batch: slice 1 batched vs unbatched after {iters} iterations = {d1:.2e}")
+    assert d1 <= 1e-3
