@@ -844,9 +844,9 @@ int mace_load_data(void* p, const float* y, const float* lam)
     if (c->n_local) {
         // weighted records need one lambda per record (a single slice) and lambda > 0 everywhere,
         // so that e = e' / sqrt(lambda) stays recoverable (mace_get_error)
-        bool pos = true;
-        for (size_t i = 0; i < total && pos; ++i) pos = lam[i] > 0.f;
-        set_weighted(c, c->allow_weighted && c->schedule == 0 && c->n_slices == 1 && pos);
+        bool want = c->allow_weighted && c->schedule == 0 && c->n_slices == 1;
+        for (size_t i = 0; i < total && want; ++i) want = lam[i] > 0.f;
+        set_weighted(c, want);
         k_gather_data<<<c->num_sms * 4, 256, 0, c->stream>>>(c->d_agents.p, c->row_base.p, c->n_local, c->total_rows,
                                                               c->n_ch, c->y.p, c->lam.p, (int64_t)rows);
         CK(cudaGetLastError());
