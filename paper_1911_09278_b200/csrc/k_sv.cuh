@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
     float* zt = sb + NG * W * U;
     float* svv = zt + T2p;
     float* swo = svv + SS;
+    float4* sred = reinterpret_cast<float4*>(swo + SS);  // the batch's {theta1', den} pairs, broadcast through smem
     const int n = P.n_side;
     const PriorC& PR = P.pr;
     const bool quad = PR.kind == 0;
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
                 num[p] = a0 + a1;
             }
             // prior of batch pixel pp, neighbour kk (independent across the batch)
-            float den_l;
+            float den_l, den4[4];
             {
                 int kl = (int)((kxw >> (8 * pp)) & 0xffu);
                 const bool okl = (PER_CLASS % 4 == 0 || kl != 0xff) && (kFull || (r0 + kl / S < n && c0 + kl % S < n));
@@ -401,7 +402,20 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
                     den_l += __shfl_xor_sync(FULL, den_l, o);
                 }
 #pragma unroll
-                for (int p = 0; p < 4; ++p) num[p] = __shfl_sync(FULL, kp, 8 * p);
+                // every lane needs all four sums: the group leaders store {num_p, den_p} and every lane
+                // reads them back as two broadcast 16-byte loads (3 LSU operations instead of 8 shuffles)
+                __syncwarp();  // the previous batch's reads are done
+                if ((lane & 7) == 0) reinterpret_cast<float2*>(sred)[pp] = make_float2(kp, den_l);
+                __syncwarp();
+                const float4 r01 = sred[0], r23 = sred[1];
+                num[0] = r01.x;
+                num[1] = r01.z;
+                num[2] = r23.x;
+                num[3] = r23.z;
+                den4[0] = r01.y;
+                den4[1] = r01.w;
+                den4[2] = r23.y;
+                den4[3] = r23.w;
             }
             // the four 1-D solves (icd.py:128-134): everything but the coupling to earlier pixels of
             // the batch is independent across p; the reference skips pixels with den <= 0
@@ -409,7 +423,7 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
             int ci[4];
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
-                const float den_p = __shfl_sync(FULL, den_l, 8 * p);
+                const float den_p = den4[p];
                 ci[p] = (kx[p] / S + 1) * S2 + kx[p] % S + 1;
                 zs[p] = zt[ci[p]];
                 float dn = den_p + bk[p] + inv_s2;
