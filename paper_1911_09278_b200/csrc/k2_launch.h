@@ -12,12 +12,12 @@ constexpr int kSvThreads = 32;  // one warp per block: a block is one tile worke
 
 // shared-memory bytes per warp: the band (per row unit u = g W + o: e, lambda and e0 as three
 // 32-word lane vectors at word 96 u; weighted records: e and e0 at word 64 u), the state tile
-// with halo, per-pixel v and w, and the batch's four {theta1, den} pairs (32 B)
+// with halo, per-pixel v and w, and the batch's four {theta1, den, z, v} (64 B)
 __host__ __device__ constexpr int sv_unit_words(bool weighted) { return weighted ? 64 : 96; }
 __host__ __device__ constexpr size_t sv_warp_bytes(int S, int ng, int wcap, bool weighted)
 {
     return 4 * (size_t)sv_unit_words(weighted) * ng * wcap + 4 * (size_t)((((S + 2) * (S + 2)) + 3) & ~3) +
-           8 * (size_t)S * S + 32;
+           8 * (size_t)S * S + 64;
 }
 
 struct SvLaunch {

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
     float* zt = sb + NG * W * U;
     float* svv = zt + T2p;
     float* swo = svv + SS;
-    float4* sred = reinterpret_cast<float4*>(swo + SS);  // the batch's {theta1', den} pairs, broadcast through smem
+    float4* sred = reinterpret_cast<float4*>(swo + SS);  // the batch's {theta1', den, z, v} per pixel, broadcast through smem
     const int n = P.n_side;
     const PriorC& PR = P.pr;
     const bool quad = PR.kind == 0;
@@ -362,11 +362,13 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
                 num[p] = a0 + a1;
             }
             // prior of batch pixel pp, neighbour kk (independent across the batch)
-            float den_l, den4[4];
+            float den_l, den4[4], zs4[4], vv4[4];
             {
                 int kl = (int)((kxw >> (8 * pp)) & 0xffu);
                 const bool okl = (PER_CLASS % 4 == 0 || kl != 0xff) && (kFull || (r0 + kl / S < n && c0 + kl % S < n));
                 if (PER_CLASS % 4 != 0 && kl == 0xff) kl = 0;
+                // z and v of this lane's batch pixel (the group leader passes them on)
+                const float zlead = zt[(kl / S + 1) * S2 + kl % S + 1], vlead = svv[kl];
                 float g = 0.f, c = 0.f;
                 if (okl && beta > 0.f) {
                     const int lr = kl / S, lc = kl % S;
@@ -402,20 +404,20 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
                     den_l += __shfl_xor_sync(FULL, den_l, o);
                 }
 #pragma unroll
-                // every lane needs all four sums: the group leaders store {num_p, den_p} and every lane
-                // reads them back as two broadcast 16-byte loads (3 LSU operations instead of 8 shuffles)
+                // every lane needs all four pixels' sums and their z, v: the group leaders store
+                // {num_p, den_p, z_p, v_p} and every lane reads them back as four broadcast 16-byte loads
+                // (7 LSU operations instead of 8 shuffles and 8 scalar loads)
                 __syncwarp();  // the previous batch's reads are done
-                if ((lane & 7) == 0) reinterpret_cast<float2*>(sred)[pp] = make_float2(kp, den_l);
+                if ((lane & 7) == 0) sred[pp] = make_float4(kp, den_l, zlead, vlead);
                 __syncwarp();
-                const float4 r01 = sred[0], r23 = sred[1];
-                num[0] = r01.x;
-                num[1] = r01.z;
-                num[2] = r23.x;
-                num[3] = r23.z;
-                den4[0] = r01.y;
-                den4[1] = r01.w;
-                den4[2] = r23.y;
-                den4[3] = r23.w;
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const float4 r = sred[p];
+                    num[p] = r.x;
+                    den4[p] = r.y;
+                    zs4[p] = r.z;
+                    vv4[p] = r.w;
+                }
             }
             // the four 1-D solves (icd.py:128-134): everything but the coupling to earlier pixels of
             // the batch is independent across p; the reference skips pixels with den <= 0
@@ -425,14 +427,14 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
             for (int p = 0; p < 4; ++p) {
                 const float den_p = den4[p];
                 ci[p] = (kx[p] / S + 1) * S2 + kx[p] % S + 1;
-                zs[p] = zt[ci[p]];
+                zs[p] = zs4[p];
                 float dn = den_p + bk[p] + inv_s2;
                 nm[p] = num[p];
                 if (quad && beta > 0.f) {
                     nm[p] -= beta * PR.eps2 * zs[p];
                     dn += beta * PR.eps2;
                 }
-                nm[p] -= inv_s2 * (zs[p] - svv[kx[p]]);
+                nm[p] -= inv_s2 * (zs[p] - vv4[p]);
                 float r;
                 asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(dn));
                 rd[p] = (ok[p] && dn > 0.f) ? r : 0.f;
@@ -454,8 +456,22 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
                 } else if (p == 2) {
                     nm[3] -= al * bk[9];
                 }
-                if (ok[p]) zt[ci[p]] = zs[p] + al;  // every lane writes the same value: no sync needed
                 dsq = fmaf(al, al, dsq);
+            }
+            {  // lane p < 4 stores pixel p's new value (one store instead of four); the next reads of
+               // zt by other lanes come after a __syncwarp
+                float zn = zs[0] + alpha[0];
+                int cw = ci[0];
+                bool okw = ok[0];
+#pragma unroll
+                for (int p = 1; p < 4; ++p)
+                    if (lane == p) {
+                        zn = zs[p] + alpha[p];
+                        cw = ci[p];
+                        okw = ok[p];
+                    }
+                if (lane < 4 && okw) zt[cw] = zn;
+                __syncwarp();
             }
             // scatter e -= alpha_p a_p in pixel order (a row may be shared within the batch, never
             // within one pixel): pixel 0 from the gathered values, then reload-modify-store
