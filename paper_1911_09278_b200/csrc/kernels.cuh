@@ -343,8 +343,10 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
                                                    int n_side, int S, int nb, int W)
 {
     const int lane = threadIdx.x & 31;
-    const long task = (long)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);  // one warp per (item, batch)
-    if (task >= (long)n_items * nb) return;
+    const long n_tasks = (long)n_items * nb;
+    // one warp per (item, batch) task, grid-stride over a persistent grid
+    for (long task = (long)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); task < n_tasks;
+         task += (long)((gridDim.x * blockDim.x) >> 5)) {
     const int item = (int)(task / nb), b = (int)(task % nb);
     const int h = S / 2, per_class = h * h, bpc = (per_class + 3) / 4;
     const int recw = NG * 32 * K + 32;
@@ -438,6 +440,7 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
             if (r0 + lr < n_side && c0 + lc < n_side) A.th[(size_t)(r0 + lr) * n_side + c0 + lc] = v;
         }
     }
+    }  // task
 }
 
 // agent rows <- global y / lambda (local row r = j n_ch + c, icd.py:187-188)

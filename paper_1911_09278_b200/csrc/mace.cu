@@ -284,7 +284,7 @@ static void compute_theta2(Ctx* c)
     } else {
         // one warp per (item, batch)
         const int nb = sv_batches(c->S);
-        const long blocks = std::max(1L, ((long)c->n_items * nb + 3) / 4);
+        const long blocks = std::max(1L, ((long)c->n_items * nb + 3) / 4);  // one warp per task (a persistent grid is slower)
         auto go = [&](auto kern) {
             kern<<<(unsigned)blocks, 128, 0, c->stream>>>(c->d_agents.p, c->n_items, c->queue.p, c->n_side, c->S, nb,
                                                           c->sv_wcap);
@@ -346,6 +346,7 @@ static void set_weighted(Ctx* c, bool on)
     }
     const bool changed = on != c->weighted;
     c->weighted = on;
+    if (!changed) return;  // the agents already point at the right records and sqrt(lambda) rows
     std::vector<int> rb(c->n_local + 1, 0);
     CK(cudaMemcpy(rb.data(), c->row_base.p, sizeof(int) * (c->n_local + 1), cudaMemcpyDeviceToHost));
     for (int va = 0; va < c->n_local; ++va) {
@@ -360,7 +361,7 @@ static void set_weighted(Ctx* c, bool on)
     if (c->sv_smem > 227 * 1024) throw std::runtime_error("super-voxel band does not fit in shared memory");
     CK(cudaMemcpyAsync(c->d_agents.p, c->h_agents.data(), sizeof(AgentDev) * c->n_local, cudaMemcpyHostToDevice,
                        c->stream));
-    if (changed) sync(c);
+    sync(c);
 }
 
 static void ensure_log(Ctx* c, int n)
@@ -845,7 +846,11 @@ int mace_load_data(void* p, const float* y, const float* lam)
         // weighted records need one lambda per record (a single slice) and lambda > 0 everywhere,
         // so that e = e' / sqrt(lambda) stays recoverable (mace_get_error)
         bool want = c->allow_weighted && c->schedule == 0 && c->n_slices == 1;
-        for (size_t i = 0; i < total && want; ++i) want = lam[i] > 0.f;
+        if (want) {  // min over the weights (vectorisable: no early exit)
+            float mn = lam[0];
+            for (size_t i = 1; i < total; ++i) mn = std::min(mn, lam[i]);
+            want = mn > 0.f;
+        }
         set_weighted(c, want);
         k_gather_data<<<c->num_sms * 4, 256, 0, c->stream>>>(c->d_agents.p, c->row_base.p, c->n_local, c->total_rows,
                                                               c->n_ch, c->y.p, c->lam.p, (int64_t)rows);
