@@ -377,9 +377,23 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
         const uint32_t* r = rb + (size_t)p * recw;
         ow[p] = __ldcs(r + NG * 32 * K + lane);
 #pragma unroll
-        for (int g = 0; g < NG; ++g)
+        for (int g = 0; g < NG; ++g) {  // the lane's K lengths are adjacent: one vector load
+            const uint32_t* rq = r + (g * 32 + lane) * K;
+            if constexpr (K == 2) {
+                const uint2 v = __ldcs(reinterpret_cast<const uint2*>(rq));
+                a[p][g][0] = __uint_as_float(v.x);
+                a[p][g][1] = __uint_as_float(v.y);
+            } else if constexpr (K == 4) {
+                const uint4 v = __ldcs(reinterpret_cast<const uint4*>(rq));
+                a[p][g][0] = __uint_as_float(v.x);
+                a[p][g][1] = __uint_as_float(v.y);
+                a[p][g][2] = __uint_as_float(v.z);
+                a[p][g][3] = __uint_as_float(v.w);
+            } else {
 #pragma unroll
-            for (int q = 0; q < K; ++q) a[p][g][q] = __uint_as_float(__ldcs(r + (g * 32 + lane) * K + q));
+                for (int q = 0; q < K; ++q) a[p][g][q] = __uint_as_float(__ldcs(rq + q));
+            }
+        }
     }
 #pragma unroll
     for (int p = 0; p < 4; ++p)
@@ -394,13 +408,23 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
             uint32_t* w = wb + (size_t)p * recw;
             __stcs(w + NG * 32 * K + lane, ow[p]);
 #pragma unroll
-            for (int g = 0; g < NG; ++g)
+            for (int g = 0; g < NG; ++g) {
 #pragma unroll
                 for (int q = 0; q < K; ++q) {
                     a[p][g][q] *= sqrtf(l[p][g][q]);
                     l[p][g][q] = 1.f;
-                    __stcs(w + (g * 32 + lane) * K + q, __float_as_uint(a[p][g][q]));
                 }
+                uint32_t* wq = w + (g * 32 + lane) * K;
+                if constexpr (K == 2) {
+                    __stcs(reinterpret_cast<uint2*>(wq), make_uint2(__float_as_uint(a[p][g][0]), __float_as_uint(a[p][g][1])));
+                } else if constexpr (K == 4) {
+                    __stcs(reinterpret_cast<uint4*>(wq), make_uint4(__float_as_uint(a[p][g][0]), __float_as_uint(a[p][g][1]),
+                                                                    __float_as_uint(a[p][g][2]), __float_as_uint(a[p][g][3])));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < K; ++q) __stcs(wq + q, __float_as_uint(a[p][g][q]));
+                }
+            }
         }
     }
     float t2[4] = {0.f, 0.f, 0.f, 0.f}, cx[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
