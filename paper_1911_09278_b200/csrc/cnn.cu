@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -270,6 +271,177 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * 64) : "memory");
 }
 
+// Row-pair variant of the 64->64 layer.  Output rows come in pairs (y, y+1) and their two
+// accumulators sit side by side in TMEM, so a halo row that feeds both rows is one N = 128 UMMA
+// against two taps' weights stored next to each other: per (dx, K-step) halo rows y and y+1 each
+// give one N = 128 UMMA (B = [W_dy1 | W_dy0] and [W_dy2 | W_dy1]) and rows y-1 and y+2 one N = 64
+// UMMA each: 48 UMMAs per pair instead of 72 (an N = 128 UMMA costs 64 cycles against 48 for
+// N = 64, tools/micro/umma_rate.cu).  Weights: [dx 3][ic-group 8][dy2 | dy1 | dy0 x 64 oc][8 ic].
+// A CTA with an odd row count finishes with one single row (N = 64 only).
+constexpr uint32_t kIdesc128 =
+    (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+constexpr int kW2Dx = 8 * 3 * kC * 16;  // 24,576 B per dx: [icg 8][192 oc][8 ic]
+constexpr int kW2Icg = 3 * kC * 16;     // 3,072 B per ic-group
+
+__device__ __forceinline__ void umma_i(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate)
+{
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ CUtensorMap amap,
+                                                       const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* out,
+                                                       int H, int W, int Wp, int rows_per_cta)
+{
+    extern __shared__ __align__(1024) unsigned char sm[];
+    unsigned char* sw = sm;
+    unsigned char* slots = sm + kWBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + kSlots * kSlotBytes);
+    uint64_t* wbar = bars;
+    uint64_t* sfull = bars + 1;
+    uint64_t* sempty = sfull + kSlots;
+    uint64_t* afull = sempty + kSlots;   // [2] accumulator pair ready
+    uint64_t* aempty = afull + kAcc;     // [2] accumulator pair drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kAcc);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int strips = (W + kTileX - 1) / kTileX;
+    const int strip = blockIdx.x % strips;
+    const int x0 = strip * kTileX;
+    const int y0 = (blockIdx.x / strips) * rows_per_cta;
+    const int y1 = min(H, y0 + rows_per_cta);
+    if (y0 >= H) return;
+    const int n_units = (y1 - y0 + 1) / 2;  // pairs, the last one possibly a single row
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(tmem_slot)),
+                     "n"(kAcc * 64)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 32) {
+        mbar_init(wbar, 1);
+        for (int i = 0; i < kSlots; ++i) {
+            mbar_init(sfull + i, 1);
+            mbar_init(sempty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(afull + i, 1);
+            mbar_init(aempty + i, 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const int rbase = y0 - 1;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer (as k_conv64_tc)
+            mbar_expect(wbar, kWBytes);
+            bulk_copy(sw, wts, kWBytes, wbar);
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            for (int r = y0 - 1; r <= y1; ++r) {
+                const int q = r - rbase, s = q % kSlots, u = q / kSlots;
+                if (u >= 1) mbar_wait(sempty + s, (uint32_t)((u - 1) & 1));
+                mbar_expect(sfull + s, kSlotBytes);
+                tma_row(slots + s * kSlotBytes, &amap, x0 / 8 - 1, r, sfull + s);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
+            mbar_wait(wbar, 0);
+            for (int t = 0; t < n_units; ++t) {
+                const int y = y0 + 2 * t, b = t & 1, ub = t >> 1;
+                const bool pair = y + 1 < y1;
+                if (ub >= 1) mbar_wait(aempty + b, (uint32_t)((ub - 1) & 1));
+                for (int r = y - 1; r <= y + (pair ? 2 : 1); ++r) {
+                    const int q = r - rbase;
+                    mbar_wait(sfull + q % kSlots, (uint32_t)((q / kSlots) & 1));
+                }
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d = tmem + (uint32_t)(b * 128);
+                // one halo row r against weight block blk (0 = dy2, 1 = dy1, 2 = dy0) with N = 64 or 128
+                auto row = [&](int r, int blk, uint32_t dcol, uint32_t idesc, bool first) {
+                    const uint64_t a0 = sdesc(sl_base + ((r - rbase) % kSlots) * kSlotBytes, kHaloX * 16, 128);
+                    const uint64_t b0 = sdesc(sw_base + blk * kC * 16, kW2Icg, 128);
+#pragma unroll
+                    for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint64_t a = a0 + (uint64_t)(((kHaloOff + dx) * 16 + 2 * j * (kHaloX * 16)) >> 4);
+                            const uint64_t bd = b0 + (uint64_t)((dx * kW2Dx + 2 * j * kW2Icg) >> 4);
+                            umma_i(dcol, a, bd, idesc, (first && dx == 0 && j == 0) ? 0u : 1u);
+                        }
+                };
+                if (pair) {
+                    row(y, 1, d, kIdesc128, true);          // [acc_y | acc_y+1] = A_y [W_dy1 | W_dy0]
+                    row(y + 1, 0, d, kIdesc128, false);     // += A_y+1 [W_dy2 | W_dy1]
+                    row(y - 1, 2, d, kIdesc, false);        // acc_y += A_y-1 W_dy0
+                    row(y + 2, 0, d + 64, kIdesc, false);   // acc_y+1 += A_y+2 W_dy2
+                } else {
+                    row(y - 1, 2, d, kIdesc, true);
+                    row(y, 1, d, kIdesc, false);
+                    row(y + 1, 0, d, kIdesc, false);
+                }
+                umma_commit(afull + b);
+                umma_commit(sempty + (y - 1 - rbase) % kSlots);  // rows y-1 and y: last read by this unit
+                umma_commit(sempty + (y - rbase) % kSlots);
+            }
+        }
+    } else {  // ---- epilogue warps 2..5
+        const int quad = warp & 3;
+        for (int t = 0; t < n_units; ++t) {
+            const int y = y0 + 2 * t, b = t & 1, ub = t >> 1;
+            const int nrows = y + 1 < y1 ? 2 : 1;
+            mbar_wait(afull + b, (uint32_t)(ub & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            for (int rr = 0; rr < nrows; ++rr) {
+                const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * 128 + rr * 64);
+                uint32_t r[64];
+                LD16(base + 0, (r + 0));
+                LD16(base + 16, (r + 16));
+                LD16(base + 32, (r + 32));
+                LD16(base + 48, (r + 48));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (rr == nrows - 1) {
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0)
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(aempty + b)) : "memory");
+                }
+                const int px = x0 + quad * 32 + lane;
+                if (px < W) {
+                    uint4* dst = reinterpret_cast<uint4*>(out) + ((size_t)(y + rr) * Wp + px);
+                    const size_t gstride = (size_t)H * Wp;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        uint32_t pk[4];
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            const float lo = fmaxf(__uint_as_float(r[8 * q + 2 * h]), 0.f);
+                            const float hi = fmaxf(__uint_as_float(r[8 * q + 2 * h + 1]), 0.f);
+                            const __nv_bfloat162 v2 = __floats2bfloat162_rn(lo, hi);
+                            pk[h] = *reinterpret_cast<const uint32_t*>(&v2);
+                        }
+                        dst[q * gstride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * 64) : "memory");
+}
+
 // layer 1: x (fp32, rounded to bf16) -> 64 ch, ReLU, bf16 blocked [8][H][W][8].  w1: [9 taps][64 oc] fp32
 __global__ void k_conv_first(const float* __restrict__ x, const float* __restrict__ w1, __nv_bfloat16* out, int H,
                              int W, int Wp)
@@ -430,6 +602,23 @@ void Cnn::set_weights(const uint16_t* bf16, int layers, int channels)
                 for (int t = 0; t < 9; ++t)
                     dst[(size_t)t * kC * kC + (ic / 8) * kC * 8 + oc * 8 + (ic % 8)] = src[(oc * kC + ic) * 9 + t];
     }
+    // row-pair layout: for each dx and ic-group, the three dy taps' [64 oc][8 ic] blocks side by side
+    // in the order dy2, dy1, dy0 (k_conv64_tc2)
+    std::vector<uint16_t> wm2(wm.size());
+    for (int l = 0; l < 15; ++l) {
+        const uint16_t* src = bf16 + n1 + l * nm;
+        uint16_t* dst = wm2.data() + (size_t)l * 9 * kC * kC;
+        for (int oc = 0; oc < kC; ++oc)
+            for (int ic = 0; ic < kC; ++ic)
+                for (int dy = 0; dy < 3; ++dy)
+                    for (int dx = 0; dx < 3; ++dx)
+                        dst[(size_t)dx * kW2Dx / 2 + (ic / 8) * kW2Icg / 2 + (2 - dy) * kC * 8 + oc * 8 + (ic % 8)] =
+                            src[(oc * kC + ic) * 9 + dy * 3 + dx];
+    }
+    w_mid2.alloc(wm2.size());
+    CKC(cudaMemcpy(w_mid2.p, wm2.data(), wm2.size() * 2, cudaMemcpyHostToDevice));
+    const char* ev = std::getenv("MACE_K5_PAIR");
+    pair = !(ev && ev[0] == '0');
     (void)n17;
     w_first.alloc(w1.size());
     w_last.alloc(w17.size());
@@ -453,6 +642,7 @@ void Cnn::ensure(int h, int w)
     map0 = make_act_map(act0.p, H, Wp);
     map1 = make_act_map(act1.p, H, Wp);
     CKC(cudaFuncSetAttribute(k_conv64_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    CKC(cudaFuncSetAttribute(k_conv64_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
 }
 
 void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int num_sms, int* launches)
@@ -481,8 +671,12 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
         cfg.stream = s;
         cfg.attrs = pdl;
         cfg.numAttrs = 1;
-        CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc, m, (const __nv_bfloat16*)(w_mid.p + (size_t)l * 9 * kC * kC), dst,
-                               H, W, Wp, per));
+        if (pair)
+            CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc2, m, (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC),
+                                   dst, H, W, Wp, per));
+        else
+            CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc, m, (const __nv_bfloat16*)(w_mid.p + (size_t)l * 9 * kC * kC),
+                                   dst, H, W, Wp, per));
     }
     // 15 middle layers: the last one wrote act1 (l = 14 even -> dst act1)
     {
