@@ -292,6 +292,12 @@ __device__ __forceinline__ void umma_i(uint32_t d_tmem, uint64_t a, uint64_t b, 
         : "memory");
 }
 
+constexpr uint32_t kIdesc192 =
+    (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(192 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+
+// R = 2 (row pairs) or 3 (row triples: the middle halo row feeds all three rows through one
+// N = 192 UMMA against [W_dy2 | W_dy1 | W_dy0]; 80 UMMAs per 3 rows)
+template <int R>
 __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ CUtensorMap amap,
                                                        const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* out,
                                                        int H, int W, int Wp, int rows_per_cta)
@@ -315,11 +321,12 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
     const int y0 = (blockIdx.x / strips) * rows_per_cta;
     const int y1 = min(H, y0 + rows_per_cta);
     if (y0 >= H) return;
-    const int n_units = (y1 - y0 + 1) / 2;  // pairs, the last one possibly a single row
+    const int n_units = (y1 - y0 + R - 1) / R;  // R-row units, the last one possibly shorter
+    constexpr int kAccCols = R == 2 ? 256 : 512;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(tmem_slot)),
-                     "n"(kAcc * 64)
+                     "n"(kAccCols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -358,15 +365,15 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
             const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
             mbar_wait(wbar, 0);
             for (int t = 0; t < n_units; ++t) {
-                const int y = y0 + 2 * t, b = t & 1, ub = t >> 1;
-                const bool pair = y + 1 < y1;
+                const int y = y0 + R * t, b = t & 1, ub = t >> 1;
+                const int nr = min(R, y1 - y);  // rows in this unit
                 if (ub >= 1) mbar_wait(aempty + b, (uint32_t)((ub - 1) & 1));
-                for (int r = y - 1; r <= y + (pair ? 2 : 1); ++r) {
+                for (int r = y - 1; r <= y + nr; ++r) {
                     const int q = r - rbase;
                     mbar_wait(sfull + q % kSlots, (uint32_t)((q / kSlots) & 1));
                 }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t d = tmem + (uint32_t)(b * 128);
+                const uint32_t d = tmem + (uint32_t)(b * R * 64);
                 // one halo row r against weight block blk (0 = dy2, 1 = dy1, 2 = dy0) with N = 64 or 128
                 auto row = [&](int r, int blk, uint32_t dcol, uint32_t idesc, bool first) {
                     const uint64_t a0 = sdesc(sl_base + ((r - rbase) % kSlots) * kSlotBytes, kHaloX * 16, 128);
@@ -380,7 +387,13 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
                             umma_i(dcol, a, bd, idesc, (first && dx == 0 && j == 0) ? 0u : 1u);
                         }
                 };
-                if (pair) {
+                if (nr == 3) {
+                    row(y + 1, 0, d, kIdesc192, true);      // [acc_y | acc_y+1 | acc_y+2] = A_y+1 [W_dy2 | W_dy1 | W_dy0]
+                    row(y, 1, d, kIdesc128, false);         // [acc_y | acc_y+1] += A_y [W_dy1 | W_dy0]
+                    row(y + 2, 0, d + 64, kIdesc128, false);  // [acc_y+1 | acc_y+2] += A_y+2 [W_dy2 | W_dy1]
+                    row(y - 1, 2, d, kIdesc, false);        // acc_y += A_y-1 W_dy0
+                    row(y + 3, 0, d + 128, kIdesc, false);  // acc_y+2 += A_y+3 W_dy2
+                } else if (nr == 2) {
                     row(y, 1, d, kIdesc128, true);          // [acc_y | acc_y+1] = A_y [W_dy1 | W_dy0]
                     row(y + 1, 0, d, kIdesc128, false);     // += A_y+1 [W_dy2 | W_dy1]
                     row(y - 1, 2, d, kIdesc, false);        // acc_y += A_y-1 W_dy0
@@ -391,19 +404,19 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
                     row(y + 1, 0, d, kIdesc, false);
                 }
                 umma_commit(afull + b);
-                umma_commit(sempty + (y - 1 - rbase) % kSlots);  // rows y-1 and y: last read by this unit
-                umma_commit(sempty + (y - rbase) % kSlots);
+                for (int r = y - 1; r < y - 1 + nr; ++r)  // rows y-1 .. y+nr-2: last read by this unit
+                    umma_commit(sempty + (r - rbase) % kSlots);
             }
         }
     } else {  // ---- epilogue warps 2..5
         const int quad = warp & 3;
         for (int t = 0; t < n_units; ++t) {
-            const int y = y0 + 2 * t, b = t & 1, ub = t >> 1;
-            const int nrows = y + 1 < y1 ? 2 : 1;
+            const int y = y0 + R * t, b = t & 1, ub = t >> 1;
+            const int nrows = min(R, y1 - y);
             mbar_wait(afull + b, (uint32_t)(ub & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             for (int rr = 0; rr < nrows; ++rr) {
-                const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * 128 + rr * 64);
+                const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * R * 64 + rr * 64);
                 uint32_t r[64];
                 LD16(base + 0, (r + 0));
                 LD16(base + 16, (r + 16));
@@ -439,7 +452,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * 64) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAccCols) : "memory");
 }
 
 // layer 1: x (fp32, rounded to bf16) -> 64 ch, ReLU, bf16 blocked [8][H][W][8].  w1: [9 taps][64 oc] fp32
@@ -617,8 +630,8 @@ void Cnn::set_weights(const uint16_t* bf16, int layers, int channels)
     }
     w_mid2.alloc(wm2.size());
     CKC(cudaMemcpy(w_mid2.p, wm2.data(), wm2.size() * 2, cudaMemcpyHostToDevice));
-    const char* ev = std::getenv("MACE_K5_PAIR");
-    pair = !(ev && ev[0] == '0');
+    const char* ev = std::getenv("MACE_K5_ROWS");  // output rows per MMA unit: 1, 2 or 3
+    rows_unit = ev ? std::max(1, std::min(3, std::atoi(ev))) : 2;
     (void)n17;
     w_first.alloc(w1.size());
     w_last.alloc(w17.size());
@@ -642,7 +655,8 @@ void Cnn::ensure(int h, int w)
     map0 = make_act_map(act0.p, H, Wp);
     map1 = make_act_map(act1.p, H, Wp);
     CKC(cudaFuncSetAttribute(k_conv64_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    CKC(cudaFuncSetAttribute(k_conv64_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    CKC(cudaFuncSetAttribute(k_conv64_tc2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    CKC(cudaFuncSetAttribute(k_conv64_tc2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
 }
 
 void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int num_sms, int* launches)
@@ -671,9 +685,12 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
         cfg.stream = s;
         cfg.attrs = pdl;
         cfg.numAttrs = 1;
-        if (pair)
-            CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc2, m, (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC),
-                                   dst, H, W, Wp, per));
+        if (rows_unit == 3)
+            CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc2<3>, m,
+                                   (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC), dst, H, W, Wp, per));
+        else if (rows_unit == 2)
+            CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc2<2>, m,
+                                   (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC), dst, H, W, Wp, per));
         else
             CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc, m, (const __nv_bfloat16*)(w_mid.p + (size_t)l * 9 * kC * kC),
                                    dst, H, W, Wp, per));

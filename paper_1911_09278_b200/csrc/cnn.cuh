@@ -36,7 +36,7 @@ struct Cnn {
     DevBuf<float> w_first, w_last;       // [9][64] fp32 holding bf16 values
     DevBuf<__nv_bfloat16> w_mid;         // [15][9 taps][8 ic-groups][64 oc][8 ic]
     DevBuf<__nv_bfloat16> w_mid2;        // row-pair layout: [15][3 dx][8 ic-groups][dy2 | dy1 | dy0][64 oc][8 ic]
-    bool pair = true;                    // row-pair layer kernel (MACE_K5_PAIR=0: one row per tile)
+    int rows_unit = 2;                   // output rows per MMA unit (k_conv64_tc2<2|3>; 1 = k_conv64_tc), MACE_K5_ROWS
     DevBuf<__nv_bfloat16> act0, act1;    // channel-blocked [8 groups][H][Wp][8 ch]
     CUtensorMap map0{}, map1{};
     // weights: 17 layers in PyTorch OIHW order, bf16 bits, concatenated
