@@ -456,13 +456,10 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
 }
 
 // layer 1: x (fp32, rounded to bf16) -> 64 ch, ReLU, bf16 blocked [8][H][W][8].  w1: [9 taps][64 oc] fp32
-__global__ void k_conv_first(const float* __restrict__ x, const float* __restrict__ w1, __nv_bfloat16* out, int H,
-                             int W, int Wp)
+__global__ void k_conv_first(const float* __restrict__ x, const __grid_constant__ ConvW9 w1, __nv_bfloat16* out,
+                             int H, int W, int Wp)
 {
-    __shared__ float ws[9 * kC];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    for (int i = threadIdx.x; i < 9 * kC; i += blockDim.x) ws[i] = w1[i];
-    __syncthreads();
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= H * W) return;
     const int yy = p / W, xx = p % W;
@@ -484,7 +481,7 @@ __global__ void k_conv_first(const float* __restrict__ x, const float* __restric
             for (int e = 0; e < 2; ++e) {
                 const int oc = 8 * q + 2 * h + e;
 #pragma unroll
-                for (int t = 0; t < 9; ++t) acc[e] = fmaf(in[t], ws[t * kC + oc], acc[e]);
+                for (int t = 0; t < 9; ++t) acc[e] = fmaf(in[t], w1.v[t * kC + oc], acc[e]);
             }
             const __nv_bfloat162 v2 = __floats2bfloat162_rn(fmaxf(acc[0], 0.f), fmaxf(acc[1], 0.f));
             pk[h] = *reinterpret_cast<const uint32_t*>(&v2);
@@ -498,15 +495,13 @@ __global__ void k_conv_first(const float* __restrict__ x, const float* __restric
 // loads, zero outside the image), then every pixel reads its 9 taps from there.
 constexpr int kLastT = 16;
 __global__ void __launch_bounds__(kLastT * kLastT) k_conv_last(const __nv_bfloat16* __restrict__ h,
-                                                                const float* __restrict__ w17,
+                                                                const __grid_constant__ ConvW9 w17,
                                                                 const float* __restrict__ x, float* out, int H, int W,
                                                                 int Wp)
 {
     constexpr int TT = kLastT + 2;
-    __shared__ float ws[9 * kC];
     __shared__ uint4 tile[8][TT][TT];  // [channel group][row][col], 41.5 KB
     const int tid = threadIdx.x;
-    for (int i = tid; i < 9 * kC; i += blockDim.x) ws[i] = w17[i];
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the last 64-channel layer
     const int bx = blockIdx.x * kLastT, by = blockIdx.y * kLastT;
     const size_t gstride = (size_t)H * Wp;
@@ -532,8 +527,8 @@ __global__ void __launch_bounds__(kLastT * kLastT) k_conv_last(const __nv_bfloat
             for (int e = 0; e < 4; ++e) {
                 const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&u[e]);
                 const float2 f = __bfloat1622float2(b2);
-                acc = fmaf(f.x, ws[t * kC + 8 * q + 2 * e], acc);
-                acc = fmaf(f.y, ws[t * kC + 8 * q + 2 * e + 1], acc);
+                acc = fmaf(f.x, w17.v[t * kC + 8 * q + 2 * e], acc);
+                acc = fmaf(f.y, w17.v[t * kC + 8 * q + 2 * e + 1], acc);
             }
         }
     }
@@ -599,12 +594,11 @@ void Cnn::set_weights(const uint16_t* bf16, int layers, int channels)
         std::memcpy(&v, &u, 4);
         return v;
     };
-    std::vector<float> w1(9 * kC), w17(9 * kC);
     for (int oc = 0; oc < kC; ++oc)
-        for (int t = 0; t < 9; ++t) w1[t * kC + oc] = f(bf16[oc * 9 + t]);
+        for (int t = 0; t < 9; ++t) w_first.v[t * kC + oc] = f(bf16[oc * 9 + t]);
     const uint16_t* wl = bf16 + n1 + 15 * nm;
     for (int ic = 0; ic < kC; ++ic)
-        for (int t = 0; t < 9; ++t) w17[t * kC + ic] = f(wl[ic * 9 + t]);
+        for (int t = 0; t < 9; ++t) w_last.v[t * kC + ic] = f(wl[ic * 9 + t]);
     // middle layers: [layer][tap][ic-group][oc][8 ic]
     std::vector<uint16_t> wm(15 * (size_t)9 * kC * kC);
     for (int l = 0; l < 15; ++l) {
@@ -633,11 +627,9 @@ void Cnn::set_weights(const uint16_t* bf16, int layers, int channels)
     const char* ev = std::getenv("MACE_K5_ROWS");  // output rows per MMA unit: 1, 2 or 3
     rows_unit = ev ? std::max(1, std::min(3, std::atoi(ev))) : 2;
     (void)n17;
-    w_first.alloc(w1.size());
-    w_last.alloc(w17.size());
+
     w_mid.alloc(wm.size());
-    CKC(cudaMemcpy(w_first.p, w1.data(), w1.size() * 4, cudaMemcpyHostToDevice));
-    CKC(cudaMemcpy(w_last.p, w17.data(), w17.size() * 4, cudaMemcpyHostToDevice));
+
     CKC(cudaMemcpy(w_mid.p, wm.data(), wm.size() * 2, cudaMemcpyHostToDevice));
     ready = true;
 }
@@ -664,7 +656,7 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
     if (!ready) throw std::runtime_error("denoiser weights not set");
     ensure(h, w);
     const int npx = H * W;
-    k_conv_first<<<(npx + 255) / 256, 256, 0, s>>>(x, w_first.p, act0.p, H, W, Wp);
+    k_conv_first<<<(npx + 255) / 256, 256, 0, s>>>(x, w_first, act0.p, H, W, Wp);
     // one CTA per (128-px strip, run of rows); one CTA per SM (140 KB smem)
     const int strips = (W + kTileX - 1) / kTileX;
     const int ctas_y = std::max(1, num_sms / strips);
@@ -703,7 +695,7 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
         cfg.stream = s;
         cfg.attrs = pdl;
         cfg.numAttrs = 1;
-        CKC(cudaLaunchKernelEx(&cfg, k_conv_last, (const __nv_bfloat16*)act1.p, (const float*)w_last.p, x, out, H, W,
+        CKC(cudaLaunchKernelEx(&cfg, k_conv_last, (const __nv_bfloat16*)act1.p, w_last, x, out, H, W,
                                Wp));
     }
     CKC(cudaGetLastError());

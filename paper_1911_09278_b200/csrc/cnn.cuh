@@ -30,10 +30,16 @@ struct DevBuf {
     }
 };
 
+// 3x3 weights of the 1-channel end layers, [tap 9][64] fp32 holding bf16 values; passed to the
+// kernels by value (__grid_constant__), so every FMA reads its weight straight from the constant bank
+struct ConvW9 {
+    float v[9 * 64];
+};
+
 struct Cnn {
     bool ready = false;
     int H = 0, W = 0, Wp = 0;  // Wp: activation row pitch (W rounded up to 8 pixels)
-    DevBuf<float> w_first, w_last;       // [9][64] fp32 holding bf16 values
+    ConvW9 w_first{}, w_last{};          // layers 1 and 17
     DevBuf<__nv_bfloat16> w_mid;         // [15][9 taps][8 ic-groups][64 oc][8 ic]
     DevBuf<__nv_bfloat16> w_mid2;        // row-pair layout: [15][3 dx][8 ic-groups][dy2 | dy1 | dy0][64 oc][8 ic]
     int rows_unit = 2;                   // output rows per MMA unit (k_conv64_tc2<2|3>; 1 = k_conv64_tc), MACE_K5_ROWS
