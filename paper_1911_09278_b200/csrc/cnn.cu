@@ -500,38 +500,42 @@ __global__ void __launch_bounds__(kLastT * kLastT) k_conv_last(const __nv_bfloat
                                                                 int Wp)
 {
     constexpr int TT = kLastT + 2;
-    __shared__ uint4 tile[8][TT][TT];  // [channel group][row][col], 41.5 KB
+    __shared__ uint4 tile[4][TT][TT];  // four channel groups at a time: 20.7 KB, so a wave holds the grid
     const int tid = threadIdx.x;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the last 64-channel layer
     const int bx = blockIdx.x * kLastT, by = blockIdx.y * kLastT;
     const size_t gstride = (size_t)H * Wp;
-    for (int i = tid; i < 8 * TT * TT; i += blockDim.x) {
-        const int g = i / (TT * TT), r = (i / TT) % TT, c = i % TT;
-        const int sy = by + r - 1, sx = bx + c - 1;
-        tile[g][r][c] = (sy >= 0 && sy < H && sx >= 0 && sx < W)
-                            ? __ldg(reinterpret_cast<const uint4*>(h) + g * gstride + (size_t)sy * Wp + sx)
-                            : make_uint4(0u, 0u, 0u, 0u);
-    }
-    __syncthreads();
     const int tx = tid % kLastT, ty = tid / kLastT;
     const int xx = bx + tx, yy = by + ty;
-    if (xx >= W || yy >= H) return;
     float acc = 0.f;
 #pragma unroll
-    for (int t = 0; t < 9; ++t) {
+    for (int half = 0; half < 2; ++half) {
+        if (half) __syncthreads();  // every read of the first half is done
+        for (int i = tid; i < 4 * TT * TT; i += blockDim.x) {
+            const int g = i / (TT * TT), r = (i / TT) % TT, c = i % TT;
+            const int sy = by + r - 1, sx = bx + c - 1;
+            tile[g][r][c] = (sy >= 0 && sy < H && sx >= 0 && sx < W)
+                                ? __ldg(reinterpret_cast<const uint4*>(h) + (4 * half + g) * gstride + (size_t)sy * Wp + sx)
+                                : make_uint4(0u, 0u, 0u, 0u);
+        }
+        __syncthreads();
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const uint4 v = tile[q][ty + t / 3][tx + t % 3];
-            const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+        for (int t = 0; t < 9; ++t) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&u[e]);
-                const float2 f = __bfloat1622float2(b2);
-                acc = fmaf(f.x, w17.v[t * kC + 8 * q + 2 * e], acc);
-                acc = fmaf(f.y, w17.v[t * kC + 8 * q + 2 * e + 1], acc);
+            for (int q = 0; q < 4; ++q) {
+                const uint4 v = tile[q][ty + t / 3][tx + t % 3];
+                const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&u[e]);
+                    const float2 f = __bfloat1622float2(b2);
+                    acc = fmaf(f.x, w17.v[t * kC + 8 * (4 * half + q) + 2 * e], acc);
+                    acc = fmaf(f.y, w17.v[t * kC + 8 * (4 * half + q) + 2 * e + 1], acc);
+                }
             }
         }
     }
+    if (xx >= W || yy >= H) return;
     const size_t p = (size_t)yy * W + xx;
     out[p] = x[p] - acc;
 }
