@@ -44,7 +44,7 @@ class AgentWorkspace:
 
     def __init__(self, problem, subset: ViewSubset, n_subsets: int, sigma: float | None,
                  beta: float | None = None, state: np.ndarray | None = None, clamp_nonneg: bool = False,
-                 schedule: str | None = None, device: int = 0):
+                 schedule: str | None = None, device: int = 0, sv_side: int | None = None):
         if sigma is not None and sigma <= 0:
             raise ValueError("sigma must be > 0")
         self.subset = subset
@@ -53,7 +53,9 @@ class AgentWorkspace:
         self.prior = problem.prior if beta is None else problem.prior.with_beta(beta)
         self.n = problem.geom.n_pixels
         self.schedule = schedule or _default_schedule(self.n)
-        self.plan = AgentPlan(problem.matrices, [tuple(subset.view_indices)], schedule=self.schedule, device=device)
+        kw = {} if sv_side is None else {"sv": int(sv_side)}  # super-voxel tile side (GPU knob)
+        self.plan = AgentPlan(problem.matrices, [tuple(subset.view_indices)], schedule=self.schedule, device=device,
+                              **kw)
         self.plan.load_data(problem.y, problem.weights)
         self.plan.set_prior(self.prior)
         self.beta_eff = self.prior.beta / n_subsets  # icd.py:198

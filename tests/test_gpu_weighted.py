@@ -107,3 +107,27 @@ def test_zero_weight_falls_back_to_plain_records(monkeypatch):
     za = mb.prox_solve(a, v, tol=1e-7, max_passes=3000)
     zb = mb.prox_solve(b, v, tol=1e-7, max_passes=3000)
     assert rel(za, zb) < 1e-4
+
+
+@pytest.mark.parametrize("sv_side", [2, 4, 6, 12, 16])
+@pytest.mark.parametrize("weighted", [True, False])
+def test_every_tile_side_reaches_the_raster_prox_point(sv_side, weighted, monkeypatch):
+    """Every compiled tile side (k2_inst.cu units), with weighted and plain records: the parallel pass
+    converges to the proximal point the reference-order raster pass reaches (icd.py:286-303).
+    Sides 2 and 6 have parity classes that are not a multiple of four pixels (padding slots);
+    a 30 x 30 image makes every side leave partial edge tiles."""
+    monkeypatch.setenv("MACE_WEIGHTED", "1" if weighted else "0")
+    ns, nv, nc = 30, 36, 33
+    geom = mb.Geometry(ns, 1.0, nv, nc, 1.0)
+    rng = np.random.default_rng(40 + sv_side)
+    y = rng.standard_normal((nv, nc))
+    w = 0.5 + rng.random((nv, nc))
+    prob = mb.ReconProblem(geom, mb.build_system_matrix(geom), y, w, mb.PriorParams("qggmrf", 0.5, 2.0, 1.2, 1.0, 1.0))
+    sub = mb.partition_views(nv, 3)[1]
+    a = mb.AgentWorkspace(prob, sub, 3, sigma=0.5, schedule="raster")
+    b = mb.AgentWorkspace(prob, sub, 3, sigma=0.5, schedule="sv", sv_side=sv_side)
+    assert b.plan.info()["S"] == sv_side and b.plan.info()["weighted"] == int(weighted)
+    v = rng.standard_normal(a.n)
+    za = mb.prox_solve(a, v, tol=1e-7, max_passes=3000)
+    zb = mb.prox_solve(b, v, tol=1e-7, max_passes=3000)
+    assert rel(zb, za) < 1e-4
