@@ -314,6 +314,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kAcc);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) K5T(0);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int strips = (W + kTileX - 1) / kTileX;
     const int strip = blockIdx.x % strips;
@@ -364,6 +365,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
         if (lane == 0) {  // ---- MMA issuer
             const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
             mbar_wait(wbar, 0);
+            K5T(1);
             for (int t = 0; t < n_units; ++t) {
                 const int y = y0 + R * t, b = t & 1, ub = t >> 1;
                 const int nr = min(R, y1 - y);  // rows in this unit
@@ -404,6 +406,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
                     row(y + 1, 0, d, kIdesc, false);
                 }
                 umma_commit(afull + b);
+                if (t < 14) K5T(2 + 2 * t);
                 for (int r = y - 1; r < y - 1 + nr; ++r)  // rows y-1 .. y+nr-2: last read by this unit
                     umma_commit(sempty + (r - rbase) % kSlots);
             }
@@ -430,6 +433,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
                         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(aempty + b)) : "memory");
                 }
                 const int px = x0 + quad * 32 + lane;
+                if (rr == 0 && warp == 2 && lane == 0 && t < 14) K5T(3 + 2 * t);  // accumulators read
                 if (px < W) {
                     uint4* dst = reinterpret_cast<uint4*>(out) + ((size_t)(y + rr) * Wp + px);
                     const size_t gstride = (size_t)H * Wp;

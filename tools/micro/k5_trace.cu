@@ -23,7 +23,7 @@ int main()
     for (int c : {0, 1, 73, 147}) {
         long long t0 = t[c][0];
         printf("cta %3d: weights %lld |", c, t[c][1] - t0);
-        for (int k = 0; k < 14; ++k) printf(" mma%d %lld epi %lld", k, t[c][2 + 2 * k] - t0, t[c][3 + 2 * k] - t0);
+        for (int k = 0; k < 14; ++k) printf(" mma%d %lld epi %lld", k, t[c][2 + 2 * k] - t0, t[c][3 + 2 * k] - t0);  // units (pairs by default)
         printf("\n   tma issue:");
         for (int q = 0; q < 16; ++q) printf(" %lld", t[c][32 + q] - t0);
         printf("\n   row landed:");

@@ -49,6 +49,17 @@ __global__ void __launch_bounds__(128, 1) k(int iters, long long* out)
                     const uint64_t bu = b + (uint64_t)((u * 256) >> 4);
                     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem), "l"(au), "l"(bu), "r"(idesc));
                 }
+            } else if (MODE == 4) {  // K5 row-pair unit pattern: 2 x 12 N=128 then 2 x 12 N=64 (D at +0 / +64)
+                constexpr uint32_t i128 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+                constexpr uint32_t i64 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+#pragma unroll
+                for (int u = 0; u < 48; ++u) {
+                    const uint32_t id = u < 24 ? i128 : i64;
+                    const uint32_t dd = tmem + (u >= 36 ? 64u : 0u);
+                    const uint64_t au = a + (uint64_t)((((u % 3) * 16) + ((u / 3) % 4) * 256) >> 4);
+                    const uint64_t bu = b + (uint64_t)(((u % 12) * 256) >> 4);
+                    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dd), "l"(au), "l"(bu), "r"(id));
+                }
             } else {
                 asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::1.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem), "l"(a), "l"(b), "r"(idesc));
 #pragma unroll
@@ -88,9 +99,9 @@ void run(int sms)
     cudaEventElapsedTime(&ms, e0, e1);
     long long cyc;
     cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
-    const double mmas = (double)iters * 8;
-    const double flop = 2.0 * 128 * N * 16 * mmas * sms;
-    printf("N=%3d mode=%d: %.1f cycles/MMA, %.0f TFLOP/s (err %s)\n", N, MODE, cyc / mmas, flop / (ms * 1e-3) / 1e12,
+    const double mmas = (double)iters * (MODE == 4 ? 48 : 8);
+    const double flop = MODE == 4 ? 2.0 * 128 * 16 * (24 * 128 + 24 * 64) * iters * sms : 2.0 * 128 * N * 16 * mmas * sms;
+    printf("N=%3d mode=%d: %.1f cycles/MMA (%.0f per 48), %.0f TFLOP/s (err %s)\n", N, MODE, cyc / mmas, cyc / mmas * 48, flop / (ms * 1e-3) / 1e12,
            cudaGetErrorString(cudaGetLastError()));
     cudaFree(d);
 }
@@ -99,6 +110,7 @@ int main()
 {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    run<64, 4>(sms);
     run<64, 0>(sms);
     run<64, 1>(sms);
     run<64, 2>(sms);
