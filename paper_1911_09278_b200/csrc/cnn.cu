@@ -36,7 +36,7 @@ constexpr int kTileX = 128;        // output pixels per tile (one row segment)
 // the 3x3 window spans pixels x0 - 1 .. x0 + 128, i.e. slot pixels 7 .. 136)
 constexpr int kHaloX = kTileX + 16;  // 144
 constexpr int kHaloOff = 7;         // pixel of the slot that holds x0 - 1
-constexpr int kSlots = 6;          // ring of halo rows (TMA runs up to 3 rows ahead)
+constexpr int kSlots = 8;          // ring of halo rows (row pairs consume two per unit: 8 keeps TMA a unit ahead)
 constexpr int kAcc = 4;            // TMEM accumulators (4 x 64 fp32 columns)
 constexpr int kSlotBytes = 8 * kHaloX * 16;         // 18,432
 constexpr int kWBytes = 9 * kC * kC * 2;            // 73,728
@@ -92,18 +92,23 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 // instruction descriptor: D f32, A/B bf16, both K-major, N = 64, M = 128
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 
-__device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate)
+// Warp-wide forms: the whole issuer warp runs the loop (so descriptor arithmetic stays in uniform
+// registers) and one elected lane issues; issuing from a single divergent lane made every
+// descriptor cross from the vector to the uniform register file (R2UR) in front of each UMMA.
+__device__ __forceinline__ void umma_e(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate)
 {
     asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate)
+        "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
         : "memory");
 }
-__device__ __forceinline__ void umma_commit(uint64_t* bar)
+__device__ __forceinline__ void umma_commit_e(uint64_t* bar)
 {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s_u32(bar))
-                 : "memory");
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(s_u32(bar))
+        : "memory");
 }
 
 #define LD16(base, r)                                                                                             \
@@ -192,17 +197,17 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer
+        {  // ---- MMA issuer (whole warp, one elected lane issues)
             const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
             mbar_wait(wbar, 0);
-            K5T(1);
+            if (lane == 0) K5T(1);
             for (int y = y0; y < y1; ++y) {
                 const int t = y - y0, b = t % kAcc, ub = t / kAcc;
                 if (ub >= 1) mbar_wait(aempty + b, (uint32_t)((ub - 1) & 1));
                 for (int r = y - 1; r <= y + 1; ++r) {
                     const int q = r - rbase;
                     mbar_wait(sfull + q % kSlots, (uint32_t)((q / kSlots) & 1));
-                    if (r == y + 1 && q < 16) K5T(48 + q);  // ring row q landed (as seen by the MMA issuer)
+                    if (lane == 0 && r == y + 1 && q < 16) K5T(48 + q);  // ring row q landed (as seen by the MMA issuer)
                 }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t d = tmem + (uint32_t)(b * 64);
@@ -218,13 +223,13 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CU
                         for (int j = 0; j < 4; ++j) {
                             const uint64_t a = a0 + (uint64_t)(((kHaloOff + dx) * 16 + 2 * j * (kHaloX * 16)) >> 4);
                             const uint64_t bd = b0 + (uint64_t)(((dy * 3 + dx) * (kC * kC * 2) + 2 * j * (kC * 16)) >> 4);
-                            umma(d, a, bd, (dy | dx | j) != 0);
+                            umma_e(d, a, bd, kIdesc, (dy | dx | j) != 0);
                         }
                     }
                 }
-                umma_commit(afull + b);
-                umma_commit(sempty + (y - 1 - rbase) % kSlots);  // row y-1: last reader was tile y
-                K5T(2 + 2 * t);
+                umma_commit_e(afull + b);
+                umma_commit_e(sempty + (y - 1 - rbase) % kSlots);  // row y-1: last reader was tile y
+                if (lane == 0) K5T(2 + 2 * t);
             }
         }
     } else {  // ---- epilogue warps 2..5
@@ -283,17 +288,35 @@ constexpr uint32_t kIdesc128 =
 constexpr int kW2Dx = 8 * 3 * kC * 16;  // 24,576 B per dx: [icg 8][192 oc][8 ic]
 constexpr int kW2Icg = 3 * kC * 16;     // 3,072 B per ic-group
 
-__device__ __forceinline__ void umma_i(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate)
-{
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
 
 constexpr uint32_t kIdesc192 =
     (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(192 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+
+// One halo row's 12 UMMAs (3 dx shifts x 4 K-steps) from one elected lane in a single asm block:
+// the descriptors step by compile-time offsets (A: dx + 2 j x 144 px rows, B: dx x 24,576 B + 2 j x
+// 3,072 B, all >> 4), so only the two base descriptors cross into uniform registers per row.
+__device__ __forceinline__ void umma_row12(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc, uint32_t accumulate)
+{
+    static_assert(kHaloX == 144 && kW2Dx == 24576 && kW2Icg == 3072, "offsets below are hard-coded");
+    asm volatile(
+        "{\n.reg .pred e, p, t;\n.reg .b64 a, b;\n"
+        "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\nsetp.eq.b32 t, 1, 1;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "add.s64 a, %1, 288;\nadd.s64 b, %2, 384;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 576;\nadd.s64 b, %2, 768;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 864;\nadd.s64 b, %2, 1152;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 1;\nadd.s64 b, %2, 1536;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 289;\nadd.s64 b, %2, 1920;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 577;\nadd.s64 b, %2, 2304;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 865;\nadd.s64 b, %2, 2688;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 2;\nadd.s64 b, %2, 3072;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 290;\nadd.s64 b, %2, 3456;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 578;\nadd.s64 b, %2, 3840;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 866;\nadd.s64 b, %2, 4224;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "}\n"
+        ::"r"(d_tmem), "l"(a0), "l"(b0), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 
 // R = 2 (row pairs) or 3 (row triples: the middle halo row feeds all three rows through one
 // N = 192 UMMA against [W_dy2 | W_dy1 | W_dy0]; 80 UMMAs per 3 rows)
@@ -362,10 +385,10 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer
+        {  // ---- MMA issuer (whole warp, one elected lane issues)
             const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
             mbar_wait(wbar, 0);
-            K5T(1);
+            if (lane == 0) K5T(1);
             for (int t = 0; t < n_units; ++t) {
                 const int y = y0 + R * t, b = t & 1, ub = t >> 1;
                 const int nr = min(R, y1 - y);  // rows in this unit
@@ -378,16 +401,10 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
                 const uint32_t d = tmem + (uint32_t)(b * R * 64);
                 // one halo row r against weight block blk (0 = dy2, 1 = dy1, 2 = dy0) with N = 64 or 128
                 auto row = [&](int r, int blk, uint32_t dcol, uint32_t idesc, bool first) {
-                    const uint64_t a0 = sdesc(sl_base + ((r - rbase) % kSlots) * kSlotBytes, kHaloX * 16, 128);
+                    const uint64_t a0 = sdesc(sl_base + ((r - rbase) % kSlots) * kSlotBytes + kHaloOff * 16,
+                                              kHaloX * 16, 128);
                     const uint64_t b0 = sdesc(sw_base + blk * kC * 16, kW2Icg, 128);
-#pragma unroll
-                    for (int dx = 0; dx < 3; ++dx)
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const uint64_t a = a0 + (uint64_t)(((kHaloOff + dx) * 16 + 2 * j * (kHaloX * 16)) >> 4);
-                            const uint64_t bd = b0 + (uint64_t)((dx * kW2Dx + 2 * j * kW2Icg) >> 4);
-                            umma_i(dcol, a, bd, idesc, (first && dx == 0 && j == 0) ? 0u : 1u);
-                        }
+                    umma_row12(dcol, a0, b0, idesc, first ? 0u : 1u);
                 };
                 if (nr == 3) {
                     row(y + 1, 0, d, kIdesc192, true);      // [acc_y | acc_y+1 | acc_y+2] = A_y+1 [W_dy2 | W_dy1 | W_dy0]
@@ -405,10 +422,10 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
                     row(y, 1, d, kIdesc, false);
                     row(y + 1, 0, d, kIdesc, false);
                 }
-                umma_commit(afull + b);
-                if (t < 14) K5T(2 + 2 * t);
+                umma_commit_e(afull + b);
+                if (lane == 0 && t < 14) K5T(2 + 2 * t);
                 for (int r = y - 1; r < y - 1 + nr; ++r)  // rows y-1 .. y+nr-2: last read by this unit
-                    umma_commit(sempty + (r - rbase) % kSlots);
+                    umma_commit_e(sempty + (r - rbase) % kSlots);
             }
         }
     } else {  // ---- epilogue warps 2..5
@@ -434,7 +451,11 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
                 }
                 const int px = x0 + quad * 32 + lane;
                 if (rr == 0 && warp == 2 && lane == 0 && t < 14) K5T(3 + 2 * t);  // accumulators read
+#ifdef K5_NO_STORE  // timing experiment only: skip the activation stores
+                if (px < 0) {
+#else
                 if (px < W) {
+#endif
                     uint4* dst = reinterpret_cast<uint4*>(out) + ((size_t)(y + rr) * Wp + px);
                     const size_t gstride = (size_t)H * Wp;
 #pragma unroll
