@@ -389,18 +389,27 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
             const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
             mbar_wait(wbar, 0);
             if (lane == 0) K5T(1);
+            int landed = y0 - 2;  // halo rows <= landed are known to be in shared memory
             for (int t = 0; t < n_units; ++t) {
                 const int y = y0 + R * t, b = t & 1, ub = t >> 1;
                 const int nr = min(R, y1 - y);  // rows in this unit
-                if (ub >= 1) mbar_wait(aempty + b, (uint32_t)((ub - 1) & 1));
-                for (int r = y - 1; r <= y + nr; ++r) {
-                    const int q = r - rbase;
-                    mbar_wait(sfull + q % kSlots, (uint32_t)((q / kSlots) & 1));
+                if (ub >= 1) {
+                    mbar_wait(aempty + b, (uint32_t)((ub - 1) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 }
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t d = tmem + (uint32_t)(b * R * 64);
                 // one halo row r against weight block blk (0 = dy2, 1 = dy1, 2 = dy0) with N = 64 or 128
                 auto row = [&](int r, int blk, uint32_t dcol, uint32_t idesc, bool first) {
+                    // wait for halo rows just before their first UMMAs, so the UMMAs already queued keep
+                    // the tensor pipe busy meanwhile (rows y+1.. of a unit were waited for by the last one)
+                    if (r > landed) {
+                        while (landed < r) {
+                            ++landed;
+                            const int q = landed - rbase;
+                            mbar_wait(sfull + q % kSlots, (uint32_t)((q / kSlots) & 1));
+                        }
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    }
                     const uint64_t a0 = sdesc(sl_base + ((r - rbase) % kSlots) * kSlotBytes + kHaloOff * 16,
                                               kHaloX * 16, 128);
                     const uint64_t b0 = sdesc(sw_base + blk * kC * 16, kW2Icg, 128);
