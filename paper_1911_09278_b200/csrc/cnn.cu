@@ -490,6 +490,17 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
 }
 
 // layer 1: x (fp32, rounded to bf16) -> 64 ch, ReLU, bf16 blocked [8][H][W][8].  w1: [9 taps][64 oc] fp32
+// packed fp32 FMA (sm_100 FFMA2): {a.x * b.x + c.x, a.y * b.y + c.y}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c)
+{
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+          "l"(*reinterpret_cast<unsigned long long*>(&c)));
+    return *reinterpret_cast<float2*>(&r);
+}
+
 __global__ void k_conv_first(const float* __restrict__ x, const __grid_constant__ ConvW9 w1, __nv_bfloat16* out,
                              int H, int W, int Wp)
 {
@@ -510,14 +521,13 @@ __global__ void k_conv_first(const float* __restrict__ x, const __grid_constant_
         uint32_t pk[4];
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-            float acc[2] = {0.f, 0.f};
+            // output channels oc, oc + 1 as one packed pair (FFMA2): same products and order as two FMAs
+            const int oc = 8 * q + 2 * h;
+            float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int oc = 8 * q + 2 * h + e;
-#pragma unroll
-                for (int t = 0; t < 9; ++t) acc[e] = fmaf(in[t], w1.v[t * kC + oc], acc[e]);
-            }
-            const __nv_bfloat162 v2 = __floats2bfloat162_rn(fmaxf(acc[0], 0.f), fmaxf(acc[1], 0.f));
+            for (int t = 0; t < 9; ++t)
+                acc = ffma2(make_float2(in[t], in[t]), make_float2(w1.v[t * kC + oc], w1.v[t * kC + oc + 1]), acc);
+            const __nv_bfloat162 v2 = __floats2bfloat162_rn(fmaxf(acc.x, 0.f), fmaxf(acc.y, 0.f));
             pk[h] = *reinterpret_cast<const uint32_t*>(&v2);
         }
         dst[q * gstride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -541,7 +551,7 @@ __global__ void __launch_bounds__(kLastT * kLastT) k_conv_last(const __nv_bfloat
     const size_t gstride = (size_t)H * Wp;
     const int tx = tid % kLastT, ty = tid / kLastT;
     const int xx = bx + tx, yy = by + ty;
-    float acc = 0.f;
+    float2 acc2 = make_float2(0.f, 0.f);  // even / odd channels
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
         if (half) __syncthreads();  // every read of the first half is done
@@ -560,18 +570,17 @@ __global__ void __launch_bounds__(kLastT * kLastT) k_conv_last(const __nv_bfloat
                 const uint4 v = tile[q][ty + t / 3][tx + t % 3];
                 const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&u[e]);
-                    const float2 f = __bfloat1622float2(b2);
-                    acc = fmaf(f.x, w17.v[t * kC + 8 * (4 * half + q) + 2 * e], acc);
-                    acc = fmaf(f.y, w17.v[t * kC + 8 * (4 * half + q) + 2 * e + 1], acc);
+                for (int e = 0; e < 4; ++e) {  // bf16 pair -> fp32 pair by shifts, one FFMA2 per pair
+                    const float2 f = make_float2(__uint_as_float(u[e] << 16), __uint_as_float(u[e] & 0xffff0000u));
+                    const int c = t * kC + 8 * (4 * half + q) + 2 * e;
+                    acc2 = ffma2(f, make_float2(w17.v[c], w17.v[c + 1]), acc2);
                 }
             }
         }
     }
     if (xx >= W || yy >= H) return;
     const size_t p = (size_t)yy * W + xx;
-    out[p] = x[p] - acc;
+    out[p] = x[p] - (acc2.x + acc2.y);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
