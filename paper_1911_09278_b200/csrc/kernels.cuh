@@ -334,44 +334,22 @@ __global__ void k_theta2_raster(const AgentDev* agents, int n_agents, int n)
     }
 }
 
-// Super-voxel batch constants from the lane-per-view layout (one warp per (agent, tile) item):
-// theta2_p = sum a_p^2 lambda (icd.py:193-195) for the kSvBatch slots of each batch, and the
-// cross terms c_ij = sum_r a_ir a_jr lambda_r that couple two pixels of a batch through shared
-// rows (k_sv.cuh).  Depends on lambda only, so it is recomputed per data load.
-template <int K, int NG, bool kW>
-__global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n_items, const uint32_t* queue,
-                                                   int n_side, int S, int nb, int W)
+// Super-voxel batch constants from the lane-per-view layout: theta2_p = sum a_p^2 lambda
+// (icd.py:193-195) for the kSvBatch slots of each batch, and the cross terms
+// c_ij = sum_r a_ir a_jr lambda_r that couple two pixels of a batch through shared rows (k_sv.cuh).
+// Depends on lambda only, so it is recomputed per data load.
+//
+// One 128-thread block per (agent, tile) item.  The tile's lambda band window (the rows its views
+// touch, [g][o][32] as in K2's shared-memory plane) is staged once in shared memory, so the
+// per-record lambda reads are bank-conflict-free shared loads instead of one scattered L2 sector
+// per (lane, record); each warp then streams the slot records of every 4th batch, the next
+// batch's records in flight while the current one is reduced.  Weighted contexts (kW) write the
+// records back as a sqrt(lambda); plain ones copy the window out as the lambda band K2 stages.
+template <int K, int NG>
+__device__ __forceinline__ void sv_load_recs(const uint32_t* __restrict__ rb, int lane, float (&a)[4][NG][K],
+                                             uint32_t (&ow)[4])
 {
-    const int lane = threadIdx.x & 31;
-    const long n_tasks = (long)n_items * nb;
-    // one warp per (item, batch) task, grid-stride over a persistent grid
-    for (long task = (long)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); task < n_tasks;
-         task += (long)((gridDim.x * blockDim.x) >> 5)) {
-    const int item = (int)(task / nb), b = (int)(task % nb);
-    const int h = S / 2, per_class = h * h, bpc = (per_class + 3) / 4;
-    const int recw = NG * 32 * K + 32;
-    const uint32_t code = queue[item];
-    const AgentDev& A = agents[code >> kAgentShift];
-    const int sv = (int)(code & kSvMask);
-    const int r0 = (sv / A.n_sv_side) * S, c0 = (sv % A.n_sv_side) * S;
-    const int2* bt = A.band + (size_t)sv * A.V;
-    int start[NG];
-#pragma unroll
-    for (int g = 0; g < NG; ++g) {
-        const int j = 32 * g + lane;
-        const int2 bj = j < A.V ? bt[j] : make_int2(0, 0);
-        start[g] = bj.x;
-        if (!kW && b == 0) {  // the band's lambda rows, laid out as the kernel's shared-memory plane
-            float* lb = A.lb + (((size_t)sv * NG + g) * W) * 32 + lane;
-            for (int o = 0; o < W; ++o) lb[o * 32] = o < bj.y ? A.lam[bj.x + o] : 0.f;
-        }
-    }
-    const uint32_t* __restrict__ rb = A.rec0 + ((size_t)sv * nb + b) * 4 * recw;
-    uint32_t* __restrict__ wb = kW ? A.recw + ((size_t)sv * nb + b) * 4 * recw : nullptr;
-    // all loads first (records, then the lambda rows they touch), then the weighted records and
-    // the sums: no store sits between two loads, so the loads of a task overlap
-    uint32_t ow[4];
-    float a[4][NG][K], l[4][NG][K];
+    constexpr int recw = NG * 32 * K + 32;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         const uint32_t* r = rb + (size_t)p * recw;
@@ -395,76 +373,129 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
             }
         }
     }
+}
+
+template <int K, int NG, bool kW>
+__global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n_items, const uint32_t* queue,
+                                                   int n_side, int S, int nb, int W)
+{
+    extern __shared__ float s_lam[];  // [NG][W][32]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int item = blockIdx.x;
+    if (item >= n_items) return;
+    const int h = S / 2, per_class = h * h, bpc = (per_class + 3) / 4;
+    constexpr int recw = NG * 32 * K + 32;
+    const uint32_t code = queue[item];
+    const AgentDev& A = agents[code >> kAgentShift];
+    const int sv = (int)(code & kSvMask);
+    const int r0 = (sv / A.n_sv_side) * S, c0 = (sv % A.n_sv_side) * S;
+    const uint32_t* __restrict__ rbase = A.rec0 + (size_t)sv * nb * 4 * recw;
+    uint32_t* __restrict__ wbase = kW ? A.recw + (size_t)sv * nb * 4 * recw : nullptr;
+
+    // first batch's records in flight while the window is staged
+    float a[4][NG][K];
+    uint32_t ow[4];
+    if (warp < nb) sv_load_recs<K, NG>(rbase + (size_t)warp * 4 * recw, lane, a, ow);
+
+    const int2* bt = A.band + (size_t)sv * A.V;
+    for (int g = warp; g < NG; g += 4) {
+        const int j = 32 * g + lane;
+        const int2 bj = j < A.V ? bt[j] : make_int2(0, 0);
+        float* sl = s_lam + (size_t)g * W * 32 + lane;
+#pragma unroll 8
+        for (int o = 0; o < W; ++o) sl[o * 32] = o < bj.y ? A.lam[bj.x + o] : 0.f;
+    }
+    __syncthreads();
+    if (!kW) {  // the band's lambda rows, laid out as the K2 shared-memory plane
+        float* lb = A.lb + (size_t)sv * NG * W * 32;
+        for (int i = threadIdx.x; i < NG * W * 32; i += blockDim.x) lb[i] = s_lam[i];
+    }
+
+    for (int b = warp; b < nb; b += 4) {
+        float an[4][NG][K];
+        uint32_t own[4];
+        if (b + 4 < nb) sv_load_recs<K, NG>(rbase + (size_t)(b + 4) * 4 * recw, lane, an, own);
+        float l[4][NG][K];
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int g = 0; g < NG; ++g)
-#pragma unroll
-            for (int q = 0; q < K; ++q)
-                l[p][g][q] = a[p][g][q] != 0.f ? __ldg(A.lam + start[g] + (int)((ow[p] >> (8 * g)) & 0xffu) + q) : 0.f;
-    if (kW) {  // weighted record a sqrt(lambda): theta2 and the cross terms are its plain products
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            uint32_t* w = wb + (size_t)p * recw;
-            __stcs(w + NG * 32 * K + lane, ow[p]);
+        for (int p = 0; p < 4; ++p)
 #pragma unroll
             for (int g = 0; g < NG; ++g) {
+                const float* sl = s_lam + ((size_t)g * W + ((ow[p] >> (8 * g)) & 0xffu)) * 32 + lane;
 #pragma unroll
-                for (int q = 0; q < K; ++q) {
-                    a[p][g][q] *= sqrtf(l[p][g][q]);
-                    l[p][g][q] = 1.f;
-                }
-                uint32_t* wq = w + (g * 32 + lane) * K;
-                if constexpr (K == 2) {
-                    __stcs(reinterpret_cast<uint2*>(wq), make_uint2(__float_as_uint(a[p][g][0]), __float_as_uint(a[p][g][1])));
-                } else if constexpr (K == 4) {
-                    __stcs(reinterpret_cast<uint4*>(wq), make_uint4(__float_as_uint(a[p][g][0]), __float_as_uint(a[p][g][1]),
-                                                                    __float_as_uint(a[p][g][2]), __float_as_uint(a[p][g][3])));
-                } else {
+                for (int q = 0; q < K; ++q) l[p][g][q] = a[p][g][q] != 0.f ? sl[q * 32] : 0.f;
+            }
+        if (kW) {  // weighted record a sqrt(lambda): theta2 and the cross terms are its plain products
+            uint32_t* wb = wbase + (size_t)b * 4 * recw;
 #pragma unroll
-                    for (int q = 0; q < K; ++q) __stcs(wq + q, __float_as_uint(a[p][g][q]));
+            for (int p = 0; p < 4; ++p) {
+                uint32_t* w = wb + (size_t)p * recw;
+                __stcs(w + NG * 32 * K + lane, ow[p]);
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+#pragma unroll
+                    for (int q = 0; q < K; ++q) {
+                        a[p][g][q] *= sqrtf(l[p][g][q]);
+                        l[p][g][q] = 1.f;
+                    }
+                    uint32_t* wq = w + (g * 32 + lane) * K;
+                    if constexpr (K == 2) {
+                        __stcs(reinterpret_cast<uint2*>(wq), make_uint2(__float_as_uint(a[p][g][0]), __float_as_uint(a[p][g][1])));
+                    } else if constexpr (K == 4) {
+                        __stcs(reinterpret_cast<uint4*>(wq), make_uint4(__float_as_uint(a[p][g][0]), __float_as_uint(a[p][g][1]),
+                                                                        __float_as_uint(a[p][g][2]), __float_as_uint(a[p][g][3])));
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < K; ++q) __stcs(wq + q, __float_as_uint(a[p][g][q]));
+                    }
                 }
             }
         }
-    }
-    float t2[4] = {0.f, 0.f, 0.f, 0.f}, cx[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        float t2[4] = {0.f, 0.f, 0.f, 0.f}, cx[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int g = 0; g < NG; ++g) {
-        int o[4];
+        for (int g = 0; g < NG; ++g) {
+            int o[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                o[p] = (int)((ow[p] >> (8 * g)) & 0xffu);
+#pragma unroll
+                for (int q = 0; q < K; ++q) t2[p] = fmaf(a[p][g][q] * a[p][g][q], l[p][g][q], t2[p]);
+            }
+            int x = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = i + 1; j < 4; ++j, ++x)
+#pragma unroll
+                    for (int q = 0; q < K; ++q)
+#pragma unroll
+                        for (int qj = 0; qj < K; ++qj)  // row o_i + q of pixel i is row o_j + qj of pixel j
+                            if (o[i] + q == o[j] + qj) cx[x] = fmaf(a[i][g][q] * a[j][g][qj], l[i][g][q], cx[x]);
+        }
+#pragma unroll
+        for (int p = 0; p < 4; ++p) t2[p] = warp_sum(t2[p]);
+#pragma unroll
+        for (int x = 0; x < 6; ++x) cx[x] = warp_sum(cx[x]);
+        float v = 0.f;
+#pragma unroll
+        for (int k = 0; k < 10; ++k)
+            if (lane == k) v = k < 4 ? t2[k & 3] : cx[(k - 4) % 6];
+        if (lane < 16) A.bc[((size_t)sv * nb + b) * 16 + lane] = v;
+        if (lane < 4) {  // theta2 image (cost kernels, diagnostics)
+            const int i = (b % bpc) * 4 + lane, cls = b / bpc;
+            if (i < per_class) {
+                const int lr = (cls >> 1) + 2 * (i / h), lc = (cls & 1) + 2 * (i % h);
+                if (r0 + lr < n_side && c0 + lc < n_side) A.th[(size_t)(r0 + lr) * n_side + c0 + lc] = v;
+            }
+        }
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            o[p] = (int)((ow[p] >> (8 * g)) & 0xffu);
+            ow[p] = own[p];
 #pragma unroll
-            for (int q = 0; q < K; ++q) t2[p] = fmaf(a[p][g][q] * a[p][g][q], l[p][g][q], t2[p]);
-        }
-        int x = 0;
+            for (int g = 0; g < NG; ++g)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = i + 1; j < 4; ++j, ++x)
-#pragma unroll
-                for (int q = 0; q < K; ++q)
-#pragma unroll
-                    for (int qj = 0; qj < K; ++qj)  // row o_i + q of pixel i is row o_j + qj of pixel j
-                        if (o[i] + q == o[j] + qj) cx[x] = fmaf(a[i][g][q] * a[j][g][qj], l[i][g][q], cx[x]);
-    }
-#pragma unroll
-    for (int p = 0; p < 4; ++p) t2[p] = warp_sum(t2[p]);
-#pragma unroll
-    for (int x = 0; x < 6; ++x) cx[x] = warp_sum(cx[x]);
-    float v = 0.f;
-#pragma unroll
-    for (int k = 0; k < 10; ++k)
-        if (lane == k) v = k < 4 ? t2[k & 3] : cx[(k - 4) % 6];
-    if (lane < 16) A.bc[((size_t)sv * nb + b) * 16 + lane] = v;
-    if (lane < 4) {  // theta2 image (cost kernels, diagnostics)
-        const int i = (b % bpc) * 4 + lane, cls = b / bpc;
-        if (i < per_class) {
-            const int lr = (cls >> 1) + 2 * (i / h), lc = (cls & 1) + 2 * (i % h);
-            if (r0 + lr < n_side && c0 + lc < n_side) A.th[(size_t)(r0 + lr) * n_side + c0 + lc] = v;
+                for (int q = 0; q < K; ++q) a[p][g][q] = an[p][g][q];
         }
     }
-    }  // task
 }
 
 // agent rows <- global y / lambda (local row r = j n_ch + c, icd.py:187-188)

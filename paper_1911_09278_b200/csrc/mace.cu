@@ -282,12 +282,13 @@ static void compute_theta2(Ctx* c)
     if (c->schedule == 1) {
         k_theta2_raster<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_agents.p, c->n_local, (int)c->n);
     } else {
-        // one warp per (item, batch)
+        // one block per (agent, tile) item, the tile's lambda window in shared memory
         const int nb = sv_batches(c->S);
-        const long blocks = std::max(1L, ((long)c->n_items * nb + 3) / 4);  // one warp per task (a persistent grid is slower)
+        const size_t smem = sizeof(float) * c->sv_ng * c->sv_wcap * 32;
         auto go = [&](auto kern) {
-            kern<<<(unsigned)blocks, 128, 0, c->stream>>>(c->d_agents.p, c->n_items, c->queue.p, c->n_side, c->S, nb,
-                                                          c->sv_wcap);
+            if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            kern<<<(unsigned)std::max(1, c->n_items), 128, smem, c->stream>>>(c->d_agents.p, c->n_items, c->queue.p,
+                                                                            c->n_side, c->S, nb, c->sv_wcap);
         };
         const int key = c->sv_K * 10 + c->sv_ng + (c->weighted ? 100 : 0);
         switch (key) {
