@@ -131,3 +131,31 @@ def test_every_tile_side_reaches_the_raster_prox_point(sv_side, weighted, monkey
     za = mb.prox_solve(a, v, tol=1e-7, max_passes=3000)
     zb = mb.prox_solve(b, v, tol=1e-7, max_passes=3000)
     assert rel(zb, za) < 1e-4
+
+
+@pytest.mark.parametrize("sv_side", [4, 8])
+@pytest.mark.parametrize("weighted", [True, False])
+def test_sv_consts_theta2_matches_oracle(golden, sv_side, weighted, monkeypatch):
+    """k_sv_consts (one block per tile, lambda window in shared memory): the theta2 image it writes
+    per data load is sum_r a_r^2 lambda_r over each agent's rows (icd.py:193-195), for weighted and
+    plain records, before and after a second data load with different weights."""
+    prob = _ellipse_problem(golden)
+    monkeypatch.setenv("MACE_WEIGHTED", "1" if weighted else "0")
+    engine.clear_cache()
+    views = [tuple(s.view_indices) for s in mb.partition_views(prob.geom.n_views, 4)]
+    plan = engine.plan_for(prob.matrices, views, schedule="sv", sv=sv_side)
+    y = np.asarray(golden["ell_y"], np.float64)
+    w0 = np.asarray(golden["ell_w"], np.float64)
+    rng = np.random.default_rng(7)
+    for w in (w0, w0 * rng.uniform(0.5, 2.0, size=w0.shape)):
+        plan.load_data(y, w)
+        assert bool(plan.info()["weighted"]) == weighted
+        wv = w.reshape(prob.geom.n_views, -1)
+        for i, vs in enumerate(views):
+            import scipy.sparse as sp
+            A = sp.vstack([O.view_csr(prob.matrices[v]) for v in vs]).tocsr()
+            lam = np.concatenate([wv[v] for v in vs])
+            ref = np.asarray(A.multiply(A).T @ lam).ravel()
+            got = plan.get_theta2(i)
+            assert rel(got, ref) < 1e-5, (i, rel(got, ref))
+    engine.clear_cache()
