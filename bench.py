@@ -1,19 +1,27 @@
-"""Benchmark: MACE voxel-updates/s on BASELINE config 1 (512^2, 720 views x 725 channels,
-N = 8 view-interleaved agents, rho = 0.8, 40 iterations, qGGMRF), one JSON line on rank 0.
+"""Benchmark: MACE voxel-updates/s and time-to-RMSE on BASELINE config 2 (1024^2, 1440 views x
+1450 channels, N = 16 view-interleaved agents, rho = 0.8, 50 iterations, qGGMRF) -- the
+metric's 1/2/4/8-GPU strong-scaling config -- one JSON line on rank 0.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+``--gpus N`` without a torchrun environment re-launches this script under
+``torch.distributed.run`` with N ranks (one process per GPU, agent i on rank i mod N).
 
 A step is one full MACE solve of the config's iteration budget on the seeded
 synthetic scan (gen.make_scan).  ``value`` = total voxel updates (N agents x n
 pixels x iterations x steps, all ranks) / max-over-ranks device time, inputs
 resident in HBM.  ``e2e`` = the same metric through the public API
 (mace_solve on host numpy arrays: H2D of y / weights, D2H of image + stack
-inside the timed region).  The per-iteration A stream (1.4 GB) exceeds the
-126 MB L2, so no L2 flush is needed between steps.
+inside the timed region).  The per-iteration record stream (1.9 GB at config 1,
+15.6 GB at config 2; ``config.l2``) exceeds the 126 MB L2, so no L2 flush is
+needed between steps.
 
 ``--impl reference`` times the CPU oracle (oracle/, the restatement of the
 reference's numba hot loop, all host threads) on a bounded sample of the same
-workload and prints the same metric with "impl": "reference".
+workload and prints the same metric with "impl": "reference".  That arm never
+loads this repo's CUDA library: the scan is traced by the oracle's tracer
+(checked against the reference's SHA-256) and the data synthesised by gen.py
+loaded as a plain module.
 """
 
 from __future__ import annotations
@@ -33,6 +41,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "MACE voxel-updates/s"
+# fresh-solve iterations run for time-to-RMSE <= 1e-3 (covers the measured first-passage iteration)
+TTR_ITERS = {0: 1500, 1: 3000, 2: 8000}
 UNIT = "voxel-updates/s"
 
 
@@ -41,6 +51,48 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_command(gpus: int, argv: list[str]) -> list[str] | None:
+    """The torchrun command that runs this script on `gpus` ranks, or None when no re-launch is
+    needed (one GPU, or already inside a torchrun environment of the right size)."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != gpus:
+            raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={world}")
+        return None
+    if gpus <= 1:
+        return None
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *argv]
+
+
+def load_gen():
+    """paper_1911_09278_b200/gen.py (the workload recipe: phantom, Poisson draw, config table) as a
+    plain module, without importing the package (the reference arm must not load libmace_b200)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("_bench_gen", os.path.join(ROOT, "paper_1911_09278_b200", "gen.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def l2_mb():
+    try:
+        import torch
+
+        return round(torch.cuda.get_device_properties(0).L2_cache_size / 2 ** 20)
+    except Exception:
+        return None
 
 
 def peaks():
@@ -141,6 +193,47 @@ def k2_traffic(config, sv):
     except (OSError, ValueError):
         return None
     return t["dram_bytes_per_launch"] if t.get("config") == config and t.get("sv_side") == sv else None
+
+
+def run_cpu_test(args):
+    """Test hook (--cpu-test): the same rank layout and max-over-ranks timing as run_ours, on CPU
+    with gloo and the oracle-backed plan of tests/cpu_backend.py, so the --gpus N launch path
+    (re-exec under torch.distributed.run, one process per rank) is exercised without a GPU."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import paper_1911_09278_b200 as mb
+    from conftest import small_problem
+    from cpu_backend import CpuPlan
+
+    _, y, w = small_problem(31, 8, 16, 11)
+    geom = mb.Geometry(8, 1.0, 16, 11, 8 / 11 * 1.1)
+    prob = mb.ReconProblem(geom, mb.build_system_matrix(geom), y, w, mb.PriorParams("qggmrf", 1.0, sigma_x=0.5))
+    cfg = mb.MaceConfig(n_subsets=4, rho=0.8, sigma=0.2, max_outer=12, tol=1e-300, residuals="none")
+    res = None
+    for _ in range(args.warmup):
+        res = _solve_api(mb, prob, cfg, True if world > 1 else None, backend=CpuPlan)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = _solve_api(mb, prob, cfg, True if world > 1 else None, backend=CpuPlan)
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    updates = cfg.n_subsets * geom.n_pixels * cfg.max_outer * args.steps
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": updates / float(dt), "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "cpu_test": True,
+                          "ranks_agents": {r: [i for i in range(cfg.n_subsets) if i % world == r] for r in range(world)},
+                          "image_sum": float(np.sum(res.image))}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def run_ours(args):
@@ -277,7 +370,8 @@ def run_ours(args):
                    f"{geom.n_channels} ch, N={N} agents, {iters} iterations, rho=0.8, qGGMRF beta={cfg['beta']}, "
                    f"sigma={cfg['sigma']}", "schedule": args.schedule, "sv_side": args.sv,
                    "parallelism": f"agents {N} over {world} GPU(s)" + (f", consensus: {args.comm}" if world > 1 else ""),
-                   "l2": "inputs > L2 (A stream 1.4 GB/iter)",
+                   "l2": f"inputs > L2: K2 streams {lay['layout_bytes'] / 1e9:.2f} GB of records per iteration "
+                         f"per GPU against a {l2_mb()} MB L2 (no flush needed)",
                    "final_relnorm": float(lg[-1, 0]) if len(lg) else None},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "note": "mace_solve() on host float64 y/weights; includes H2D, solve, D2H image+stack"},
@@ -357,11 +451,11 @@ def plan_stream(plan):
     return s.value
 
 
-def _solve_api(mb, prob, cfg, comm, denoiser=None):
+def _solve_api(mb, prob, cfg, comm, denoiser=None, backend=None):
     try:
         if denoiser is not None:
-            return mb.mace_pnp_solve(prob, cfg, comm=comm, denoiser=denoiser)
-        return mb.mace_solve(prob, cfg, comm=comm)
+            return mb.mace_pnp_solve(prob, cfg, comm=comm, denoiser=denoiser, _backend=backend)
+        return mb.mace_solve(prob, cfg, comm=comm, _backend=backend)
     except mb.ConvergenceError as err:
         return err.last_iterate
 
@@ -380,7 +474,7 @@ def cpu_baseline(config, mats, y, lam, sample_iters=2, threads=None):
     threads = threads or min(N, cores)
     ns = int(np.sqrt(mats[0].n_pixels))
     prior = O.Prior("qggmrf", cfg["beta"], 2.0, 1.2, 1.0, 0.01)
-    agents = O.build_agents(mats, y, lam, N, cfg["sigma"], prior, ns)
+    agents = O.build_agents(mats, y, lam, N, cfg["sigma"], prior, ns, workers=threads)
     O.mace_run(agents, 1, 0.8, workers=threads)  # warm-up
     t0 = time.perf_counter()
     run = O.mace_run(agents, sample_iters, 0.8, workers=threads)
@@ -392,22 +486,51 @@ def cpu_baseline(config, mats, y, lam, sample_iters=2, threads=None):
             "seconds": dt}
 
 
+def reference_scan(config: int, workers: int | None = None):
+    """The config's scan for the reference arm without this repo's CUDA library: the oracle's
+    tracer (oracle.iter_system_matrix, bit-identical to the reference's build_system_matrix; SHA-256
+    tests in tests/test_oracle_golden.py) and gen.make_scan's data recipe (same phantom, same
+    scipy per-view product, same Poisson draw), so y and weights equal the GPU arm's."""
+    import scipy.sparse as sp
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    gen = load_gen()
+    c = gen.CONFIGS[config]
+    ns, nv, nc = c["n_side"], c["n_views"], c["n_channels"]
+    pitch = 1.0 if config == 0 else gen.pitch_for(ns)
+    mats = O.build_system_matrix_parallel(ns, pitch, nv, nc, pitch, workers)
+    phantom = gen.ellipse_phantom(ns, pitch, c["n_ellipses"], seed=0)
+    proj = np.stack([sp.csr_matrix((m.lens, m.cols, m.row_ptr), shape=(m.n_channels, m.n_pixels)) @ phantom
+                     for m in mats])
+    y, lam = gen.poisson_sinogram(proj, c["I0"], seed=1)
+    return c, ns, mats, y, lam
+
+
+def _libmace_loaded() -> bool:
+    try:
+        return "libmace_b200" in open("/proc/self/maps").read()
+    except OSError:
+        return False
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_1911_09278_b200 import gen
-
-    cfg = gen.CONFIGS[args.config]
-    geom, mats, phantom, y, lam = gen.make_scan(args.config)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
 
-    N = cfg["n_agents"]
     cores = os.cpu_count() or 1
+    t0 = time.time()
+    cfg, ns, mats, y, lam = reference_scan(args.config, cores)
+    N = cfg["n_agents"]
     threads = min(N, cores)
     prior = O.Prior("qggmrf", cfg["beta"], 2.0, 1.2, 1.0, 0.01)
-    agents = O.build_agents(mats, y, lam, N, cfg["sigma"], prior, geom.n_side)
+    agents = O.build_agents(mats, y, lam, N, cfg["sigma"], prior, ns, workers=threads)
+    del mats
+    t_setup = time.time() - t0
     per_step = max(1, args.cpu_iters)
     for _ in range(args.warmup):
         O.mace_run(agents, 1, 0.8, workers=threads)
@@ -417,19 +540,22 @@ def run_reference(args):
         run = O.mace_run(agents, per_step, 0.8, workers=threads)
         done += len(run.relnorms)
     dt = time.perf_counter() - t0
-    n = geom.n_pixels
+    n = ns * ns
     value = N * n * done / dt
+    if _libmace_loaded():
+        raise SystemExit("reference arm mapped libmace_b200.so")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen.make_scan)",
-            "impl": "reference",
-            "config": {"workload": f"BASELINE config {args.config}: {geom.n_side}^2, {geom.n_views} views x "
-                       f"{geom.n_channels} ch, N={N} agents; each step = {per_step} MACE iteration(s) (bounded "
-                       "sample of the 40-iteration solve)"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded ellipse phantom, "
+            "Poisson counts; gen.py recipe, oracle tracer)", "impl": "reference",
+            "config": {"workload": f"BASELINE config {args.config}: {ns}^2, {y.shape[0]} views x {y.shape[1]} ch, "
+                       f"N={N} agents; each step = {per_step} MACE iteration(s) (bounded sample of the "
+                       f"{cfg['iters']}-iteration solve)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{per_step} MACE iteration(s) per step, oracle/sweep.c float64, "
-                                       f"{threads} threads of {cores}"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": f"{per_step} MACE iteration(s) per step, oracle/sweep.c float64 raster "
+                                       f"ICD, agents over {threads} threads of {cores}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "libmace_b200_loaded": False, "setup_s": t_setup}
     print(json.dumps(line), flush=True)
 
 
@@ -526,20 +652,31 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--iters", type=int, default=0)
     ap.add_argument("--schedule", default="sv", choices=["sv", "raster"])
     ap.add_argument("--sv", type=int, default=8)
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--ttr-iters", type=int, default=3000, help="iterations for time-to-RMSE (0: skip)")
+    ap.add_argument("--ttr-iters", type=int, default=-1,
+                    help="iterations for time-to-RMSE (0: skip; default: per config, TTR_ITERS)")
     ap.add_argument("--slices", type=int, default=0, help="config 4: number of slices (default 64)")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
                     help="N > 1: consensus by an NCCL all-reduce on the library stream, or by the library's own "
                          "push/reduce kernels over NVLink peer memory (PeerComm)")
+    ap.add_argument("--cpu-test", action="store_true", help=argparse.SUPPRESS)  # tests: gloo ranks on CPU
     args = ap.parse_args()
+    if args.ttr_iters < 0:
+        args.ttr_iters = TTR_ITERS.get(args.config, 0)
+    if args.impl == "ours":
+        cmd = launch_command(args.gpus, sys.argv[1:])
+        if cmd is not None:  # one process per GPU: re-run this script under torchrun
+            sys.stdout.flush()
+            os.execv(cmd[0], cmd)
     if args.impl == "reference":
         run_reference(args)
+    elif args.cpu_test:
+        run_cpu_test(args)
     elif args.config == 4:
         run_batch(args)
     else:

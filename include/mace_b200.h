@@ -83,6 +83,10 @@ int mace_setup_agents(void* ctx, int n_agents, const int* view_counts, const int
 /* super-voxel schedule: at most `concurrency` x (tiles in the pass) tiles in flight (>= 1 per agent);
  * max_warps > 0 caps the number of resident warps */
 int mace_set_schedule(void* ctx, double concurrency, int64_t max_warps);
+/* super-voxel queue in consecutive groups of `group` agents (0: every agent at once): each agent
+ * of a group then has about (resident warps / group) tiles in flight, the per-agent staleness of a
+ * rank that owns `group` agents (1-GPU emulation of an N-GPU partition) */
+int mace_set_agent_groups(void* ctx, int group);
 /* local < 0: every local agent */
 int mace_set_agent_params(void* ctx, int local, double beta_eff, double inv_sigma2, int clamp);
 /* global sinogram y and weights, n_views x n_ch float32; recomputes theta2.  Single-slice
@@ -100,6 +104,11 @@ int mace_refresh(void* ctx, int local);
 /* n_passes passes over pixels [s_begin, s_end) (s_end < 0: all; ranges need the raster schedule) */
 int mace_pass(void* ctx, int local, const float* v, int n_passes, int64_t s_begin, int64_t s_end, double* dsq);
 
+/* every local agent's proximal map F_i(v_i; sigma) at once (equilibrium_residuals, mace.py:440-452):
+ * v[n_local * n] targets, x0[n] start; passes until every agent's sqrt(sum alpha^2)/||z|| < tol
+ * (prox_solve's test, icd.py:286-303) or max_passes; results in the agents' states */
+int mace_prox_all(void* ctx, const float* v, const float* x0, int max_passes, double tol, int* passes_out,
+                  double* rel_out);
 int mace_forward_project(void* ctx, const float* x, float* out);
 /* out[n] (fp64) = A^T sino: back_project geometry.py:273-282, the exact transpose of forward_project */
 int mace_back_project(void* ctx, const float* sino, double* out);
@@ -140,6 +149,8 @@ int mace_read_log(void* ctx, int n, double* log, int* done2);
 int mace_cnn_set_weights(void* ctx, const uint16_t* bf16, int layers, int channels);
 int mace_cnn_apply(void* ctx); /* g = H(wbar), on the device */
 int mace_cnn_run(void* ctx, const float* x, float* out, int h, int w, float* ms_out);
+/* one 64->64 layer alone (layer 0..14 = net layers 2..16: conv + ReLU, bf16 out), bf16 CHW host arrays */
+int mace_cnn_layer(void* ctx, int layer, const uint16_t* in_chw, uint16_t* out_chw, int h, int w);
 /* per-launch CUDA-event timing of K2 on the context stream (enable=1 start, 0 stop + read) */
 int mace_k2_timing(void* ctx, int enable, double* total_ms, int64_t* launches);
 

@@ -40,6 +40,8 @@ _SIGS = {
     "mace_set_prior": (c_int, [P, c_int, c_double, c_double, c_double, c_double, c_double]),
     "mace_setup_agents": (c_int, [P, c_int, P, P, c_int, c_int, c_int, c_int, c_int]),
     "mace_set_schedule": (c_int, [P, c_double, c_int64]),
+    "mace_set_agent_groups": (c_int, [P, c_int]),
+    "mace_prox_all": (c_int, [P, P, P, c_int, c_double, P, P]),
     "mace_set_agent_params": (c_int, [P, c_int, c_double, c_double, c_int]),
     "mace_load_data": (c_int, [P, P, P]),
     "mace_set_weighting": (c_int, [P, c_int]),
@@ -74,6 +76,7 @@ _SIGS = {
     "mace_cnn_set_weights": (c_int, [P, P, c_int, c_int]),
     "mace_cnn_apply": (c_int, [P]),
     "mace_cnn_run": (c_int, [P, P, P, c_int, c_int, P]),
+    "mace_cnn_layer": (c_int, [P, c_int, P, P, c_int, c_int]),
     "mace_sweep_f64": (c_int, [P] * 10 + [c_double, c_double, c_double, c_int, c_double, c_double, c_double,
                                           c_double, c_int, c_int64, c_int64, c_int64, c_int64, P]),
     "mace_agent_csc": (c_int, [c_int, c_int, c_int, P, P, P, c_int, P, P, P, P]),

@@ -698,42 +698,69 @@ void Cnn::ensure(int h, int w)
     CKC(cudaFuncSetAttribute(k_conv64_tc2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
 }
 
+// one 64 -> 64 layer (2..16) from map -> dst on stream s with the current launch geometry
+void Cnn::launch_mid(int l, const CUtensorMap& m, __nv_bfloat16* dst, cudaStream_t s, int num_sms, bool pdl_on)
+{
+    // one CTA per (128-px strip, run of rows); one CTA per SM (140 KB smem)
+    const int strips = (W + kTileX - 1) / kTileX;
+    const int ctas_y = std::max(1, num_sms / strips);
+    const int per = (H + ctas_y - 1) / ctas_y;  // rows per CTA
+    const int ctas = strips * ((H + per - 1) / per);
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = s;
+    cfg.attrs = pdl;
+    cfg.numAttrs = pdl_on ? 1 : 0;
+    if (rows_unit == 3)
+        CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc2<3>, m, (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC),
+                               dst, H, W, Wp, per));
+    else if (rows_unit == 2)
+        CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc2<2>, m, (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC),
+                               dst, H, W, Wp, per));
+    else
+        CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc, m, (const __nv_bfloat16*)(w_mid.p + (size_t)l * 9 * kC * kC), dst,
+                               H, W, Wp, per));
+}
+
+void Cnn::layer(int l, const uint16_t* in_chw, uint16_t* out_chw, int h, int w, cudaStream_t s, int num_sms)
+{
+    if (!ready) throw std::runtime_error("denoiser weights not set");
+    if (l < 0 || l >= 15) throw std::runtime_error("middle layer index 0..14");
+    ensure(h, w);
+    // CHW bf16 -> channel-blocked [8 groups][H][Wp][8 ch] (padding columns zero)
+    std::vector<uint16_t> blk((size_t)H * Wp * kC, 0);
+    for (int c = 0; c < kC; ++c)
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x)
+                blk[(((size_t)(c / 8) * H + y) * Wp + x) * 8 + (c % 8)] = in_chw[((size_t)c * H + y) * W + x];
+    CKC(cudaMemcpyAsync(act0.p, blk.data(), blk.size() * 2, cudaMemcpyHostToDevice, s));
+    launch_mid(l, map0, act1.p, s, num_sms, false);
+    CKC(cudaMemcpyAsync(blk.data(), act1.p, blk.size() * 2, cudaMemcpyDeviceToHost, s));
+    CKC(cudaStreamSynchronize(s));
+    for (int c = 0; c < kC; ++c)
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x)
+                out_chw[((size_t)c * H + y) * W + x] = blk[(((size_t)(c / 8) * H + y) * Wp + x) * 8 + (c % 8)];
+}
+
 void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int num_sms, int* launches)
 {
     if (!ready) throw std::runtime_error("denoiser weights not set");
     ensure(h, w);
     const int npx = H * W;
     k_conv_first<<<(npx + 255) / 256, 256, 0, s>>>(x, w_first, act0.p, H, W, Wp);
-    // one CTA per (128-px strip, run of rows); one CTA per SM (140 KB smem)
-    const int strips = (W + kTileX - 1) / kTileX;
-    const int ctas_y = std::max(1, num_sms / strips);
-    const int per = (H + ctas_y - 1) / ctas_y;  // rows per CTA
-    const int ctas = strips * ((H + per - 1) / per);
     // layers 2..17 are launched with programmatic stream serialization (PDL): each one's prologue
     // overlaps the previous layer's tail; griddepcontrol.wait orders the activation reads
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     pdl[0].val.programmaticStreamSerializationAllowed = 1;
-    for (int l = 0; l < 15; ++l) {
-        const CUtensorMap& m = (l & 1) ? map1 : map0;
-        __nv_bfloat16* dst = (l & 1) ? act0.p : act1.p;
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(ctas);
-        cfg.blockDim = dim3(192);
-        cfg.dynamicSmemBytes = kSmem;
-        cfg.stream = s;
-        cfg.attrs = pdl;
-        cfg.numAttrs = 1;
-        if (rows_unit == 3)
-            CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc2<3>, m,
-                                   (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC), dst, H, W, Wp, per));
-        else if (rows_unit == 2)
-            CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc2<2>, m,
-                                   (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC), dst, H, W, Wp, per));
-        else
-            CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc, m, (const __nv_bfloat16*)(w_mid.p + (size_t)l * 9 * kC * kC),
-                                   dst, H, W, Wp, per));
-    }
+    for (int l = 0; l < 15; ++l)
+        launch_mid(l, (l & 1) ? map1 : map0, (l & 1) ? act0.p : act1.p, s, num_sms, true);
     // 15 middle layers: the last one wrote act1 (l = 14 even -> dst act1)
     {
         cudaLaunchConfig_t cfg{};

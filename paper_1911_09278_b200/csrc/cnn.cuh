@@ -50,6 +50,9 @@ struct Cnn {
     void ensure(int h, int w);
     // out = x - net(x) for an h x w fp32 image (device pointers), on stream s
     void apply(const float* x, float* out, int h, int w, cudaStream_t s, int num_sms, int* launches);
+    // one middle layer l (0..14 = layers 2..16) alone on a bf16 CHW input (host arrays; tests)
+    void layer(int l, const uint16_t* in_chw, uint16_t* out_chw, int h, int w, cudaStream_t s, int num_sms);
+    void launch_mid(int l, const CUtensorMap& m, __nv_bfloat16* dst, cudaStream_t s, int num_sms, bool pdl);
 };
 
 }  // namespace mace

@@ -89,7 +89,8 @@ void build_raster_layout(const AgentCSC& csc, int n, RasterLayout& out);
 void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int n_views_agent, int svs, SVLayout& out, int ng = 0);
 // Queue of (agent << 22 | sv) items: colour classes (sv_row mod C, sv_col mod C) in
 // order, SVs of a class in raster order, agents interleaved within a position.
-std::vector<uint32_t> build_queue(int n_agents, int n_sv_side, int colours, int n_slices = 1);
+// group > 0: agents in consecutive groups of `group` (each group's tiles before the next group's).
+std::vector<uint32_t> build_queue(int n_agents, int n_sv_side, int colours, int n_slices = 1, int group = 0);
 
 void set_error(const std::string& msg);
 

@@ -181,23 +181,28 @@ void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SV
     }
 }
 
-std::vector<uint32_t> build_queue(int n_agents, int n_sv_side, int C, int n_slices)
+std::vector<uint32_t> build_queue(int n_agents, int n_sv_side, int C, int n_slices, int group)
 {
     if (C < 1) C = 1;
     if (C > n_sv_side) C = n_sv_side;
+    if (group < 1 || group > n_agents) group = n_agents;
     if ((int64_t)n_agents * n_slices > (1 << (32 - 22)) || (int64_t)n_sv_side * n_sv_side > (1 << 22))
         throw std::runtime_error("work queue: too many agents x slices or super-voxels");
     std::vector<uint32_t> q;
     q.reserve((size_t)n_agents * n_slices * n_sv_side * n_sv_side);
     // local (virtual) agent index = slice * n_agents + agent; at one tile position the slices
-    // of an agent are adjacent, so they run concurrently and share that tile's A columns in L2
-    for (int cr = 0; cr < C; ++cr)
-        for (int cc = 0; cc < C; ++cc)
-            for (int r = cr; r < n_sv_side; r += C)
-                for (int c = cc; c < n_sv_side; c += C)
-                    for (int a = 0; a < n_agents; ++a)
-                        for (int s = 0; s < n_slices; ++s)
-                            q.push_back(((uint32_t)(s * n_agents + a) << 22) | (uint32_t)(r * n_sv_side + c));
+    // of an agent are adjacent, so they run concurrently and share that tile's A columns in L2.
+    // Agents run in groups of `group` (default: all at once): a group's tiles fill the whole
+    // grid before the next group's start, so each agent of a group has about warps / group tiles
+    // in flight -- the per-agent concurrency (staleness) of a rank that owns `group` agents.
+    for (int g0 = 0; g0 < n_agents; g0 += group)
+        for (int cr = 0; cr < C; ++cr)
+            for (int cc = 0; cc < C; ++cc)
+                for (int r = cr; r < n_sv_side; r += C)
+                    for (int c = cc; c < n_sv_side; c += C)
+                        for (int a = g0; a < std::min(n_agents, g0 + group); ++a)
+                            for (int s = 0; s < n_slices; ++s)
+                                q.push_back(((uint32_t)(s * n_agents + a) << 22) | (uint32_t)(r * n_sv_side + c));
     return q;
 }
 

@@ -118,6 +118,7 @@ struct Ctx {
     size_t sv_smem = 0;
     int sv_grid = 0, sv_warps = 0;
     double sv_frac = 1.0 / 16.0;  // max fraction of an agent's tiles in flight
+    int colours = 4, n_sv_side = 1, sv_group = 0;  // queue geometry (mace_set_agent_groups rebuilds it)
     long sv_max_warps = 0;        // optional hard cap (0: none)
     int passes = 0;
     int num_sms = 148;
@@ -735,6 +736,9 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
     while (c->NV < 16 && 128 * c->NV < max_col) c->NV *= 2;
     if (max_col > 128 * 16) throw std::runtime_error("column longer than 2048 entries");
     if (schedule == 0) {
+        c->colours = colours;
+        c->n_sv_side = n_sv_side;
+        c->sv_group = 0;
         std::vector<uint32_t> q = build_queue(n_agents, n_sv_side, colours, n_slices);
         c->queue.alloc(q.size());
         CK(cudaMemcpy(c->queue.p, q.data(), sizeof(uint32_t) * q.size(), cudaMemcpyHostToDevice));
@@ -799,6 +803,20 @@ int mace_set_schedule(void* p, double concurrency, int64_t max_warps)
     if (!(concurrency > 0.0) || concurrency > 1.0) throw std::runtime_error("concurrency must be in (0, 1]");
     c->sv_frac = concurrency;
     c->sv_max_warps = (long)max_warps;
+    API_END
+}
+
+int mace_set_agent_groups(void* p, int group)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (c->schedule != 0) throw std::runtime_error("agent groups need the super-voxel schedule");
+    if (group < 0) throw std::runtime_error("group must be >= 0");
+    std::vector<uint32_t> q = build_queue(c->n_real, c->n_sv_side, c->colours, c->n_slices, group);
+    if ((int)q.size() != c->n_items) throw std::runtime_error("queue size changed");
+    sync(c);
+    CK(cudaMemcpy(c->queue.p, q.data(), sizeof(uint32_t) * q.size(), cudaMemcpyHostToDevice));
+    c->sv_group = group;
     API_END
 }
 
@@ -943,6 +961,66 @@ int mace_pass(void* p, int local, const float* v, int n_passes, int64_t s_begin,
         }
     }
     sync(c);
+    API_END
+}
+
+// Every local agent's proximal map at once (equilibrium_residuals, mace.py:440-452): agent i starts
+// from x0 with target v_i (v: [n_local][n]) and runs plain passes of the context's schedule until
+// sqrt(sum alpha^2) / ||z_i|| < tol for every agent (prox_solve's test, icd.py:286-303), refreshing e
+// every 50 passes.  passes_out = passes run, rel_out[n_local] = each agent's last relative update.
+// The solutions stay in the agents' states (mace_get_state).
+int mace_prox_all(void* p, const float* v, const float* x0, int max_passes, double tol, int* passes_out,
+                  double* rel_out)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (c->n_slices != 1) throw std::runtime_error("prox_all needs a single-slice context");
+    const int NL = c->n_local;
+    for (int a = 0; a < NL; ++a) {
+        CK(cudaMemcpyAsync(c->h_agents[a].vt, v + (size_t)a * c->n, sizeof(float) * c->n, cudaMemcpyHostToDevice,
+                           c->stream));
+        CK(cudaMemcpyAsync(c->h_agents[a].z, x0, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream));
+    }
+    CK(cudaMemsetAsync(c->done.p, 0, 2 * sizeof(int), c->stream));
+    refresh(c, 0, NL);
+    // item -> agent of the pass's queue (super-voxel: queue order; raster: one item per agent)
+    std::vector<int> item_agent(c->n_items);
+    if (c->schedule == 0) {
+        std::vector<uint32_t> q(c->n_items);
+        CK(cudaMemcpyAsync(q.data(), c->queue.p, sizeof(uint32_t) * q.size(), cudaMemcpyDeviceToHost, c->stream));
+        sync(c);
+        for (int i = 0; i < c->n_items; ++i) item_agent[i] = (int)(q[i] >> kAgentShift);
+    } else {
+        for (int i = 0; i < c->n_items; ++i) item_agent[i] = i;
+    }
+    std::vector<double> part((size_t)c->n_items * 4), dsq(NL), rel(NL, INFINITY);
+    std::vector<float> z((size_t)NL * c->n);
+    int k = 0;
+    for (; k < max_passes; ++k) {
+        run_pass(c, 0, 0.f, nullptr, 0, NL);
+        if ((k + 1) % 50 == 0) refresh(c, 0, NL);  // icd.py:29,298-299
+        CK(cudaMemcpyAsync(part.data(), c->part.p, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(z.data(), c->Z.p, sizeof(float) * z.size(), cudaMemcpyDeviceToHost, c->stream));
+        sync(c);
+        std::fill(dsq.begin(), dsq.end(), 0.0);
+        for (int i = 0; i < c->n_items; ++i) dsq[item_agent[i]] += part[(size_t)i * 4];
+        double worst = 0.0;
+        for (int a = 0; a < NL; ++a) {
+            double zz = 0.0;
+            const float* za = z.data() + (size_t)a * c->n;
+            for (size_t s = 0; s < c->n; ++s) zz += (double)za[s] * za[s];
+            rel[a] = std::sqrt(dsq[a]) / std::max(std::sqrt(zz), 1e-300);
+            worst = std::max(worst, rel[a]);
+        }
+        if (worst < tol) {
+            ++k;
+            break;
+        }
+    }
+    c->passes += k;
+    if (passes_out) *passes_out = k;
+    if (rel_out)
+        for (int a = 0; a < NL; ++a) rel_out[a] = rel[a];
     API_END
 }
 
@@ -1538,6 +1616,15 @@ int mace_cnn_apply(void* p)
     API_BEGIN
     Ctx* c = C(p);
     cnn_all_slices(c);
+    API_END
+}
+
+// one middle layer alone (layer index 0..14 = layers 2..16), bf16 CHW in/out (host); the per-layer test
+int mace_cnn_layer(void* p, int layer, const uint16_t* in_chw, uint16_t* out_chw, int h, int w)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    c->cnn.layer(layer, in_chw, out_chw, h, w, c->stream, c->num_sms);
     API_END
 }
 

@@ -106,6 +106,23 @@ class CnnDenoiser:
         self._load(plan)
         plan.call("mace_cnn_apply")
 
+    def layer(self, index: int, x_bits: np.ndarray) -> np.ndarray:
+        """One 64 -> 64 layer alone on the tensor cores: middle layer `index` (0..14 = net layers
+        2..16) of a (64, h, w) bf16 input given as uint16 bits; returns the bf16 bits of
+        ReLU(conv) as (64, h, w).  Test hook for the per-layer rounding check."""
+        from . import _native as N
+        from .engine import _Context
+
+        if self._ctx is None:
+            self._ctx = _Context(self.device)
+        self._load(self._ctx)
+        x = np.ascontiguousarray(x_bits, np.uint16)
+        if x.ndim != 3 or x.shape[0] != CNN_CHANNELS:
+            raise ValueError("input must be (64, h, w) bf16 bits")
+        out = np.empty_like(x)
+        self._ctx.call("mace_cnn_layer", int(index), N.ptr(x), N.ptr(out), int(x.shape[1]), int(x.shape[2]))
+        return out
+
     def __call__(self, v):
         import ctypes
 

@@ -246,6 +246,10 @@ class AgentPlan(_Context):
     def set_schedule(self, concurrency=DEFAULT_CONCURRENCY, max_warps=0):
         self.call("mace_set_schedule", float(concurrency), int(max_warps))
 
+    def set_agent_groups(self, group: int):
+        """Super-voxel queue in groups of `group` agents (0: all at once); see mace_set_agent_groups."""
+        self.call("mace_set_agent_groups", int(group))
+
     def set_agent_params(self, local, beta_eff, inv_sigma2, clamp=False):
         self.call("mace_set_agent_params", int(local), float(beta_eff), float(inv_sigma2), int(bool(clamp)))
 
@@ -271,6 +275,18 @@ class AgentPlan(_Context):
 
     def refresh(self, local=-1):
         self.call("mace_refresh", int(local))
+
+    def prox_all(self, v, x0, tol, max_passes=500):
+        """Every local agent's proximal map at once: states start at x0, targets v (n_local, n);
+        passes until each agent's sqrt(sum alpha^2)/||z|| < tol.  Returns (passes, rel[n_local]);
+        the solutions are the agents' states."""
+        v = N.f32(np.asarray(v).reshape(self.n_local, self.n))
+        x0 = N.f32(x0)
+        passes = ctypes.c_int(0)
+        rel = np.zeros(self.n_local, np.float64)
+        self.call("mace_prox_all", N.ptr(v), N.ptr(x0), int(max_passes), float(tol), ctypes.byref(passes),
+                  N.ptr(rel))
+        return passes.value, rel
 
     def run_pass(self, local, v, n_passes=1, s_begin=0, s_end=-1) -> np.ndarray:
         v = N.f32(v)

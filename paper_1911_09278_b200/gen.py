@@ -20,14 +20,16 @@ FOV_MM = 128.0
 
 # BASELINE.json:configs -> (n_side, n_views, n_channels, n_agents, iterations, I0, n_ellipses, slices)
 # beta is the reference-convention qGGMRF strength (p=2, q=1.2, T=1, sigma_x=0.01); sigma is the
-# agents' proximal parameter.  BASELINE leaves both open; values and probes in DESIGN.md §3.
+# agents' proximal parameter.  BASELINE leaves both open; values and probes in DESIGN.md §3
+# (config 2: sigma 7e-4 reaches NRMSE 1e-3 in 5,561 iterations, 3.5e-4 needs 22,126, 1e-3 diverges;
+# the same at the 8-GPU per-agent staleness, tools/probe_sigma.py, profiles/r02_probe_c2_sigma.log).
 CONFIGS = {
     0: dict(n_side=128, n_views=180, n_channels=185, n_agents=4, iters=30, I0=1e4, n_ellipses=10, slices=1,
             beta=100.0, sigma=2.5e-4),
     1: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=40, I0=1e4, n_ellipses=10, slices=1,
             beta=25.0, sigma=3.5e-4),
     2: dict(n_side=1024, n_views=1440, n_channels=1450, n_agents=16, iters=50, I0=5e3, n_ellipses=40, slices=1,
-            beta=4.0, sigma=3.5e-4),
+            beta=4.0, sigma=7e-4),
     # PnP agents run at sqrt(N) sigma (mace.py:263-265): sigma = 3.5e-4 / sqrt(8) keeps them at c1's margin
     3: dict(n_side=512, n_views=720, n_channels=725, n_agents=8, iters=40, I0=1e4, n_ellipses=10, slices=1,
             beta=25.0, sigma=1.24e-4),

@@ -27,7 +27,7 @@ import numpy as np
 from .denoisers import DenoiserSpec, make_denoiser
 from .engine import DEFAULT_COLOURS, DEFAULT_SV, plan_for
 from .geometry import partition_views
-from .icd import AgentWorkspace, ConvergenceError, prox_solve
+from .icd import ConvergenceError
 
 __all__ = ["PeerComm", "MaceConfig", "MaceResult", "ConvergenceLog", "ResidualReport", "WorkerPool", "new_stack", "average",
            "consensus_G", "reflect_G", "consensus_GH", "mann_step", "mace_solve", "mace_pnp_solve",
@@ -587,28 +587,53 @@ def mace_solve_batch(problems, config: MaceConfig) -> list:
     return results
 
 
+# float32 state: the relative update of a proximal pass bottoms out near 1e-7 (rounding of theta1 and of
+# z itself), so the equilibrium check's prox solves stop at max(prox_tol, PROX_TOL_FP32) instead of the
+# reference's float64 1e-9 (mace.py:411); r_F is then resolved to ~1e-6 (tests/test_gpu_residuals.py)
+PROX_TOL_FP32 = 1e-6
+
+
 def equilibrium_residuals(problem, config: MaceConfig, w, prox_tol: float = 1e-9, denoiser=None) -> ResidualReport:
-    """Equilibrium check of a stacked state (mace.py:407-454), proximal maps solved on the GPU."""
+    """Equilibrium check of a stacked state (mace.py:407-454).  Conventional: x_hat = mean w,
+    u_i = x_hat - w_i, r_F = max_i ||F_i(x_hat + u_i; sigma) - x_hat|| / ||x_hat|| with F_i the
+    converged proximal map of agent i, r_u = ||sum_i u_i|| / ||x_hat||.  PnP: x_hat = H(mean w),
+    t_i = x_hat - w_i, agents at sqrt(N) sigma and beta 0, r_H = ||H(x_hat + (mean w - x_hat)) -
+    x_hat|| / ||x_hat||.  All N proximal maps are solved at once on the GPU, by the context of
+    the agents' layouts (cached per scan: the one mace_solve used), raster order up to 65,536
+    pixels (as AgentWorkspace) and super-voxel passes beyond."""
     w = _check_stack(w)
-    subsets = partition_views(problem.geom.n_views, config.n_subsets)
+    N = config.n_subsets
+    subsets = partition_views(problem.geom.n_views, N)
+    if w.shape[0] != N:
+        raise ValueError(f"w must have {N} rows")
     w_bar = average(w)
     if config.mode == PNP:
         if denoiser is None:
             denoiser = make_denoiser(config.denoiser, problem.geom.n_side)
         x_hat = np.asarray(denoiser(w_bar), np.float64)
-        sigma, beta = np.sqrt(config.n_subsets) * config.sigma, 0.0
+        sigma, beta = np.sqrt(N) * config.sigma, 0.0
         seconds = x_hat - w
-        aux = float(np.linalg.norm(np.asarray(denoiser(x_hat + (w_bar - x_hat))) - x_hat))
+        aux = float(np.linalg.norm(np.asarray(denoiser(x_hat + (w_bar - x_hat)), np.float64) - x_hat))
     else:
         x_hat = w_bar
-        sigma, beta = config.sigma, config.beta
+        sigma = config.sigma
+        beta = problem.prior.beta if config.beta is None else config.beta
         seconds = x_hat - w
         aux = float(np.linalg.norm(seconds.sum(axis=0)))
     scale = max(float(np.linalg.norm(x_hat)), 1e-300)
-    per_agent = []
-    for i, sub in enumerate(subsets):
-        ws = AgentWorkspace(problem, sub, config.n_subsets, sigma=sigma, beta=beta, state=x_hat,
-                            device=getattr(config, "device", 0))
-        fi = prox_solve(ws, x_hat + seconds[i], tol=prox_tol)
-        per_agent.append(float(np.linalg.norm(fi - x_hat)) / scale)
+    n = problem.geom.n_pixels
+    from .icd import _default_schedule
+
+    plan = plan_for(problem.matrices, [s.view_indices for s in subsets], schedule=_default_schedule(n),
+                    sv=getattr(config, "sv_side", DEFAULT_SV), colours=getattr(config, "colours", DEFAULT_COLOURS),
+                    device=getattr(config, "device", 0))
+    plan.load_data(problem.y, problem.weights)
+    plan.set_prior(problem.prior)
+    plan.set_agent_params(-1, beta / N, 1.0 / (sigma * sigma), getattr(config, "clamp_nonneg", False))
+    tol = max(prox_tol, PROX_TOL_FP32)
+    passes, rel = plan.prox_all(x_hat[None, :] + seconds, x_hat, tol, max_passes=500)
+    if not np.all(rel < tol):
+        raise ConvergenceError(f"equilibrium_residuals: proximal maps not converged to {tol:g} in {passes} passes "
+                               f"(worst {float(rel.max()):.2e})")
+    per_agent = [float(np.linalg.norm(plan.get_state(i).astype(np.float64) - x_hat)) / scale for i in range(N)]
     return ResidualReport(mode=config.mode, r_F=max(per_agent), r_u=aux / scale, per_agent=per_agent)

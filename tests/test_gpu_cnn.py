@@ -76,6 +76,59 @@ def test_cnn_exact_taps_channels_padding(n_side, seed):
     assert np.array_equal(np.asarray(out, np.float32), np.asarray(ref, np.float32))
 
 
+def _bf16_rne_f64(v):
+    """exact fp64 -> bf16 round-to-nearest-even (no double rounding through fp32)"""
+    m, e = np.frexp(v)
+    return np.ldexp(np.rint(m * 256.0) / 256.0, e)
+
+
+@pytest.mark.parametrize("h,w,layer,seed", [(128, 128, 0, 21), (96, 200, 14, 22), (33, 130, 7, 23)])
+def test_cnn_one_layer_bf16_rounding(h, w, layer, seed):
+    """One 64->64 layer alone (tcgen05 UMMAs, fp32 accumulation in TMEM, ReLU, bf16 epilogue) on a
+    fixed bf16 input against the exact fp64 conv rounded once to bf16.  At least 99.9% of the
+    outputs must be bit-identical and every other one exactly one bf16 ulp away AND explained by
+    a near-tie: the exact value within the fp32 accumulation bound (576 terms x 2^-24 x sum|terms|)
+    of the midpoint between its two bf16 neighbours.  A wrong tap, channel, K-step or fragment
+    order would break the count by orders of magnitude."""
+    from paper_1911_09278_b200.denoisers import from_bf16_bits, to_bf16_bits
+
+    rng = np.random.default_rng(seed)
+    wts = cnn_weights(seed, scale=1.0)
+    Wl = wts[1 + layer].astype(np.float64)  # (64 oc, 64 ic, 3, 3), bf16 values
+    x_bits = to_bf16_bits(rng.random((64, h, w)).astype(np.float32))
+    x = from_bf16_bits(x_bits).astype(np.float64)
+    xp = np.zeros((64, h + 2, w + 2))
+    xp[:, 1:-1, 1:-1] = x
+    exact = np.zeros((64, h, w))
+    mag = np.zeros((64, h, w))
+    for dy in range(3):
+        for dx in range(3):
+            sh = xp[:, dy:dy + h, dx:dx + w].reshape(64, -1)
+            exact += (Wl[:, :, dy, dx] @ sh).reshape(64, h, w)
+            mag += (np.abs(Wl[:, :, dy, dx]) @ np.abs(sh)).reshape(64, h, w)
+    ref = _bf16_rne_f64(np.maximum(exact, 0.0))
+    got = from_bf16_bits(CnnDenoiser(h, weights=wts).layer(layer, x_bits)).astype(np.float64)
+    same = got == ref
+    frac = same.mean()
+    bad = ~same
+    ulp = np.ldexp(1.0, np.frexp(np.maximum(np.abs(ref), 1e-30))[1] - 8)
+    bound = 576 * 2.0 ** -24 * mag
+    relu = bad & ((got == 0) | (ref == 0))  # fp32 sum and exact value on either side of the ReLU
+    rnd = bad & ~relu
+    ulps = np.abs(got - ref)[rnd] / ulp[rnd]
+    mid = np.minimum(got, ref)[rnd] + 0.5 * np.abs(got - ref)[rnd]
+    tie = np.abs(exact[rnd] - mid) / bound[rnd]
+    print(f"layer {layer} {h}x{w}: {frac * 100:.4f}% bit-identical; {rnd.sum()} rounding and {relu.sum()} ReLU "
+          f"mismatches; max {ulps.max() if ulps.size else 0:.3f} ulp; midpoint distance / fp32 bound max "
+          f"{tie.max() if tie.size else 0:.3e}; ReLU mismatch / bound max "
+          f"{(np.abs(got - ref)[relu] / bound[relu]).max() if relu.any() else 0:.3e}")
+    assert frac >= 0.999, frac
+    assert np.all(np.abs(got - ref)[relu] <= bound[relu] + 1e-30)
+    assert np.all(ulps <= 1.0 + 1e-6)
+    # every other mismatch sits next to the midpoint between its two bf16 neighbours
+    assert np.all(tie <= 1.0)
+
+
 def test_cnn_config3_weights_run():
     """The literal BASELINE config-3 weights (He-normal x 0.1 per layer) shrink the residual
     by ~0.1 per layer, so H is the identity to fp32 precision: check exactly that."""

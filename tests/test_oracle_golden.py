@@ -165,3 +165,45 @@ def test_ellipse_problem_and_costs_vs_reference(golden):
     x = golden["ell_central"]
     cost = O.likelihood_cost(mats, y, lam, x) + O.prior_cost(x, "qggmrf", 20.0, 2.0, 1.2, 1.0, 0.01, 0, 32)
     assert cost == pytest.approx(golden["ell_cost_central"][0], rel=1e-12)
+
+
+def _digest(mats):
+    import hashlib
+
+    h = hashlib.sha256()
+    for m in mats:
+        h.update(np.ascontiguousarray(m.row_ptr, np.int64).tobytes())
+        h.update(np.ascontiguousarray(m.cols, np.int32).tobytes())
+        h.update(np.ascontiguousarray(m.lens, np.float64).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("name,workers", [("c0", 1), ("c0", 4), ("c1", 8)])
+def test_parallel_oracle_tracer_matches_reference_digest(name, workers):
+    """oracle.iter_system_matrix (views traced by a process pool, consumed in view order; the
+    path bench.py's reference arm and tools/cpu_central_lean.py use) reproduces the reference's
+    full system matrix: SHA-256 written by the reference itself (sysmat_digests.json; config 2's
+    digest is checked by cpu_central_lean.py when it builds the config-2 oracle MAP)."""
+    import json
+    import os
+
+    from conftest import GOLDEN
+
+    d = json.load(open(os.path.join(GOLDEN, "sysmat_digests.json")))
+    assert "c2" in d and d["c2"]["nnz"] == 1922520128
+    ns, pp, nv, nc, cp = d[name]["params"]
+    mats = list(O.iter_system_matrix(int(ns), pp, int(nv), int(nc), cp, workers=workers))
+    assert _digest(mats) == d[name]["sha256"]
+
+
+def test_reference_arm_scan_equals_gpu_arm_scan():
+    """bench.reference_scan (oracle tracer + gen recipe, no CUDA library) yields bit-identical y and
+    weights to gen.make_scan (the GPU arm's), so both arms solve the same problem."""
+    import bench
+
+    from paper_1911_09278_b200 import gen
+
+    _, _, mats_r, y_r, lam_r = bench.reference_scan(0, workers=4)
+    _, mats_g, _, y_g, lam_g = gen.make_scan(0)
+    assert np.array_equal(y_r, y_g) and np.array_equal(lam_r, lam_g)
+    assert all(np.array_equal(a.cols, b.cols) and np.array_equal(a.lens, b.lens) for a, b in zip(mats_r, mats_g))
