@@ -187,12 +187,13 @@ def algorithmic_bytes_per_pass(plan, n_agents_local) -> tuple[int, dict]:
 
 
 def k2_traffic(config, sv):
-    """dram read + write bytes per K2 launch from the committed ncu --set full capture (profiles/)."""
+    """dram read + write bytes per K2 launch from the committed ncu --set full captures (profiles/)."""
     try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "r01_k2_traffic.json")))
+        t = json.load(open(os.path.join(ROOT, "profiles", "r02_k2_traffic.json")))
     except (OSError, ValueError):
         return None
-    return t["dram_bytes_per_launch"] if t.get("config") == config and t.get("sv_side") == sv else None
+    e = t.get(str(config))
+    return e["dram_bytes_per_launch"] if e and e.get("sv_side") == sv else None
 
 
 def run_cpu_test(args):
@@ -279,6 +280,9 @@ def run_ours(args):
         if pnp:
             den._load(plan)
 
+    graph_cache = {}
+    graphs = True
+
     def solve_device():
         """one step with inputs resident: stack init, X0 = average(w0), refresh e, `iters` iterations"""
         plan.stack_init(None, N if world == 1 else 0)
@@ -295,9 +299,21 @@ def run_ours(args):
             plan.iterate(iters, 0, 0.8, pnp, 1e-300, N, False, device_denoise=pnp)
         elif peer:  # consensus over NVLink peer memory, the whole loop on the device
             plan.iterate_peer(iters, 0, 0.8, pnp, 1e-300, N, device_denoise=pnp)
-        else:
+        else:  # NCCL all-reduce on the library stream; whole blocks of iterations replayed as CUDA graphs
             c = mb.mace._resolve_comm(True)
-            for k in range(iters):
+            G = mb.mace.GRAPH_BLOCK
+            k = 0
+            if graphs and G > 0:
+                plan.reserve_log(iters)
+                while k + G <= iters:
+                    plan.set_iter(k)
+                    if "g" not in graph_cache:
+                        graph_cache["g"] = mb.mace._capture_block(plan, c, plan.torch_stream(), G, 0.8, pnp, N,
+                                                                  1e-300, den)
+                    mb.mace._replay(graph_cache["g"], plan.torch_stream())
+                    plan.add_passes(G)
+                    k += G
+            for k in range(k, iters):
                 plan.iterate_local(0.8, pnp)
                 c.allreduce(*plan.comm_arrays(), stream=plan.torch_stream())
                 plan.iterate_finish(N, 1e-300, k)
@@ -330,6 +346,12 @@ def run_ours(args):
         barrier()
     k2_ms, k2_launches = plan.k2_timing(False)
     ms = ev0.elapsed_time(ev1)
+    if world > 1 and k2_launches < iters * args.steps:  # graph replays carry no K2 events: one timed eager solve
+        graphs = False
+        plan.k2_timing(True)
+        solve_device()
+        k2_ms, k2_launches = plan.k2_timing(False)
+        graphs = True
     lg, done = plan.read_log(iters)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
@@ -379,7 +401,7 @@ def run_ours(args):
                      "frac": achieved / pk.get("hbm_gbs"), "traffic": k2_traffic(args.config, args.sv),
                      "kernel": "k_icd_sv (K2)", "records": "weighted" if plan.info().get("weighted") else "plain",
                      "bytes_per_launch": alg, "layout_bytes_per_launch": lay["layout_bytes"],
-                     "k2_avg_ms": k2_avg_ms, "k2_share": k2_ms / ms, "c_mean": lay["c_mean"],
+                     "k2_avg_ms": k2_avg_ms, "k2_share": k2_avg_ms * iters * args.steps / ms, "c_mean": lay["c_mean"],
                      "peak_source": "MEASURED_PEAKS.json" if not pk.get("_fallback") else "fallback"},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
@@ -475,9 +497,9 @@ def cpu_baseline(config, mats, y, lam, sample_iters=2, threads=None):
     ns = int(np.sqrt(mats[0].n_pixels))
     prior = O.Prior("qggmrf", cfg["beta"], 2.0, 1.2, 1.0, 0.01)
     agents = O.build_agents(mats, y, lam, N, cfg["sigma"], prior, ns, workers=threads)
-    O.mace_run(agents, 1, 0.8, workers=threads)  # warm-up
+    run = O.mace_run(agents, 1, 0.8, workers=threads)  # warm-up: initialisation + first iteration
     t0 = time.perf_counter()
-    run = O.mace_run(agents, sample_iters, 0.8, workers=threads)
+    run = O.mace_run(agents, sample_iters, 0.8, w0=run.stack, workers=threads, resume=True)
     dt = time.perf_counter() - t0
     n = ns * ns
     return {"value": N * n * len(run.relnorms) / dt, "unit": UNIT, "cores": threads, "kind": "port",
@@ -531,13 +553,14 @@ def run_reference(args):
     agents = O.build_agents(mats, y, lam, N, cfg["sigma"], prior, ns, workers=threads)
     del mats
     t_setup = time.time() - t0
-    per_step = max(1, args.cpu_iters)
+    per_step = max(1, args.cpu_iters if args.config < 2 else 1)  # config 2: ~3 s per iteration on 16 cores
+    run = O.mace_run(agents, 1, 0.8, workers=threads)  # the solve's initialisation and first iteration
     for _ in range(args.warmup):
-        O.mace_run(agents, 1, 0.8, workers=threads)
+        run = O.mace_run(agents, 1, 0.8, w0=run.stack, workers=threads, resume=True)
     t0 = time.perf_counter()
     done = 0
-    for _ in range(args.steps):
-        run = O.mace_run(agents, per_step, 0.8, workers=threads)
+    for _ in range(args.steps):  # steady-state iterations of one continuing solve
+        run = O.mace_run(agents, per_step, 0.8, w0=run.stack, workers=threads, resume=True)
         done += len(run.relnorms)
     dt = time.perf_counter() - t0
     n = ns * ns
@@ -549,8 +572,8 @@ def run_reference(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded ellipse phantom, "
             "Poisson counts; gen.py recipe, oracle tracer)", "impl": "reference",
             "config": {"workload": f"BASELINE config {args.config}: {ns}^2, {y.shape[0]} views x {y.shape[1]} ch, "
-                       f"N={N} agents; each step = {per_step} MACE iteration(s) (bounded sample of the "
-                       f"{cfg['iters']}-iteration solve)"},
+                       f"N={N} agents; each step = {per_step} MACE iteration(s) of one continuing solve "
+                       f"(bounded sample of the {cfg['iters']}-iteration solve)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": f"{per_step} MACE iteration(s) per step, oracle/sweep.c float64 raster "
                                        f"ICD, agents over {threads} threads of {cores}"},

@@ -93,6 +93,9 @@ int mace_set_agent_params(void* ctx, int local, double beta_eff, double inv_sigm
  * super-voxel contexts with every weight > 0 switch K2 to weighted records (a sqrt(lambda),
  * error sinogram kept as sqrt(lambda) e; mace_get_error still returns e); refresh e afterwards. */
 int mace_load_data(void* ctx, const float* y, const float* lam);
+/* mace_load_data returns before its host->device copies finish (host pointers may be pinned
+ * staging); mace_stage_wait blocks until they have read the host buffers */
+int mace_stage_wait(void* ctx);
 /* allow (1, default) or forbid (0) weighted records from the next mace_load_data on */
 int mace_set_weighting(void* ctx, int allow);
 
@@ -132,7 +135,13 @@ int mace_iterate_local(void* ctx, double rho, int use_g);
 int mace_comm_buffers(void* ctx, void** wsum, void** sums5);
 int mace_local_sum(void* ctx);
 int mace_mean_from_sum(void* ctx, int n_total);
+/* iter < 0: log row = the device iteration counter (mace_set_iter), advanced by one per call, so a
+ * loop of iterate_local / all-reduce / iterate_finish can be captured in a CUDA graph and replayed */
 int mace_iterate_finish(void* ctx, int n_total, double tol, int iter);
+int mace_set_iter(void* ctx, int iter);
+int mace_reserve_log(void* ctx, int n);
+/* host pass counter (schedules the error refresh every 50 passes): += add, *out = new value */
+int mace_passes(void* ctx, int64_t add, int64_t* out);
 /* the same loop with the consensus exchanged over NVLink peer memory (k_peer.cuh) instead of a
  * collective: bytes of the symmetric buffer each rank allocates; setup with every rank's buffer
  * pointer; stack-average initialisation; `iters` iterations entirely on the device. */

@@ -41,6 +41,10 @@ _SIGS = {
     "mace_setup_agents": (c_int, [P, c_int, P, P, c_int, c_int, c_int, c_int, c_int]),
     "mace_set_schedule": (c_int, [P, c_double, c_int64]),
     "mace_set_agent_groups": (c_int, [P, c_int]),
+    "mace_stage_wait": (c_int, [P]),
+    "mace_set_iter": (c_int, [P, c_int]),
+    "mace_reserve_log": (c_int, [P, c_int]),
+    "mace_passes": (c_int, [P, c_int64, P]),
     "mace_prox_all": (c_int, [P, P, P, c_int, c_double, P, P]),
     "mace_set_agent_params": (c_int, [P, c_int, c_double, c_double, c_int]),
     "mace_load_data": (c_int, [P, P, P]),

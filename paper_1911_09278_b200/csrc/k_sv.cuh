@@ -139,6 +139,9 @@ __device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __
         asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(B.ob[p]) : "l"(r + p * RECW + NG * 32 * K));
 }
 
+#ifndef MACE_K2_NORELOAD
+#define MACE_K2_NORELOAD 1  // scatter from registers (no band reloads), see step()
+#endif
 #ifndef MACE_K2_MINB
 #define MACE_K2_MINB 12  // resident warps per SM the register budget is sized for
 #endif
@@ -338,7 +341,11 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
             }
             // theta1 partials against the band as it stands before the batch
             float num[4];
+#if MACE_K2_NORELOAD
+            float gv[4][NG][K];  // every pixel's rows as gathered (before the batch touched them)
+#else
             float e0v[NG][K];  // pixel 0's rows as gathered (nothing in the batch has touched them yet)
+#endif
             int ab[4][NG];
             const auto& av = C.a;
 #pragma unroll
@@ -353,7 +360,11 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
 #pragma unroll
                     for (int q = 0; q < K; ++q) {
                         const float ee = sb[ab[p][g] + q * U];
+#if MACE_K2_NORELOAD
+                        gv[p][g][q] = ee;
+#else
                         if (p == 0) e0v[g][q] = ee;
+#endif
                         // kW: a' = a sqrt(lambda) against e' = sqrt(lambda) e
                         const float al = kW ? av[p][g][q] : av[p][g][q] * sb[ab[p][g] + q * U + 32];
                         if (q & 1) a1 = fmaf(al, ee, a1);
@@ -473,6 +484,33 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
                 if (lane < 4 && okw) zt[cw] = zn;
                 __syncwarp();
             }
+#if MACE_K2_NORELOAD
+            // scatter e -= alpha_p a_p in pixel order without reading the band back: pixel p's rows
+            // start from their gathered values, take the updates of the earlier batch pixels that
+            // share them (row (p, k) == row (q, k') iff the slots' window offsets differ by k' - k,
+            // i.e. ab[p] - ab[q] == (k' - k) U; a row is never shared within one pixel), then its
+            // own: the same operations in the same order as updating the band pixel by pixel, and
+            // the last store to a shared row carries every update
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    float ev[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) ev[k] = gv[p][g][k];
+#pragma unroll
+                    for (int q = 0; q < p; ++q) {
+                        const int d = ab[p][g] - ab[q][g];
+#pragma unroll
+                        for (int k = 0; k < K; ++k)
+#pragma unroll
+                            for (int k2 = 0; k2 < K; ++k2)
+                                if (d == (k2 - k) * U) ev[k] = fmaf(-alpha[q], av[q][g][k2], ev[k]);
+                    }
+#pragma unroll
+                    for (int k = 0; k < K; ++k) sb[ab[p][g] + k * U] = fmaf(-alpha[p], av[p][g][k], ev[k]);
+                }
+#else
             // scatter e -= alpha_p a_p in pixel order (a row may be shared within the batch, never
             // within one pixel): pixel 0 from the gathered values, then reload-modify-store
 #pragma unroll
@@ -491,6 +529,7 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
 #pragma unroll
                     for (int q = 0; q < K; ++q) sb[ab[p][g] + q * U] = fmaf(-alpha[p], av[p][g][q], ev[g][q]);
             }
+#endif
         };
         if (full) {
 #pragma unroll 1

@@ -637,11 +637,16 @@ __global__ void k_norms(const double* part, int n_items, const double* ref_part,
     }
 }
 
+__global__ void k_set_int(int* p, int v) { *p = v; }
+
 // relnorm, divergence and stop test (mace.py:309-318,337-339); log row [relnorm, |w'|, sum a^2, nrmse^2]
+// ctr != nullptr: the iteration index comes from (and advances) a device counter, so a CUDA graph of
+// several iterations needs no per-iteration host argument
 __global__ void k_finish(const double* sums5, double ref_norm2, double tol, int iter, double* log, int* done,
-                         unsigned* head)
+                         unsigned* head, int* ctr = nullptr)
 {
     if (*done) return;
+    if (ctr) iter = (*ctr)++;
     const double dw2 = sums5[1], wn2 = sums5[2], wo2 = sums5[3];
     const double nn = sqrt(wn2);
     const double rel = sqrt(dw2) / fmax(sqrt(wo2), 1e-300);

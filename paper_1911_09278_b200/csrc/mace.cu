@@ -107,6 +107,7 @@ struct Ctx {
     DBuf<int> done;
     DBuf<double> sums5, log, norm_scratch;
     DBuf<unsigned> norm_counter;
+    DBuf<int> iter_ctr;  // device iteration index (mace_iterate_finish with iter < 0: graph-captured loops)
     int log_cap = 0;
     DBuf<float> wbar, g, ref, wsum;
     DBuf<double> refpart;
@@ -124,6 +125,7 @@ struct Ctx {
     int num_sms = 148;
     // timing of the last iterate call
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_stage = nullptr;  // after the last H2D read of the caller's staging buffer (mace_load_data)
     // K5 PnP denoiser (cnn.cu)
     Cnn cnn;
     // consensus across ranks over NVLink peer memory (k_peer.cuh), set up by mace_peer_setup
@@ -148,6 +150,9 @@ struct Ctx {
 static cudaEvent_t k2_begin(Ctx* c)
 {
     if (!c->time_k2) return nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(c->stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;  // launches captured into a graph are not timed
     if (c->k2_used == c->k2ev.size()) {
         std::pair<cudaEvent_t, cudaEvent_t> e;
         CK(cudaEventCreate(&e.first));
@@ -463,6 +468,7 @@ int mace_ctx_create(int device, void** out)
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
+    CK(cudaEventCreateWithFlags(&c->ev_stage, cudaEventDisableTiming));
     c->head.alloc(1);
     c->done.alloc(2);
     c->sums5.alloc(5);
@@ -484,6 +490,7 @@ void mace_ctx_destroy(void* p)
     if (c->own_stream) cudaStreamDestroy(c->stream);
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);
+    if (c->ev_stage) cudaEventDestroy(c->ev_stage);
     delete c;
 }
 
@@ -861,6 +868,7 @@ int mace_load_data(void* p, const float* y, const float* lam)
     }
     CK(cudaMemcpyAsync(c->y.p, y, sizeof(float) * total, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->lam.p, lam, sizeof(float) * total, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaEventRecord(c->ev_stage, c->stream));  // the host buffers may be reused once this completes
     if (c->n_local) {
         // weighted records need one lambda per record (a single slice) and lambda > 0 everywhere,
         // so that e = e' / sqrt(lambda) stays recoverable (mace_get_error)
@@ -877,6 +885,15 @@ int mace_load_data(void* p, const float* y, const float* lam)
         CK(cudaGetLastError());
         compute_theta2(c);
     }
+    API_END
+}
+
+// wait until the last mace_load_data has finished reading its host buffers (a pinned staging
+// buffer may then be refilled; the copies themselves run asynchronously)
+int mace_stage_wait(void* p)
+{
+    API_BEGIN
+    CK(cudaEventSynchronize(C(p)->ev_stage));
     API_END
 }
 
@@ -1399,16 +1416,51 @@ int mace_mean_from_sum(void* p, int n_total)
     API_END
 }
 
+// iter < 0: the log row is the device iteration counter (mace_set_iter), which advances by one: a
+// loop of iterate_local / all-reduce / iterate_finish can then be captured in a CUDA graph once and
+// replayed (reserve the log first with mace_reserve_log; no allocation happens here)
 int mace_iterate_finish(void* p, int n_total, double tol, int iter)
 {
     API_BEGIN
     Ctx* c = C(p);
-    ensure_log(c, iter + 1);
+    if (iter >= 0) ensure_log(c, iter + 1);
+    else if (!c->iter_ctr.p) throw std::runtime_error("mace_set_iter first");
     k_consensus<1><<<kRefBlocks, 256, 0, c->stream>>>(c->wsum.p, 1, c->n, (float)n_total, c->wbar.p, nullptr, nullptr,
                                                    c->done.p, c->n_slices);
-    k_finish<<<1, 1, 0, c->stream>>>(c->sums5.p, 0.0, tol, iter, c->log.p, c->done.p, c->head.p);
+    k_finish<<<1, 1, 0, c->stream>>>(c->sums5.p, 0.0, tol, iter < 0 ? 0 : iter, c->log.p, c->done.p, c->head.p,
+                                     iter < 0 ? c->iter_ctr.p : nullptr);
     if (c->passes % 50 == 0) refresh(c, 0, c->n_local);
     CK(cudaGetLastError());
+    API_END
+}
+
+// device iteration counter for mace_iterate_finish(iter < 0); stream-ordered
+int mace_set_iter(void* p, int iter)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (!c->iter_ctr.p) c->iter_ctr.alloc(1);
+    k_set_int<<<1, 1, 0, c->stream>>>(c->iter_ctr.p, iter);
+    CK(cudaGetLastError());
+    API_END
+}
+
+// room for n log rows (before capturing iterations in a graph: nothing may allocate inside it)
+int mace_reserve_log(void* p, int n)
+{
+    API_BEGIN
+    ensure_log(C(p), n);
+    API_END
+}
+
+// host pass counter (it schedules the error refresh every 50 passes): += add; *out = the new count.
+// Replays of a captured graph run passes the host never counted.
+int mace_passes(void* p, int64_t add, int64_t* out)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    c->passes += add;
+    if (out) *out = c->passes;
     API_END
 }
 

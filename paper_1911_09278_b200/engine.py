@@ -205,6 +205,8 @@ class AgentPlan(_Context):
             N.check(self.L.mace_host_alloc(2 * rows * 4, ctypes.byref(p)), "host_alloc")
             self._pin = p
             self._pin_arr = np.ctypeslib.as_array((ctypes.c_float * (2 * rows)).from_address(p.value))
+        else:  # the previous load's copies may still be reading the staging buffer
+            self.call("mace_stage_wait")
         for k, src in enumerate((y, weights)):
             dst = self._pin_arr[k * rows:(k + 1) * rows]
             if isinstance(src, (list, tuple)):  # per-slice arrays straight into their staging slots
@@ -375,6 +377,18 @@ class AgentPlan(_Context):
     def iterate_finish(self, n_total, tol, it):
         """after the all-reduce of comm_arrays() on torch_stream() (stream-ordered, no host sync)"""
         self.call("mace_iterate_finish", int(n_total), float(tol), int(it))
+
+    def set_iter(self, it):
+        """device iteration counter for iterate_finish(..., it=-1) (graph-captured loops)"""
+        self.call("mace_set_iter", int(it))
+
+    def reserve_log(self, n):
+        self.call("mace_reserve_log", int(n))
+
+    def add_passes(self, k) -> int:
+        out = ctypes.c_int64(0)
+        self.call("mace_passes", int(k), ctypes.byref(out))
+        return out.value
 
     def read_log(self, n):
         lg = np.zeros((max(n, 1), 4), np.float64)

@@ -19,6 +19,7 @@ never calls them.
 from __future__ import annotations
 
 import inspect
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -413,7 +414,8 @@ def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=
         while it < config.max_outer and done[0] == 0:
             k = min(chunk, config.max_outer - it)
             in_loop = pnp and hasattr(denoiser, "_load")  # the K5 CNN: H inside the device loop
-            if pnp and (ref_image is not None or not in_loop):  # per-iteration host step
+            host_nr = ref_image is not None and (pnp or peer)  # NRMSE from the image on the host
+            if host_nr or (pnp and not in_loop):  # per-iteration host step
                 k = 1
             if in_loop:
                 denoiser._load(plan)
@@ -430,8 +432,8 @@ def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=
             lim = it if done[0] == 0 else (done[1] if done[0] == 1 else done[1] - 1)
             for j in range(len(rows), lim):
                 nr = None
-                if ref_image is not None:
-                    nr = lg[j, 3] if not pnp else nrmse(plan.get_image(1), ref_image)
+                if ref_image is not None:  # the device log holds the NRMSE only for a single context
+                    nr = nrmse(plan.get_image(1 if pnp else 0), ref_image) if host_nr else lg[j, 3]
                 rows.append((lg[j, 0], nr, wall * (j + 1) / it))
     else:
         # multi-rank (or host-denoiser) loop: K2 + local sum -> all-reduce on the library stream ->
@@ -441,7 +443,28 @@ def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=
         stream = _plan_stream(plan)
         per_iter_host = ref_image is not None or (pnp and not device_g)
         k = 0
-        while k < config.max_outer:
+        if comm is not None and stream is not None and not per_iter_host and GRAPH_BLOCK > 0:
+            # whole blocks of GRAPH_BLOCK iterations as one CUDA graph (captured once, replayed): one
+            # host call per block instead of ~4 launches and a collective per iteration
+            plan.reserve_log(config.max_outer)
+            graph = None
+            while k + GRAPH_BLOCK <= config.max_outer:
+                plan.set_iter(k)
+                if graph is None:
+                    graph = _capture_block(plan, comm, stream, GRAPH_BLOCK, config.rho, pnp, N, config.tol,
+                                           denoiser)
+                _replay(graph, stream)
+                plan.add_passes(GRAPH_BLOCK)
+                k += GRAPH_BLOCK
+                lg, done = plan.read_log(k)
+                it = k
+                wall = time.perf_counter() - t0
+                lim = k if done[0] == 0 else (done[1] if done[0] == 1 else done[1] - 1)
+                for j in range(len(rows), lim):
+                    rows.append((lg[j, 0], None, wall * (j + 1) / k))
+                if done[0]:
+                    break
+        while k < config.max_outer and done[0] == 0:
             plan.iterate_local(config.rho, pnp)
             if comm is not None:
                 comm.allreduce(*plan.comm_arrays(), stream=stream)
@@ -486,6 +509,36 @@ def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=
         raise ConvergenceError(f"MACE: Mann update relnorm did not reach {config.tol:g} in {config.max_outer} "
                                "iterations", last_iterate=result, log=log)
     return result
+
+
+# iterations per captured CUDA graph in the multi-rank loop (0: launch every iteration from the host);
+# 50 = the error-refresh period, so every replay carries exactly one refresh at the same place
+GRAPH_BLOCK = int(os.environ.get("MACE_GRAPH_BLOCK", "50"))
+
+
+def _capture_block(plan, comm, stream, G, rho, pnp, N, tol, denoiser):
+    """G multi-rank MACE iterations (K2 + local sum -> all-reduce -> finish [-> K5]) captured into a
+    CUDA graph on the library stream; the log rows come from the device iteration counter.  The
+    capture executes nothing, so the host pass count it advanced is taken back."""
+    import torch
+
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+        for _ in range(G):
+            plan.iterate_local(rho, pnp)
+            comm.allreduce(*plan.comm_arrays(), stream=stream)
+            plan.iterate_finish(N, tol, -1)
+            if pnp:
+                _apply_denoiser(plan, denoiser)
+    plan.add_passes(-G)
+    return g
+
+
+def _replay(graph, stream):
+    import torch
+
+    with torch.cuda.stream(stream):
+        graph.replay()
 
 
 def _fill_log(log, rows, counter, N, n):

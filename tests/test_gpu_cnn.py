@@ -86,10 +86,12 @@ def _bf16_rne_f64(v):
 def test_cnn_one_layer_bf16_rounding(h, w, layer, seed):
     """One 64->64 layer alone (tcgen05 UMMAs, fp32 accumulation in TMEM, ReLU, bf16 epilogue) on a
     fixed bf16 input against the exact fp64 conv rounded once to bf16.  At least 99.9% of the
-    outputs must be bit-identical and every other one exactly one bf16 ulp away AND explained by
+    outputs must be bit-identical and every other one explained by one fp32 accumulation plus one
+    rounding: one bf16 ulp away and
     a near-tie: the exact value within the fp32 accumulation bound (576 terms x 2^-24 x sum|terms|)
-    of the midpoint between its two bf16 neighbours.  A wrong tap, channel, K-step or fragment
-    order would break the count by orders of magnitude."""
+    of the midpoint between its two bf16 neighbours, or (more than one ulp) an output that cancels
+    far below its terms, where the fp32 bound exceeds the output's own ulp.  A wrong tap, channel,
+    K-step or fragment order would break the count by orders of magnitude."""
     from paper_1911_09278_b200.denoisers import from_bf16_bits, to_bf16_bits
 
     rng = np.random.default_rng(seed)
@@ -123,10 +125,15 @@ def test_cnn_one_layer_bf16_rounding(h, w, layer, seed):
           f"{tie.max() if tie.size else 0:.3e}; ReLU mismatch / bound max "
           f"{(np.abs(got - ref)[relu] / bound[relu]).max() if relu.any() else 0:.3e}")
     assert frac >= 0.999, frac
-    assert np.all(np.abs(got - ref)[relu] <= bound[relu] + 1e-30)
-    assert np.all(ulps <= 1.0 + 1e-6)
-    # every other mismatch sits next to the midpoint between its two bf16 neighbours
-    assert np.all(tie <= 1.0)
+    # every mismatch is one fp32 accumulation (|sum - exact| <= bound) plus one rounding to bf16
+    ulp_got = np.ldexp(1.0, np.frexp(np.maximum(np.abs(got), 1e-30))[1] - 8)
+    assert np.all((np.abs(got - exact.clip(min=0.0)) <= 0.5 * ulp_got + bound)[bad])
+    # more than one ulp apart only where the output cancels far below its terms (bound >= ulp)
+    far = np.zeros_like(bad)
+    far[rnd] = ulps > 1.0 + 1e-6
+    assert np.all(bound[far] >= ulp[far]), (bound[far] / ulp[far]).min()
+    # the one-ulp ones sit next to the midpoint between their two bf16 neighbours
+    assert np.all(tie[ulps <= 1.0 + 1e-6] <= 1.0)
 
 
 def test_cnn_config3_weights_run():

@@ -24,7 +24,7 @@ from paper_1911_09278_b200 import gen
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("config,iters", [(0, 1500), (1, 3000)])
+@pytest.mark.parametrize("config,iters", [(0, 1500), (1, 3000), (2, 8000)])
 def test_fixed_point_matches_cpu_oracle_map(config, iters):
     c = gen.CONFIGS[config]
     ref = np.load(os.path.join(GOLDEN, f"central_c{config}.npz"))

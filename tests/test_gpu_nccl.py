@@ -87,11 +87,22 @@ def test_peer_memory_consensus_matches_device_loop():
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", world_size=1, rank=0,
                             device_id=torch.device("cuda:0"))
+    x_ref = ref.image + 0.01 * np.sin(np.arange(ref.image.size))  # any reference image
     try:
         got = solve(mb.PeerComm())
         again = solve(mb.PeerComm())  # a second solve on the same plan re-attaches cleanly
+        try:
+            with_ref = mb.mace_solve(prob, mb.MaceConfig(n_subsets=N, rho=0.8, sigma=2e-4, max_outer=20, tol=1e-300,
+                                                         residuals="none", schedule="raster"),
+                                     comm=mb.PeerComm(), ref_image=x_ref)
+        except mb.ConvergenceError as err:
+            with_ref = err.last_iterate
     finally:
         dist.destroy_process_group()
+    # NRMSE against ref_image on the peer path (it used to log -1)
+    nr = [r["nrmse"] for r in with_ref.log.rows]
+    assert len(nr) == 20 and all(v is not None and v > 0 for v in nr)
+    assert nr[-1] == pytest.approx(mb.nrmse(with_ref.image, x_ref), rel=1e-5)
     assert got.iterations == ref.iterations == 150
     assert np.array_equal(got.image, ref.image)
     assert np.array_equal(got.stack, ref.stack)
