@@ -104,6 +104,10 @@ int mace_get_state(void* ctx, int local, float* x);
 int mace_get_error(void* ctx, int local, float* e);
 int mace_get_theta2(void* ctx, int local, float* th);
 int mace_refresh(void* ctx, int local);
+/* super-voxel batch constants of a local agent, [n_sv][batches][16] floats: theta2 of the batch's
+ * four slots, then c01 c02 c03 c12 c13 c23 (sum a_i a_j lambda over shared rows); out may be NULL
+ * to query *count */
+int mace_get_batch_consts(void* ctx, int local, float* out, int64_t* count);
 /* n_passes passes over pixels [s_begin, s_end) (s_end < 0: all; ranges need the raster schedule) */
 int mace_pass(void* ctx, int local, const float* v, int n_passes, int64_t s_begin, int64_t s_end, double* dsq);
 

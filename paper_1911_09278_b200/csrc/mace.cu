@@ -944,6 +944,23 @@ int mace_get_theta2(void* p, int local, float* th)
     API_END
 }
 
+// the super-voxel batch constants of local agent `local` (k_sv_consts): [n_sv][nb][16] floats =
+// theta2 of the batch's four slots, cross terms c01 c02 c03 c12 c13 c23, 6 unused
+int mace_get_batch_consts(void* p, int local, float* out, int64_t* count)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (c->schedule != 0) throw std::runtime_error("batch constants need the super-voxel schedule");
+    const AgentMem& m = *c->am.at(local % c->n_real);
+    const size_t cnt = (size_t)m.n_sv * m.nb * 16;
+    if (count) *count = (int64_t)cnt;
+    if (out) {
+        CK(cudaMemcpyAsync(out, c->h_agents.at(local).bc, sizeof(float) * cnt, cudaMemcpyDeviceToHost, c->stream));
+        sync(c);
+    }
+    API_END
+}
+
 int mace_refresh(void* p, int local)
 {
     API_BEGIN

@@ -275,6 +275,15 @@ class AgentPlan(_Context):
         self.call("mace_get_theta2", int(local), N.ptr(out))
         return out
 
+    def get_batch_consts(self, local) -> np.ndarray:
+        """(n_sv, batches, 16) float32: k_sv_consts' theta2 x4 and cross terms of each 4-pixel batch"""
+        cnt = ctypes.c_int64(0)
+        self.call("mace_get_batch_consts", int(local), None, ctypes.byref(cnt))
+        out = np.empty(cnt.value, np.float32)
+        self.call("mace_get_batch_consts", int(local), N.ptr(out), ctypes.byref(cnt))
+        info = self.agent_info(local % self.n_agents)
+        return out.reshape(info["n_sv"], -1, 16)
+
     def refresh(self, local=-1):
         self.call("mace_refresh", int(local))
 

@@ -159,3 +159,65 @@ def test_sv_consts_theta2_matches_oracle(golden, sv_side, weighted, monkeypatch)
             got = plan.get_theta2(i)
             assert rel(got, ref) < 1e-5, (i, rel(got, ref))
     engine.clear_cache()
+
+
+def _slot_pixel(S, t):
+    """internal.h sv_slot_pixel: visit-order slot t of an S x S tile -> local pixel, -1 for padding"""
+    h = S // 2
+    per_class = h * h
+    bpc = (per_class + 3) // 4
+    b, cls = t // 4, (t // 4) // bpc
+    i = (b % bpc) * 4 + t % 4
+    if i >= per_class:
+        return -1
+    return ((cls >> 1) + 2 * (i // h)) * S + (cls & 1) + 2 * (i % h)
+
+
+@pytest.mark.parametrize("sv_side", [8, 16])
+@pytest.mark.parametrize("weighted", [True, False])
+def test_sv_consts_cross_terms_match_oracle(golden, sv_side, weighted, monkeypatch):
+    """k_sv_consts' batch constants read back: for every batch of every tile, theta2 of
+    the four slots and the six cross terms c_ij = sum_r a_ir a_jr lambda_r = (A^T diag(lambda) A)[p_i, p_j]
+    against the oracle CSR, tile sides 8 and 16 (16 and 64 batches per tile, so the next-batch
+    prefetch runs for every warp), weighted and plain records."""
+    import scipy.sparse as sp
+
+    prob = _ellipse_problem(golden)
+    monkeypatch.setenv("MACE_WEIGHTED", "1" if weighted else "0")
+    engine.clear_cache()
+    views = [tuple(s.view_indices) for s in mb.partition_views(prob.geom.n_views, 4)]
+    plan = engine.plan_for(prob.matrices, views, schedule="sv", sv=sv_side)
+    plan.load_data(golden["ell_y"], golden["ell_w"])
+    assert bool(plan.info()["weighted"]) == weighted
+    ns = prob.geom.n_side
+    wv = np.asarray(golden["ell_w"], np.float64).reshape(prob.geom.n_views, -1)
+    nss = -(-ns // sv_side)
+    pairs = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
+    checked = 0
+    for i, vs in enumerate(views[:2]):
+        A = sp.vstack([O.view_csr(prob.matrices[v]) for v in vs]).tocsc()
+        lam = np.concatenate([wv[v] for v in vs])
+        M = (A.T @ sp.diags(lam) @ A).tocsr()  # n x n, exact in float64
+        bc = plan.get_batch_consts(i)
+        assert bc.shape[0] == nss * nss
+        for sv in range(bc.shape[0]):
+            r0, c0 = (sv // nss) * sv_side, (sv % nss) * sv_side
+            for b in range(bc.shape[1]):
+                px = []
+                for p in range(4):
+                    k = _slot_pixel(sv_side, 4 * b + p)
+                    r, c = (r0 + k // sv_side, c0 + k % sv_side) if k >= 0 else (ns, ns)
+                    px.append(r * ns + c if (r < ns and c < ns) else -1)
+                ref = np.zeros(10)
+                for p in range(4):
+                    if px[p] >= 0:
+                        ref[p] = M[px[p], px[p]]
+                for j, (p, q) in enumerate(pairs):
+                    if px[p] >= 0 and px[q] >= 0:
+                        ref[4 + j] = M[px[p], px[q]]
+                got = bc[sv, b, :10].astype(np.float64)
+                scale = max(np.abs(ref[:4]).max(), 1e-30)
+                assert np.abs(got - ref).max() <= 1e-5 * scale, (sv, b, got, ref)
+                checked += 1
+    print(f"sv {sv_side} weighted {weighted}: {checked} batches checked")
+    engine.clear_cache()
