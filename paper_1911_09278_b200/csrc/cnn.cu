@@ -489,6 +489,346 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAccCols) : "memory");
 }
 
+// All 15 middle layers in ONE persistent launch (k_conv64_seq): every CTA keeps its (strip, row run)
+// for the whole stack, its TMEM allocation and barriers live across layers, and the halo-row ring,
+// accumulator pair ring and mbarrier phases simply continue from layer to layer.  Layer l reads
+// act[l % 2] and writes act[(l + 1) % 2].  Between layers a CTA waits only for its 3 x 3
+// neighbourhood: after its epilogue warps have stored a layer's rows (and fenced them), one thread
+// publishes flags[cta] = 16 epoch + l + 1 (release); before loading halo rows for layer l the TMA
+// thread acquires flags >= 16 epoch + l of itself and its neighbours, then a proxy fence orders the
+// TMA (async proxy) reads after those generic-proxy writes.  Because a neighbour's flag for layer l - 1
+// also means it has finished READING act[(l - 1) % 2] = the buffer layer l overwrites, the same wait
+// covers the write-after-read hazard.  The next layer's 72 KB of weights are copied in as soon as
+// the MMA issuer has committed the layer's last UMMA (wfree).  Launched cooperatively (all CTAs
+// co-resident: one per SM), so the spin-waits cannot deadlock.  Measured SLOWER than 15 launches with
+// programmatic dependent launch (0.333 vs 0.277 ms per 512^2 denoise on B200), so it is an option
+// (MACE_K5_SEQ=1), bit-identical to the default (tests/test_gpu_cnn.py); DESIGN.md §6.
+__device__ __forceinline__ void flag_wait_ge(const int* f, int v)
+{
+    int x;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(x) : "l"(f) : "memory");
+        if (x >= v) break;
+    }
+}
+
+__global__ void __launch_bounds__(192, 1) k_conv64_seq(const __grid_constant__ CUtensorMap map0,
+                                                       const __grid_constant__ CUtensorMap map1,
+                                                       const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* act0,
+                                                       __nv_bfloat16* act1, int H, int W, int Wp, int rows_per_cta,
+                                                       int n_layers, int* flags, int epoch)
+{
+    constexpr int R = 2;
+    extern __shared__ __align__(1024) unsigned char sm[];
+    unsigned char* sw = sm;
+    unsigned char* slots = sm + kWBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + kSlots * kSlotBytes);
+    uint64_t* wbar = bars;
+    uint64_t* sfull = bars + 1;
+    uint64_t* sempty = sfull + kSlots;
+    uint64_t* afull = sempty + kSlots;  // [2] accumulator pair ready
+    uint64_t* aempty = afull + 2;       // [2] accumulator pair drained
+    uint64_t* wfree = aempty + 2;       // the layer's last UMMA completed: weights may be replaced
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfree + 1);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int strips = (W + kTileX - 1) / kTileX;
+    const int strip = blockIdx.x % strips, rb = blockIdx.x / strips;
+    const int x0 = strip * kTileX;
+    const int y0 = rb * rows_per_cta;
+    const int y1 = min(H, y0 + rows_per_cta);
+    const int n_rb = (H + rows_per_cta - 1) / rows_per_cta;
+    if (y0 >= H) return;  // never: the grid is exactly strips x n_rb
+    const int n_units = (y1 - y0 + R - 1) / R;
+    const int rows_l = y1 - y0 + 2;  // halo rows per layer (y0 - 1 .. y1)
+    constexpr int kAccCols = 256;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(tmem_slot)),
+                     "n"(kAccCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 32) {
+        mbar_init(wbar, 1);
+        mbar_init(wfree, 1);
+        for (int i = 0; i < kSlots; ++i) {
+            mbar_init(sfull + i, 1);
+            mbar_init(sempty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(afull + i, 1);
+            mbar_init(aempty + i, 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const int rbase = y0 - 1;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            long q0 = 0;
+            for (int l = 0; l < n_layers; ++l) {
+                if (l > 0) mbar_wait(wfree, (uint32_t)((l - 1) & 1));
+                mbar_expect(wbar, kWBytes);
+                bulk_copy(sw, wts + (size_t)l * 9 * kC * kC, kWBytes, wbar);
+                if (l > 0) {  // the neighbourhood's layer l - 1 is written (and its layer l - 1 reads are done)
+                    const int want = 16 * epoch + l;
+                    for (int dr = -1; dr <= 1; ++dr)
+                        for (int dc = -1; dc <= 1; ++dc) {
+                            const int r2 = rb + dr, c2 = strip + dc;
+                            if (r2 >= 0 && r2 < n_rb && c2 >= 0 && c2 < strips) flag_wait_ge(flags + r2 * strips + c2, want);
+                        }
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
+                const CUtensorMap* m = (l & 1) ? &map1 : &map0;
+                for (int r = y0 - 1; r <= y1; ++r) {
+                    const long q = q0 + (r - rbase);
+                    const int s = (int)(q % kSlots);
+                    const long u = q / kSlots;
+                    if (u >= 1) mbar_wait(sempty + s, (uint32_t)((u - 1) & 1));
+                    mbar_expect(sfull + s, kSlotBytes);
+                    tma_row(slots + s * kSlotBytes, m, x0 / 8 - 1, r, sfull + s);
+                }
+                q0 += rows_l;
+            }
+        }
+    } else if (warp == 1) {  // ---- MMA issuer (whole warp, one elected lane issues)
+        const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
+        long q0 = 0;
+        int tg = 0;  // accumulator-pair units issued so far (all layers)
+        for (int l = 0; l < n_layers; ++l) {
+            mbar_wait(wbar, (uint32_t)(l & 1));
+            int landed = y0 - 2;
+            int y_last = y0, nr_last = 0;
+            for (int t = 0; t < n_units; ++t, ++tg) {
+                const int y = y0 + R * t, b = tg & 1, ub = tg >> 1;
+                const int nr = min(R, y1 - y);
+                if (ub >= 1) {
+                    mbar_wait(aempty + b, (uint32_t)((ub - 1) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                }
+                const uint32_t d = tmem + (uint32_t)(b * R * 64);
+                auto row = [&](int r, int blk, uint32_t dcol, uint32_t idesc, bool first) {
+                    if (r > landed) {
+                        while (landed < r) {
+                            ++landed;
+                            const long q = q0 + (landed - rbase);
+                            mbar_wait(sfull + q % kSlots, (uint32_t)((q / kSlots) & 1));
+                        }
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    }
+                    const long q = q0 + (r - rbase);
+                    const uint64_t a0 = sdesc(sl_base + (uint32_t)(q % kSlots) * kSlotBytes + kHaloOff * 16, kHaloX * 16, 128);
+                    const uint64_t b0 = sdesc(sw_base + blk * kC * 16, kW2Icg, 128);
+                    umma_row12(dcol, a0, b0, idesc, first ? 0u : 1u);
+                };
+                if (nr == 2) {
+                    row(y, 1, d, kIdesc128, true);
+                    row(y + 1, 0, d, kIdesc128, false);
+                    row(y - 1, 2, d, kIdesc, false);
+                    row(y + 2, 0, d + 64, kIdesc, false);
+                } else {
+                    row(y - 1, 2, d, kIdesc, true);
+                    row(y, 1, d, kIdesc, false);
+                    row(y + 1, 0, d, kIdesc, false);
+                }
+                umma_commit_e(afull + b);
+                for (int r = y - 1; r < y - 1 + nr; ++r) umma_commit_e(sempty + (q0 + r - rbase) % kSlots);
+                y_last = y;
+                nr_last = nr;
+            }
+            // rows never read again in this layer (the last unit's bottom halo) go back to the ring
+            for (int r = y_last - 1 + nr_last; r <= y1; ++r) umma_commit_e(sempty + (q0 + r - rbase) % kSlots);
+            umma_commit_e(wfree);
+            q0 += rows_l;
+        }
+    } else {  // ---- epilogue warps 2..5
+        const int quad = warp & 3;
+        int tg = 0;
+        for (int l = 0; l < n_layers; ++l) {
+            __nv_bfloat16* out = (l & 1) ? act0 : act1;
+            for (int t = 0; t < n_units; ++t, ++tg) {
+                const int y = y0 + R * t, b = tg & 1, ub = tg >> 1;
+                const int nrows = min(R, y1 - y);
+                mbar_wait(afull + b, (uint32_t)(ub & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int rr = 0; rr < nrows; ++rr) {
+                    const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * R * 64 + rr * 64);
+                    uint32_t r[64];
+                    LD16(base + 0, (r + 0));
+                    LD16(base + 16, (r + 16));
+                    LD16(base + 32, (r + 32));
+                    LD16(base + 48, (r + 48));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (rr == nrows - 1) {
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0)
+                            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(aempty + b)) : "memory");
+                    }
+                    const int px = x0 + quad * 32 + lane;
+                    if (px < W) {
+                        uint4* dst = reinterpret_cast<uint4*>(out) + ((size_t)(y + rr) * Wp + px);
+                        const size_t gstride = (size_t)H * Wp;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            uint32_t pk[4];
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) {
+                                const float lo = fmaxf(__uint_as_float(r[8 * q + 2 * h]), 0.f);
+                                const float hi = fmaxf(__uint_as_float(r[8 * q + 2 * h + 1]), 0.f);
+                                const __nv_bfloat162 v2 = __floats2bfloat162_rn(lo, hi);
+                                pk[h] = *reinterpret_cast<const uint32_t*>(&v2);
+                            }
+                            dst[q * gstride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        }
+                    }
+                }
+            }
+            // publish the layer: every epilogue thread's stores, then one release of the CTA's flag
+            __threadfence();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (tid == 64) {
+                const int v = 16 * epoch + l + 1;
+                asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + blockIdx.x), "r"(v) : "memory");
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAccCols) : "memory");
+}
+
+// Layer 17 on the tensor cores: out = x - conv(h, w17).  The single output channel is padded to
+// N = 16 (the smallest UMMA N at M = 128), so a 128-px row segment is 36 UMMAs M=128 x N=16 x K=16
+// (9 taps x 4 K-steps) into a 16-column fp32 accumulator; the epilogue reads column 0 only and writes
+// the fp32 residual.  Same warp roles, halo ring and TMA map as k_conv64_tc (one row per unit);
+// weights [9 taps][8 ic-groups][16 oc][8 ic] bf16 (18 KB, oc 1..15 zero).
+constexpr int kLOC = 16;
+constexpr int kLWBytes = 9 * 8 * kLOC * 16;  // 18,432
+constexpr uint32_t kIdescL = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kLOC >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+constexpr int kLSmem = kLWBytes + kSlots * kSlotBytes + 1024;
+
+__global__ void __launch_bounds__(192, 1) k_conv_last_tc(const __grid_constant__ CUtensorMap amap,
+                                                         const __nv_bfloat16* __restrict__ wts,
+                                                         const float* __restrict__ x, float* out, int H, int W,
+                                                         int rows_per_cta)
+{
+    extern __shared__ __align__(1024) unsigned char sm[];
+    unsigned char* sw = sm;
+    unsigned char* slots = sm + kLWBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + kSlots * kSlotBytes);
+    uint64_t* wbar = bars;
+    uint64_t* sfull = bars + 1;
+    uint64_t* sempty = sfull + kSlots;
+    uint64_t* afull = sempty + kSlots;
+    uint64_t* aempty = afull + kAcc;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kAcc);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int strips = (W + kTileX - 1) / kTileX;
+    const int strip = blockIdx.x % strips;
+    const int x0 = strip * kTileX;
+    const int y0 = (blockIdx.x / strips) * rows_per_cta;
+    const int y1 = min(H, y0 + rows_per_cta);
+    if (y0 >= H) return;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(tmem_slot)),
+                     "n"(kAcc * kLOC)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 32) {
+        mbar_init(wbar, 1);
+        for (int i = 0; i < kSlots; ++i) {
+            mbar_init(sfull + i, 1);
+            mbar_init(sempty + i, 1);
+        }
+        for (int i = 0; i < kAcc; ++i) {
+            mbar_init(afull + i, 1);
+            mbar_init(aempty + i, 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const int rbase = y0 - 1;
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            mbar_expect(wbar, kLWBytes);
+            bulk_copy(sw, wts, kLWBytes, wbar);
+            asm volatile("griddepcontrol.wait;" ::: "memory");  // the last 64-channel layer
+            for (int r = y0 - 1; r <= y1; ++r) {
+                const int q = r - rbase, s = q % kSlots, u = q / kSlots;
+                if (u >= 1) mbar_wait(sempty + s, (uint32_t)((u - 1) & 1));
+                mbar_expect(sfull + s, kSlotBytes);
+                tma_row(slots + s * kSlotBytes, &amap, x0 / 8 - 1, r, sfull + s);
+            }
+        }
+    } else if (warp == 1) {  // ---- MMA issuer (whole warp, one elected lane issues)
+        const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
+        mbar_wait(wbar, 0);
+        for (int y = y0; y < y1; ++y) {
+            const int t = y - y0, b = t % kAcc, ub = t / kAcc;
+            if (ub >= 1) mbar_wait(aempty + b, (uint32_t)((ub - 1) & 1));
+            for (int r = y - 1; r <= y + 1; ++r) {
+                const int q = r - rbase;
+                mbar_wait(sfull + q % kSlots, (uint32_t)((q / kSlots) & 1));
+            }
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t d = tmem + (uint32_t)(b * kLOC);
+            const uint64_t b0 = sdesc(sw_base, kLOC * 16, 128);
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy) {
+                const uint64_t a0 = sdesc(sl_base + ((y - 1 + dy - rbase) % kSlots) * kSlotBytes, kHaloX * 16, 128);
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t a = a0 + (uint64_t)(((kHaloOff + dx) * 16 + 2 * j * (kHaloX * 16)) >> 4);
+                        const uint64_t bd = b0 + (uint64_t)(((dy * 3 + dx) * (8 * kLOC * 16) + 2 * j * (kLOC * 16)) >> 4);
+                        umma_e(d, a, bd, kIdescL, (dy | dx | j) != 0);
+                    }
+                }
+            }
+            umma_commit_e(afull + b);
+            umma_commit_e(sempty + (y - 1 - rbase) % kSlots);  // row y-1: last reader was row y
+        }
+    } else {  // ---- epilogue warps 2..5: column 0 of the accumulator -> out = x - net(x)
+        const int quad = warp & 3;
+        for (int y = y0; y < y1; ++y) {
+            const int t = y - y0, b = t % kAcc, ub = t / kAcc;
+            mbar_wait(afull + b, (uint32_t)(ub & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * kLOC);
+            uint32_t v;
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(base));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(aempty + b)) : "memory");
+            const int px = x0 + quad * 32 + lane;
+            if (px < W) {
+                const size_t p = (size_t)y * W + px;
+                out[p] = x[p] - __uint_as_float(v);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * kLOC) : "memory");
+}
+
 // layer 1: x (fp32, rounded to bf16) -> 64 ch, ReLU, bf16 blocked [8][H][W][8].  w1: [9 taps][64 oc] fp32
 // packed fp32 FMA (sm_100 FFMA2): {a.x * b.x + c.x, a.y * b.y + c.y}
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c)
@@ -646,6 +986,18 @@ void Cnn::set_weights(const uint16_t* bf16, int layers, int channels)
     const uint16_t* wl = bf16 + n1 + 15 * nm;
     for (int ic = 0; ic < kC; ++ic)
         for (int t = 0; t < 9; ++t) w_last.v[t * kC + ic] = f(wl[ic * 9 + t]);
+    // layer 17 for the tensor cores: [tap][ic-group][16 oc][8 ic], output channel 0 only
+    {
+        std::vector<uint16_t> wt((size_t)kLWBytes / 2, 0);
+        for (int ic = 0; ic < kC; ++ic)
+            for (int t = 0; t < 9; ++t) wt[(size_t)t * 8 * kLOC * 8 + (ic / 8) * kLOC * 8 + ic % 8] = wl[ic * 9 + t];
+        w_last_tc.alloc(wt.size());
+        CKC(cudaMemcpy(w_last_tc.p, wt.data(), wt.size() * 2, cudaMemcpyHostToDevice));
+    }
+    const char* el = std::getenv("MACE_K5_LAST");  // "fma": layer 17 on the CUDA cores
+    last_tc = !(el && std::strcmp(el, "fma") == 0);
+    const char* es = std::getenv("MACE_K5_SEQ");  // "1": the 15 middle layers as one persistent launch
+    seq = es && std::strcmp(es, "1") == 0;
     // middle layers: [layer][tap][ic-group][oc][8 ic]
     std::vector<uint16_t> wm(15 * (size_t)9 * kC * kC);
     for (int l = 0; l < 15; ++l) {
@@ -696,6 +1048,11 @@ void Cnn::ensure(int h, int w)
     CKC(cudaFuncSetAttribute(k_conv64_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv64_tc2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv64_tc2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    CKC(cudaFuncSetAttribute(k_conv_last_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kLSmem));
+    CKC(cudaFuncSetAttribute(k_conv64_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    flags.alloc(1024);
+    CKC(cudaMemset(flags.p, 0, 1024 * sizeof(int)));
+    epoch = 0;
 }
 
 // one 64 -> 64 layer (2..16) from map -> dst on stream s with the current launch geometry
@@ -759,10 +1116,43 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     pdl[0].val.programmaticStreamSerializationAllowed = 1;
-    for (int l = 0; l < 15; ++l)
-        launch_mid(l, (l & 1) ? map1 : map0, (l & 1) ? act0.p : act1.p, s, num_sms, true);
+    if (seq && rows_unit == 2) {  // the 15 middle layers as one persistent cooperative launch
+        const int strips = (W + kTileX - 1) / kTileX;
+        const int ctas_y = std::max(1, num_sms / strips);
+        const int per = (H + ctas_y - 1) / ctas_y;
+        const int ctas = strips * ((H + per - 1) / per);
+        if (ctas > 1024) throw std::runtime_error("denoiser grid too large");
+        ++epoch;
+        cudaLaunchAttribute coop[1];
+        coop[0].id = cudaLaunchAttributeCooperative;
+        coop[0].val.cooperative = 1;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(ctas);
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = kSmem;
+        cfg.stream = s;
+        cfg.attrs = coop;
+        cfg.numAttrs = 1;
+        CKC(cudaLaunchKernelEx(&cfg, k_conv64_seq, map0, map1, (const __nv_bfloat16*)w_mid2.p, act0.p, act1.p, H, W,
+                               Wp, per, 15, flags.p, epoch));
+    } else {
+        for (int l = 0; l < 15; ++l)
+            launch_mid(l, (l & 1) ? map1 : map0, (l & 1) ? act0.p : act1.p, s, num_sms, true);
+    }
     // 15 middle layers: the last one wrote act1 (l = 14 even -> dst act1)
-    {
+    if (last_tc) {
+        const int strips = (W + kTileX - 1) / kTileX;
+        const int ctas_y = std::max(1, num_sms / strips);
+        const int per = (H + ctas_y - 1) / ctas_y;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(strips * ((H + per - 1) / per));
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = kLSmem;
+        cfg.stream = s;
+        cfg.attrs = pdl;
+        cfg.numAttrs = 1;
+        CKC(cudaLaunchKernelEx(&cfg, k_conv_last_tc, map1, (const __nv_bfloat16*)w_last_tc.p, x, out, H, W, per));
+    } else {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((W + kLastT - 1) / kLastT, (H + kLastT - 1) / kLastT);
         cfg.blockDim = dim3(kLastT * kLastT);

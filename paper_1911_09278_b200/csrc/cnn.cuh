@@ -43,6 +43,11 @@ struct Cnn {
     DevBuf<__nv_bfloat16> w_mid;         // [15][9 taps][8 ic-groups][64 oc][8 ic]
     DevBuf<__nv_bfloat16> w_mid2;        // row-pair layout: [15][3 dx][8 ic-groups][dy2 | dy1 | dy0][64 oc][8 ic]
     int rows_unit = 2;                   // output rows per MMA unit (k_conv64_tc2<2|3>; 1 = k_conv64_tc), MACE_K5_ROWS
+    DevBuf<__nv_bfloat16> w_last_tc;     // layer 17 for k_conv_last_tc: [9 taps][8 ic-groups][16 oc][8 ic]
+    bool last_tc = true;                 // layer 17 on the tensor cores (MACE_K5_LAST=fma: CUDA cores)
+    bool seq = false;                    // layers 2..16 in one persistent launch (MACE_K5_SEQ=1; slower)
+    DevBuf<int> flags;                   // per-CTA layer-done flags of k_conv64_seq
+    int epoch = 0;                       // flag epoch (one per persistent launch)
     DevBuf<__nv_bfloat16> act0, act1;    // channel-blocked [8 groups][H][Wp][8 ch]
     CUtensorMap map0{}, map1{};
     // weights: 17 layers in PyTorch OIHW order, bf16 bits, concatenated

@@ -140,7 +140,11 @@ __device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __
 }
 
 #ifndef MACE_K2_NORELOAD
-#define MACE_K2_NORELOAD 1  // scatter from registers (no band reloads), see step()
+// 1: scatter from registers, the rows an earlier batch pixel shares picked by selects (no band
+// reloads: -18 of ~108 shared wavefronts per batch).  Measured slower on B200 (c1 0.536 vs 0.436 ms,
+// c2 4.41 vs 3.60 ms; 168 registers): the ~160 extra selects / FMAs per batch cost more issue slots
+// than the reloads cost LSU slots.  Kept as an A/B variant; off by default.
+#define MACE_K2_NORELOAD 0
 #endif
 #ifndef MACE_K2_MINB
 #define MACE_K2_MINB 12  // resident warps per SM the register budget is sized for
@@ -502,10 +506,14 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
                     for (int q = 0; q < p; ++q) {
                         const int d = ab[p][g] - ab[q][g];
 #pragma unroll
-                        for (int k = 0; k < K; ++k)
+                        for (int k = 0; k < K; ++k) {
+                            // the length of q's entry on this row, 0 if q does not touch it (selects, not
+                            // branches: the lanes disagree); fmaf(-alpha, 0, e) == e
+                            float sel = 0.f;
 #pragma unroll
-                            for (int k2 = 0; k2 < K; ++k2)
-                                if (d == (k2 - k) * U) ev[k] = fmaf(-alpha[q], av[q][g][k2], ev[k]);
+                            for (int k2 = 0; k2 < K; ++k2) sel = d == (k2 - k) * U ? av[q][g][k2] : sel;
+                            ev[k] = fmaf(-alpha[q], sel, ev[k]);
+                        }
                     }
 #pragma unroll
                     for (int k = 0; k < K; ++k) sb[ab[p][g] + k * U] = fmaf(-alpha[p], av[p][g][k], ev[k]);

@@ -193,3 +193,24 @@ def test_pnp_denoiser_in_device_loop_matches_host_steps():
     host = solve(lambda v: H(v))  # no device hooks: host round trip every iteration
     assert rel(dev.image, host.image) < 1e-6
     assert rel(dev.stack, host.stack) < 1e-6
+
+
+@pytest.mark.parametrize("n_side", [64, 200, 512])
+def test_cnn_launch_variants_are_bit_identical(n_side, monkeypatch):
+    """The middle layers as 15 launches or as one persistent launch (MACE_K5_SEQ), and the last layer
+    on the tensor cores or on the CUDA cores (MACE_K5_LAST): the persistent kernel runs the same
+    UMMAs, so it must match the per-layer launches bit for bit; the two last-layer kernels sum the
+    576 products in different orders (fp32), so they agree to fp32 rounding."""
+    rng = np.random.default_rng(31)
+    x = rng.random(n_side * n_side)
+    w = cnn_weights(31, scale=1.0)
+    outs = {}
+    for seq in ("0", "1"):
+        for last in ("tc", "fma"):
+            monkeypatch.setenv("MACE_K5_SEQ", seq)
+            monkeypatch.setenv("MACE_K5_LAST", last)
+            outs[(seq, last)] = CnnDenoiser(n_side, weights=w)(x)
+    assert np.array_equal(outs[("1", "tc")], outs[("0", "tc")])
+    assert np.array_equal(outs[("1", "fma")], outs[("0", "fma")])
+    r_tc, r_fma = _net(x, outs[("0", "tc")]), _net(x, outs[("0", "fma")])
+    assert rel(r_tc, r_fma) < 1e-5
