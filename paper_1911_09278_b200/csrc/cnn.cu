@@ -503,6 +503,21 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
 // co-resident: one per SM), so the spin-waits cannot deadlock.  Measured SLOWER than 15 launches with
 // programmatic dependent launch (0.333 vs 0.277 ms per 512^2 denoise on B200), so it is an option
 // (MACE_K5_SEQ=1), bit-identical to the default (tests/test_gpu_cnn.py); DESIGN.md §6.
+#ifdef K5SEQ_TRACE  // profiling builds only: per-CTA, per-layer %globaltimer stamps of k_conv64_seq
+// [cta][layer][0 weights free seen, 1 neighbour flags passed, 2 weights landed (MMA), 3 first unit
+// issued, 4 last unit issued, 5 layer published]
+__device__ unsigned long long g_k5seq[148][16][6];
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define K5S(l, i) (blockIdx.x < 148 && (l) < 16 ? (void)(g_k5seq[blockIdx.x][(l)][(i)] = gtimer()) : (void)0)
+#else
+#define K5S(l, i) ((void)0)
+#endif
+
 __device__ __forceinline__ void flag_wait_ge(const int* f, int v)
 {
     int x;
@@ -573,6 +588,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_seq(const __grid_constant__ C
             long q0 = 0;
             for (int l = 0; l < n_layers; ++l) {
                 if (l > 0) mbar_wait(wfree, (uint32_t)((l - 1) & 1));
+                K5S(l, 0);
                 mbar_expect(wbar, kWBytes);
                 bulk_copy(sw, wts + (size_t)l * 9 * kC * kC, kWBytes, wbar);
                 if (l > 0) {  // the neighbourhood's layer l - 1 is written (and its layer l - 1 reads are done)
@@ -584,6 +600,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_seq(const __grid_constant__ C
                         }
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
+                K5S(l, 1);
                 const CUtensorMap* m = (l & 1) ? &map1 : &map0;
                 for (int r = y0 - 1; r <= y1; ++r) {
                     const long q = q0 + (r - rbase);
@@ -602,6 +619,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_seq(const __grid_constant__ C
         int tg = 0;  // accumulator-pair units issued so far (all layers)
         for (int l = 0; l < n_layers; ++l) {
             mbar_wait(wbar, (uint32_t)(l & 1));
+            if (lane == 0) K5S(l, 2);
             int landed = y0 - 2;
             int y_last = y0, nr_last = 0;
             for (int t = 0; t < n_units; ++t, ++tg) {
@@ -638,6 +656,8 @@ __global__ void __launch_bounds__(192, 1) k_conv64_seq(const __grid_constant__ C
                 }
                 umma_commit_e(afull + b);
                 for (int r = y - 1; r < y - 1 + nr; ++r) umma_commit_e(sempty + (q0 + r - rbase) % kSlots);
+                if (lane == 0 && t == 0) K5S(l, 3);
+                if (lane == 0 && t == n_units - 1) K5S(l, 4);
                 y_last = y;
                 nr_last = nr;
             }
@@ -694,6 +714,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_seq(const __grid_constant__ C
             asm volatile("fence.proxy.async.global;" ::: "memory");
             asm volatile("bar.sync 1, 128;" ::: "memory");
             if (tid == 64) {
+                K5S(l, 5);
                 const int v = 16 * epoch + l + 1;
                 asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + blockIdx.x), "r"(v) : "memory");
             }
@@ -968,6 +989,12 @@ CUtensorMap make_act_map(void* base, int H, int Wp)
 
 #ifdef K5_TRACE
 void k5_trace_copy(long long* host) { cudaMemcpyFromSymbol(host, g_k5_trace, sizeof(g_k5_trace)); }
+#endif
+#ifdef K5SEQ_TRACE
+extern "C" int mace_k5seq_trace(unsigned long long* host)
+{
+    return cudaMemcpyFromSymbol(host, g_k5seq, sizeof(g_k5seq)) == cudaSuccess ? 0 : -1;
+}
 #endif
 
 void Cnn::set_weights(const uint16_t* bf16, int layers, int channels)

@@ -139,6 +139,9 @@ __device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __
         asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(B.ob[p]) : "l"(r + p * RECW + NG * 32 * K));
 }
 
+#ifndef MACE_K2_PF
+#define MACE_K2_PF 2  // L2 bulk prefetch distance of the slot records in batches (0: off); DESIGN.md §6
+#endif
 #ifndef MACE_K2_NORELOAD
 // 1: scatter from registers, the rows an earlier batch pixel shares picked by selects (no band
 // reloads: -18 of ~108 shared wavefronts per batch).  Measured slower on B200 (c1 0.536 vs 0.436 ms,
@@ -268,6 +271,11 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
         const unsigned nitem = fetch_item();
         const bool more = nitem < (unsigned)P.n_items;
         const uint32_t ncode = more ? __ldg(P.queue + nitem) : 0u;
+#if MACE_K2_PF > 0
+        // the next tile's records, for the L2 prefetch that runs MACE_K2_PF batches ahead
+        const uint32_t* nrecs = more ? P.agents[ncode >> kAgentShift].rec + (size_t)(ncode & kSvMask) * NB * 4 * RECW
+                                     : nullptr;
+#endif
 
         // -- 1. band: lambda rows by one coalesced copy, e rows from the prefetched windows
         if constexpr (!kW) {  // lambda: pre-arranged per tile (k_sv_consts) as [u][32]; 16-byte copies into the units
@@ -328,6 +336,19 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
         auto step = [&](const int b, const SvBatch<K, NG>& C, SvBatch<K, NG>& Nx, auto full_tag) {
             constexpr bool kFull = decltype(full_tag)::value;
             if (b + 1 < NB) load_batch<K, NG>(Nx, recs + (size_t)(b + 1) * 4 * RECW, lane);
+#if MACE_K2_PF > 0
+            // records of batch b + PF (this tile's or the next one's) pulled into L2 by one bulk
+            // prefetch (TMA unit, no LSU work, no registers): the register load one batch ahead then
+            // sees L2 rather than DRAM latency
+            if (lane == 0) {
+                const int tb = b + MACE_K2_PF;
+                const uint32_t* pf = tb < NB ? recs + (size_t)tb * 4 * RECW
+                                             : (nrecs ? nrecs + (size_t)(tb - NB) * 4 * RECW : nullptr);
+                if (pf)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"((uint32_t)(4 * RECW * 4))
+                                 : "memory");
+            }
+#endif
             const float4 k0 = __ldg(reinterpret_cast<const float4*>(bcs + 16 * b));
             const float4 k1 = __ldg(reinterpret_cast<const float4*>(bcs + 16 * b) + 1);
             const float2 k2 = __ldg(reinterpret_cast<const float2*>(bcs + 16 * b + 8));
