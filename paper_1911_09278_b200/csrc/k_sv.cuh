@@ -142,6 +142,9 @@ __device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __
 #ifndef MACE_K2_PF
 #define MACE_K2_PF 2  // L2 bulk prefetch distance of the slot records in batches (0: off); DESIGN.md §6
 #endif
+#ifndef MACE_K2_BCPF
+#define MACE_K2_BCPF 1  // L2 bulk prefetch of the next tile's batch constants
+#endif
 #ifndef MACE_K2_NORELOAD
 // 1: scatter from registers, the rows an earlier batch pixel shares picked by selects (no band
 // reloads: -18 of ~108 shared wavefronts per batch).  Measured slower on B200 (c1 0.536 vs 0.436 ms,
@@ -275,6 +278,15 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
         // the next tile's records, for the L2 prefetch that runs MACE_K2_PF batches ahead
         const uint32_t* nrecs = more ? P.agents[ncode >> kAgentShift].rec + (size_t)(ncode & kSvMask) * NB * 4 * RECW
                                      : nullptr;
+#endif
+#if MACE_K2_BCPF
+        // the next tile's batch constants (1 KB, read from the first batch on) into L2 a whole tile
+        // ahead: at config 2 they do not stay in L2 between passes (16 agents x 16.8 MB)
+        if (lane == 0 && more)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.agents[ncode >> kAgentShift].bc +
+                                                                            (size_t)(ncode & kSvMask) * NB * 16),
+                         "r"((uint32_t)(NB * 16 * 4))
+                         : "memory");
 #endif
 
         // -- 1. band: lambda rows by one coalesced copy, e rows from the prefetched windows

@@ -670,8 +670,9 @@ __global__ void k_finish(const double* sums5, double ref_norm2, double tol, int 
 // in the last block to finish a fixed-order fold of the block sums followed by the stop test and log
 // row (k_finish).  Same arithmetic order as k_consensus + k_norms + k_finish; gridDim <= 256.
 template <int NL>
-__global__ void __launch_bounds__(256) k_tail(const float* W, int n_local, size_t n, float scale, float* out,
-                                              const float* ref, const double* part, int n_items, double* scratch,
+__global__ void __launch_bounds__(256) k_tail(const float* __restrict__ W, int n_local, size_t n, float scale,
+                                              float* __restrict__ out, const float* __restrict__ ref,
+                                              const double* __restrict__ part, int n_items, double* scratch,
                                               unsigned* counter, double* sums5, double ref_norm2, double tol,
                                               int iter, double* log, int* done, unsigned* head, int n_groups)
 {
@@ -729,8 +730,11 @@ __global__ void __launch_bounds__(256) k_tail(const float* W, int n_local, size_
     }
     __syncthreads();
     if (!last) return;
-    for (int k = 0; k < 5; ++k)
-        sh[k][threadIdx.x] = (int)threadIdx.x < (int)gridDim.x ? __ldcg(scratch + 5 * threadIdx.x + k) : 0.0;
+    for (int k = 0; k < 5; ++k) {  // the block sums, gridDim <= 1024: a fixed-order fold in 256 lanes
+        double v = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v += __ldcg(scratch + 5 * b + k);
+        sh[k][threadIdx.x] = v;
+    }
     __syncthreads();
     for (int o = blockDim.x / 2; o; o >>= 1) {
         if ((int)threadIdx.x < o)

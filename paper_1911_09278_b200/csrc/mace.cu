@@ -172,6 +172,7 @@ static void k2_end(Ctx* c, cudaEvent_t second)
 }
 
 static const int kRefBlocks = 256;
+static const int kTailBlocksMax = 1024;  // k_tail: 4 blocks per SM (the stack average streams n_local x n floats)
 static const int kNormBlocks = 64;
 
 static void sync(Ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
@@ -472,7 +473,7 @@ int mace_ctx_create(int device, void** out)
     c->head.alloc(1);
     c->done.alloc(2);
     c->sums5.alloc(5);
-    c->norm_scratch.alloc(5 * std::max(kNormBlocks, kRefBlocks));  // k_norms and k_tail block sums
+    c->norm_scratch.alloc(5 * std::max(kNormBlocks, kTailBlocksMax));  // k_norms and k_tail block sums
     c->norm_counter.alloc(1);
     CK(cudaMemset(c->norm_counter.p, 0, sizeof(unsigned)));
     CK(cudaMemset(c->head.p, 0, sizeof(unsigned)));
@@ -1253,7 +1254,8 @@ static void iteration_tail(Ctx* c, float scale, bool with_ref, double tol, int i
     const float* rf = with_ref ? c->ref.p : nullptr;
     const double rn2 = with_ref ? c->ref_norm2 : 0.0;
 #define MACE_TAIL(NL_)                                                                                             \
-    k_tail<NL_><<<kRefBlocks, 256, 0, c->stream>>>(c->W.p, c->n_real, c->n, scale, c->wbar.p, rf, c->part.p,        \
+    k_tail<NL_><<<std::min(kTailBlocksMax, 4 * c->num_sms), 256, 0, c->stream>>>(                                  \
+        c->W.p, c->n_real, c->n, scale, c->wbar.p, rf, c->part.p,                                                     \
                                                    c->n_items, c->norm_scratch.p, c->norm_counter.p, c->sums5.p, rn2, \
                                                    tol, iter, c->log.p, c->done.p, c->head.p, c->n_slices)
     switch (c->n_real) {
