@@ -87,6 +87,11 @@ int mace_set_schedule(void* ctx, double concurrency, int64_t max_warps);
  * of a group then has about (resident warps / group) tiles in flight, the per-agent staleness of a
  * rank that owns `group` agents (1-GPU emulation of an N-GPU partition) */
 int mace_set_agent_groups(void* ctx, int group);
+/* deterministic super-voxel passes (on != 0): one launch per colour class, each tile staging e as it
+ * stood at the class start, the tiles' e changes summed in 2^-40 fixed point and folded between
+ * classes -- bitwise reproducible for any concurrency, like the reference's fixed visiting order
+ * (pkg/tests/test_mace.py:161-170).  Needs agent groups off. */
+int mace_set_deterministic(void* ctx, int on);
 /* local < 0: every local agent */
 int mace_set_agent_params(void* ctx, int local, double beta_eff, double inv_sigma2, int clamp);
 /* global sinogram y and weights, n_views x n_ch float32; recomputes theta2.  Single-slice

@@ -41,6 +41,7 @@ _SIGS = {
     "mace_setup_agents": (c_int, [P, c_int, P, P, c_int, c_int, c_int, c_int, c_int]),
     "mace_set_schedule": (c_int, [P, c_double, c_int64]),
     "mace_set_agent_groups": (c_int, [P, c_int]),
+    "mace_set_deterministic": (c_int, [P, c_int]),
     "mace_stage_wait": (c_int, [P]),
     "mace_get_batch_consts": (c_int, [P, c_int, P, P]),
     "mace_set_iter": (c_int, [P, c_int]),

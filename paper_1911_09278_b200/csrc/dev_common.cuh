@@ -44,6 +44,7 @@ struct AgentDev {
     const uint32_t* rec0;  // the plain records (layout.cpp, lane-per-view)
     uint32_t* recw;        // weighted records k_sv_consts writes (== rec when sq != nullptr, else nullptr)
     float* bc;             // [n_sv][nb][16] batch constants: theta2 x4, cross terms x6 (per local agent)
+    unsigned long long* ed;  // [R] deterministic mode: fixed-point e deltas of the running colour class
     float* lb;             // [n_sv][ng][wcap][32] band lambda in shared-memory order (per local agent)
     int ng, rec_words;     // view groups ceil(V / 32); words per slot record
     // raster layout
@@ -66,9 +67,15 @@ struct PassParams {
     unsigned* head;
     double* part;  // [n_items * 4]: sum alpha^2, sum (w'-w)^2, sum w'^2, sum w^2
     int ng, wcap;  // shared-memory band geometry (max over agents)
+    int chunks;    // view chunks (warps) per super-voxel tile: 1, or > 1 for agents with > 128 views
+    int det;       // deterministic class-synchronous mode: write-back into AgentDev::ed (fixed point)
     const int* done;
     long s_begin, s_end;  // raster passes: pixel range [s_begin, s_end) (icd.py:222-246)
 };
+
+// deterministic mode: e deltas accumulated as signed 2^-40 fixed point (k_sv.cuh write-back,
+// k_fold_delta); |delta| < 2^23 per row and class, resolution 9e-13
+constexpr double kDetScale = 1099511627776.0;
 
 static __constant__ int c_dr[8] = {-1, -1, -1, 0, 0, 1, 1, 1};  // models.py:50
 static __constant__ int c_dc[8] = {-1, 0, 1, -1, 1, -1, 0, 1};

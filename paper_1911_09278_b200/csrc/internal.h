@@ -59,15 +59,17 @@ struct RasterLayout {
 // precomputed cross term per pair (k_sv.cuh).  Slot records are stored in visit order,
 // batch-contiguous, so a batch is one contiguous copy.
 constexpr int kSvBatch = 4;
+constexpr int kSvMaxChunks = 16;  // multi-warp tiles: at most 16 warps (chunks of 96 views) per tile
 struct SVLayout {
     int svs = 0, n_sv_side = 0, n_sv = 0, views = 0;
-    int ng = 0;                  // view groups ceil(views / 32) (<= 4)
+    int ng = 0;                  // view groups per chunk: ceil(views / 32) (<= 4), or 3 with chunks
+    int chunks = 1;              // chunks of 3 view groups (one warp each) when views > 128
     int K = 0;                   // entries per (pixel, view) slot (max over the agent, 2 for pitch = channel pitch)
     int wcap = 0;                // max window rows over tiles and views
     int nb = 0;                  // batches per tile
     int rec = 0;                 // words per pixel slot: ng*32*K lengths ([g][lane][k]) + 32 offset words
     std::vector<int2_t> band;    // [n_sv * views] {local row start, cnt}
-    std::vector<uint32_t> data;  // [n_sv][nb][kSvBatch][rec] (lengths as float bits; empty slots 0)
+    std::vector<uint32_t> data;  // [n_sv][nb][chunks][kSvBatch][rec] (lengths as float bits; empty slots 0)
     int max_col = 0;             // max entries per column (info)
     int64_t entries = 0;         // stored nonzeros (== nnz of the agent)
     int64_t duplicates = 0;      // repeated (row, pixel) pairs merged (never seen in practice)

@@ -152,30 +152,54 @@ __device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __
 // than the reloads cost LSU slots.  Kept as an A/B variant; off by default.
 #define MACE_K2_NORELOAD 0
 #endif
+#ifndef MACE_K2_LEAN
+// 1: pixel 0 of a batch is scattered by reload-modify-store like the others (6 fewer live registers;
+// an occupancy experiment for 16 resident warps per SM)
+#define MACE_K2_LEAN 0
+#endif
 #ifndef MACE_K2_MINB
 #define MACE_K2_MINB 12  // resident warps per SM the register budget is sized for
 #endif
 #ifndef MACE_K2_MINB_W
 #define MACE_K2_MINB_W 12  // weighted records (16 fits the shared memory but spills registers: slower)
 #endif
-template <int S, int K, int NG, bool kW>
-__global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_sv(PassParams P)
+// MW > 0: multi-warp tiles for agents with more than 128 views (the centralized ICD of
+// icd_map_solve, icd.py:306-345, or few agents): warp w of a block owns view chunk w (3 groups of
+// 32 views, layout.cpp) of the same tile; per batch the warps exchange their theta1 partials
+// through shared memory (one named barrier) and then run identical solves, so every warp's copy
+// of the tile state stays identical; warp 0 writes z, w and the norm partials.  MW = 1: up to 8
+// chunks per tile, MW = 2: up to kSvMaxChunks.
+template <int S, int K, int NG, bool kW, int MW = 0>
+__global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
+                                  MW == 0 ? (kW ? MACE_K2_MINB_W : MACE_K2_MINB) : 1) k_icd_sv(PassParams P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     if (P.done && *P.done) return;
     constexpr int SS = S * S, S2 = S + 2, T2 = S2 * S2, T2p = (T2 + 3) & ~3;
     constexpr int H = S / 2, PER_CLASS = H * H, BPC = (PER_CLASS + 3) / 4, NB = 4 * BPC;
     constexpr int RECW = sv_rec_words(NG, K);
-    constexpr int U = sv_unit_words(kW);  // words per band row unit: e | lambda | e0 (kW: e | e0)
-    constexpr int E0 = U - 32;            // e0 plane offset
+    constexpr int U = sv_unit_words(kW);  // words per band row unit: e | lambda [| e0] (kW: e [| e0])
+    [[maybe_unused]] constexpr int E0 = U - 32;  // e0 plane offset (MACE_K2_RAW 0)
     const int lane = threadIdx.x & 31;
     const int W = P.wcap;
-    unsigned char* base = smem + (threadIdx.x >> 5) * sv_warp_bytes(S, NG, W, kW);
-    float* sb = reinterpret_cast<float*>(base);  // band: e at U u + lane, lambda +32, e0 +E0
+    const int wid = MW ? (int)(threadIdx.x >> 5) : 0;  // chunk of this warp
+    const int CH = MW ? P.chunks : 1;
+    unsigned char* base = smem + wid * sv_warp_bytes(S, NG, W, kW);
+    // multi-warp tiles: block area after the warps' regions (sv_block_extra_bytes): the next item,
+    // warp 0's tile-state snapshot, and the theta1 partials [2][4][CH]
+    unsigned* s_item = reinterpret_cast<unsigned*>(smem + CH * sv_warp_bytes(S, NG, W, kW));
+    float* s_stage = reinterpret_cast<float*>(s_item + 4);
+    float* s_part = s_stage + ((((S + 2) * (S + 2)) + 3) & ~3) + 2 * S * S;
+    auto bar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(32 * CH) : "memory"); };
+    float* sb = reinterpret_cast<float*>(base);  // band: e at U u + lane, lambda +32[, e0 +E0]
     float* zt = sb + NG * W * U;
     float* svv = zt + T2p;
     float* swo = svv + SS;
     float4* sred = reinterpret_cast<float4*>(swo + SS);  // the batch's {theta1', den, z, v} per pixel, broadcast through smem
+#if MACE_K2_RAW
+    const int RQ = sv_raw_quads(W);             // 16-byte quads per (group, lane) raw slot
+    float4* raw = sred + 4;                     // [g][lane][RQ]: the aligned span of each window
+#endif
     const int n = P.n_side;
     const PriorC& PR = P.pr;
     const bool quad = PR.kind == 0;
@@ -201,10 +225,33 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
         const int svn = (int)(cd & kSvMask), Vn = An.V;
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
-            const int j = 32 * g + lane;
+            const int j = 32 * (wid * NG + g) + lane;
             mb[g] = j < Vn ? __ldg(An.band + (size_t)svn * Vn + j) : make_int2(0, 0);
         }
     };
+#if MACE_K2_RAW
+    // e windows into the raw area: the aligned span of view 32 g + 8 k + (lane & 7) is copied by the
+    // four lanes 8 m + (lane & 7), quad v by lane m = v mod 4: one cp.async instruction covers 8
+    // views (8 lines) instead of 32, and needs no registers until the owner transposes it
+    auto issue_windows = [&](uint32_t cd, const int2 (&mb)[NG]) {
+        const float* en = P.agents[cd >> kAgentShift].e;
+        const int m = lane >> 3, vl = lane & 7;
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int src = 8 * k + vl;
+                const int st = __shfl_sync(FULL, mb[g].x, src), cnt = __shfl_sync(FULL, mb[g].y, src);
+                const int s0 = st & 3, nv = (cnt + s0 + 3) >> 2;
+                float4* dst = raw + (32 * g + src) * RQ + m;
+                const float* sp = en + (st - s0) + 4 * m;
+                if (m < nv) cp_async16(dst, sp);
+                if (m + 4 < nv) cp_async16(dst + 4, sp + 16);
+                for (int v = m + 8; v < nv; v += 4) cp_async16(raw + (32 * g + src) * RQ + v, en + (st - s0) + 4 * v);
+            }
+        cp_async_commit();
+    };
+#endif
     // e windows: 16-byte loads over the aligned span of each window (a lane's window is one
     // contiguous run of rows; the loads of one instruction hit 32 different lines)
     auto ewin_of = [&](uint32_t cd, const int2 (&mb)[NG], float4 (&ev4)[NG][EV], int (&shf)[NG]) {
@@ -246,16 +293,30 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
             }
         }
     };
-    unsigned item = fetch_item();
+    unsigned item;
+    if constexpr (MW > 0) {
+        if (threadIdx.x == 0) s_item[0] = atomicAdd(P.head, 1u);
+        bar();
+        item = s_item[0];
+    } else {
+        item = fetch_item();
+    }
     if (item >= (unsigned)P.n_items) return;
     uint32_t code = __ldg(P.queue + item);
     int2 myb[NG];
+#if MACE_K2_RAW
+    float zpre[ZN], wpre[VN], vpre[VN];
+    band_of(code, myb);
+    issue_windows(code, myb);
+#else
     float4 ew[NG][EV];
     int sh[NG];
     float zpre[ZN], wpre[VN], vpre[VN];
     band_of(code, myb);
     ewin_of(code, myb, ew, sh);
-    state_of(code, zpre, wpre, vpre);
+#endif
+    if (!MW || wid == 0) state_of(code, zpre, wpre, vpre);
+    int tpar = 1;  // multi-warp: s_item slot of the next item
 
     for (;;) {
         const AgentDev& A = P.agents[code >> kAgentShift];
@@ -268,21 +329,54 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
         const bool full = r0 + S <= n && c0 + S <= n;  // interior tile: no image-edge checks
         const float beta = A.beta_eff, inv_s2 = A.inv_s2;
         const int clamp = A.clamp;
-        const uint32_t* __restrict__ recs = A.rec + (size_t)sv * NB * 4 * RECW;
+        // records [sv][batch][chunk][slot][RECW]: this warp's chunk, batch stride BST
+        const size_t BST = (size_t)CH * 4 * RECW;
+        const uint32_t* __restrict__ recs = A.rec + (size_t)sv * NB * BST + (size_t)wid * 4 * RECW;
         const float* __restrict__ bcs = A.bc + (size_t)sv * NB * 16;
         // next item
-        const unsigned nitem = fetch_item();
+        unsigned nitem;
+        if constexpr (MW > 0) {
+            // warp 0 fetches the next item and publishes its snapshot of this tile's state; one
+            // barrier, then every warp starts from the same state
+            if (threadIdx.x == 0) s_item[tpar] = atomicAdd(P.head, 1u);
+            if (wid == 0) {
+#pragma unroll
+                for (int k = 0; k < ZN; ++k)
+                    if (32 * k + lane < T2) s_stage[32 * k + lane] = zpre[k];
+#pragma unroll
+                for (int k = 0; k < VN; ++k)
+                    if (32 * k + lane < SS) {
+                        s_stage[T2p + 32 * k + lane] = wpre[k];
+                        s_stage[T2p + SS + 32 * k + lane] = vpre[k];
+                    }
+            }
+            bar();
+            nitem = s_item[tpar];
+            tpar ^= 1;
+#pragma unroll
+            for (int k = 0; k < ZN; ++k)
+                if (32 * k + lane < T2) zpre[k] = s_stage[32 * k + lane];
+#pragma unroll
+            for (int k = 0; k < VN; ++k)
+                if (32 * k + lane < SS) {
+                    wpre[k] = s_stage[T2p + 32 * k + lane];
+                    vpre[k] = s_stage[T2p + SS + 32 * k + lane];
+                }
+        } else {
+            nitem = fetch_item();
+        }
         const bool more = nitem < (unsigned)P.n_items;
         const uint32_t ncode = more ? __ldg(P.queue + nitem) : 0u;
 #if MACE_K2_PF > 0
         // the next tile's records, for the L2 prefetch that runs MACE_K2_PF batches ahead
-        const uint32_t* nrecs = more ? P.agents[ncode >> kAgentShift].rec + (size_t)(ncode & kSvMask) * NB * 4 * RECW
+        const uint32_t* nrecs = more ? P.agents[ncode >> kAgentShift].rec + (size_t)(ncode & kSvMask) * NB * BST +
+                                           (size_t)wid * 4 * RECW
                                      : nullptr;
 #endif
 #if MACE_K2_BCPF
         // the next tile's batch constants (1 KB, read from the first batch on) into L2 a whole tile
         // ahead: at config 2 they do not stay in L2 between passes (16 agents x 16.8 MB)
-        if (lane == 0 && more)
+        if (lane == 0 && wid == 0 && more)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.agents[ncode >> kAgentShift].bc +
                                                                             (size_t)(ncode & kSvMask) * NB * 16),
                          "r"((uint32_t)(NB * 16 * 4))
@@ -291,7 +385,7 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
 
         // -- 1. band: lambda rows by one coalesced copy, e rows from the prefetched windows
         if constexpr (!kW) {  // lambda: pre-arranged per tile (k_sv_consts) as [u][32]; 16-byte copies into the units
-            const float* lsrc = A.lb + (size_t)sv * NG * W * 32;
+            const float* lsrc = A.lb + ((size_t)sv * CH + wid) * NG * W * 32;
             for (int c = lane; c < NG * W * 8; c += 32) cp_async16(sb + (c >> 3) * U + 32 + 4 * (c & 7), lsrc + 4 * c);
             cp_async_commit();
         }
@@ -314,6 +408,31 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
 
         // -- 4. batches of four same-parity pixels
         float dsq = 0.f;
+#if MACE_K2_RAW
+        // e plane from the raw windows (rows past the window are zero); the raw slot is this lane's
+        // own view, read as 16-byte quads (conflict-free: RQ is odd)
+        if constexpr (kW) cp_async_wait<0>();
+        else cp_async_wait<1>();  // the window group (committed last tile), not this tile's lambda copies
+        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            const int cnt = myb[g].y, s0 = myb[g].x & 3;
+            float* d = sb + g * W * U + lane;
+            const float4* rr = raw + (size_t)(32 * g + lane) * RQ;
+#pragma unroll 2
+            for (int v = 0; v < RQ; ++v) {
+                const float4 x4 = rr[v];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int o = 4 * v + i - s0;
+                    if (o >= 0 && o < W) {
+                        const float xi = i == 0 ? x4.x : i == 1 ? x4.y : i == 2 ? x4.z : x4.w;
+                        d[o * U] = o < cnt ? xi : 0.f;
+                    }
+                }
+            }
+        }
+#else
         // e and e0 planes from the registers (rows past the window are zero)
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
@@ -341,21 +460,22 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
                 }
             }
         }
+#endif
         if constexpr (!kW) cp_async_wait<0>();  // this lane's lambda copies have landed
         __syncwarp();        // ... and every other lane's; band / zt / v / w stores visible
         // kFull: the tile lies inside the image (all but the last tile row / column), so no slot
         // needs the image-edge test
         auto step = [&](const int b, const SvBatch<K, NG>& C, SvBatch<K, NG>& Nx, auto full_tag) {
             constexpr bool kFull = decltype(full_tag)::value;
-            if (b + 1 < NB) load_batch<K, NG>(Nx, recs + (size_t)(b + 1) * 4 * RECW, lane);
+            if (b + 1 < NB) load_batch<K, NG>(Nx, recs + (size_t)(b + 1) * BST, lane);
 #if MACE_K2_PF > 0
             // records of batch b + PF (this tile's or the next one's) pulled into L2 by one bulk
             // prefetch (TMA unit, no LSU work, no registers): the register load one batch ahead then
             // sees L2 rather than DRAM latency
             if (lane == 0) {
                 const int tb = b + MACE_K2_PF;
-                const uint32_t* pf = tb < NB ? recs + (size_t)tb * 4 * RECW
-                                             : (nrecs ? nrecs + (size_t)(tb - NB) * 4 * RECW : nullptr);
+                const uint32_t* pf = tb < NB ? recs + (size_t)tb * BST
+                                             : (nrecs ? nrecs + (size_t)(tb - NB) * BST : nullptr);
                 if (pf)
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"((uint32_t)(4 * RECW * 4))
                                  : "memory");
@@ -380,7 +500,7 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
             float num[4];
 #if MACE_K2_NORELOAD
             float gv[4][NG][K];  // every pixel's rows as gathered (before the batch touched them)
-#else
+#elif !MACE_K2_LEAN
             float e0v[NG][K];  // pixel 0's rows as gathered (nothing in the batch has touched them yet)
 #endif
             int ab[4][NG];
@@ -399,7 +519,7 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
                         const float ee = sb[ab[p][g] + q * U];
 #if MACE_K2_NORELOAD
                         gv[p][g][q] = ee;
-#else
+#elif !MACE_K2_LEAN
                         if (p == 0) e0v[g][q] = ee;
 #endif
                         // kW: a' = a sqrt(lambda) against e' = sqrt(lambda) e
@@ -445,11 +565,19 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
                 k1 += __shfl_xor_sync(FULL, h16 ? num[1] : num[3], 16);
                 float kp = h8 ? k1 : k0;
                 kp += __shfl_xor_sync(FULL, h8 ? k0 : k1, 8);
-                kp -= beta * g;
+                if (!MW || wid == 0) kp -= beta * g;  // the prior gradient once per block
 #pragma unroll
                 for (int o = 4; o; o >>= 1) {
                     kp += __shfl_xor_sync(FULL, kp, o);
                     den_l += __shfl_xor_sync(FULL, den_l, o);
+                }
+                if constexpr (MW > 0) {  // theta1 = sum of the chunks' partials, in chunk order in every warp
+                    float* sp = s_part + ((b & 1) * 4 + pp) * CH;
+                    if ((lane & 7) == 0) sp[wid] = kp;
+                    bar();
+                    float t = 0.f;
+                    for (int w2 = 0; w2 < CH; ++w2) t += sp[w2];
+                    kp = t;
                 }
 #pragma unroll
                 // every lane needs all four pixels' sums and their z, v: the group leaders store
@@ -554,12 +682,14 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
 #else
             // scatter e -= alpha_p a_p in pixel order (a row may be shared within the batch, never
             // within one pixel): pixel 0 from the gathered values, then reload-modify-store
+#if !MACE_K2_LEAN
 #pragma unroll
             for (int g = 0; g < NG; ++g)
 #pragma unroll
                 for (int q = 0; q < K; ++q) sb[ab[0][g] + q * U] = fmaf(-alpha[0], av[0][g][q], e0v[g][q]);
+#endif
 #pragma unroll
-            for (int p = 1; p < 4; ++p) {
+            for (int p = MACE_K2_LEAN ? 0 : 1; p < 4; ++p) {
                 float ev[NG][K];
 #pragma unroll
                 for (int g = 0; g < NG; ++g)
@@ -594,14 +724,35 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
             float* ep = eg + (st - s0);
             const float* d = sb + g * W * U + lane;
             const int nv = (cnt + s0 + 3) >> 2;
+#if MACE_K2_RAW
+            const float4* rr = raw + (size_t)(32 * g + lane) * RQ;  // the snapshot e0 the band was staged from
+#endif
             for (int v = 0; v < nv; ++v) {
                 float dv[4];
+#if MACE_K2_RAW
+                const float4 r4 = rr[v];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int o = 4 * v + i - s0;
+                    const float e0 = i == 0 ? r4.x : i == 1 ? r4.y : i == 2 ? r4.z : r4.w;
+                    dv[i] = (o >= 0 && o < cnt) ? d[o * U] - e0 : 0.f;
+                }
+#else
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int o = 4 * v + i - s0;
                     dv[i] = (o >= 0 && o < cnt) ? d[o * U] - d[o * U + E0] : 0.f;
                 }
-                if (dv[0] != 0.f || dv[1] != 0.f || dv[2] != 0.f || dv[3] != 0.f)
+#endif
+                if (P.det) {  // integer adds commute: the class's sum is independent of the tile order
+                    unsigned long long* q = A.ed + (st - s0) + 4 * v;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (dv[i] != 0.f)
+                            asm volatile("red.global.add.u64 [%0], %1;" ::"l"(q + i),
+                                         "l"((unsigned long long)__double2ll_rn((double)dv[i] * kDetScale))
+                                         : "memory");
+                } else if (dv[0] != 0.f || dv[1] != 0.f || dv[2] != 0.f || dv[3] != 0.f)
                     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(ep + 4 * v), "f"(dv[0]),
                                  "f"(dv[1]), "f"(dv[2]), "f"(dv[3])
                                  : "memory");
@@ -613,7 +764,7 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
         for (int i0 = 0; i0 < SS; i0 += 32) {
             const int i = i0 + lane;
             const int rr = r0 + i / S, cc = c0 + i % S;
-            if (i < SS && rr < n && cc < n) {
+            if (i < SS && rr < n && cc < n && wid == 0) {
                 const size_t s = (size_t)rr * n + cc;
                 const float zn = zt[(i / S + 1) * S2 + (i % S + 1)];
                 __stcg(z + s, zn);
@@ -631,20 +782,24 @@ __global__ void __launch_bounds__(32, kW ? MACE_K2_MINB_W : MACE_K2_MINB) k_icd_
         dw2 = warp_sum_d(dw2);
         wn2 = warp_sum_d(wn2);
         wo2 = warp_sum_d(wo2);
-        if (lane == 0) {  // dsq: every lane holds the same sum (alpha is warp-uniform)
+        if (lane == 0 && wid == 0) {  // dsq: every lane holds the same sum (alpha is warp-uniform)
             double* o = P.part + (size_t)item * 4;
             o[0] = (double)dsq;
             o[1] = dw2;
             o[2] = wn2;
             o[3] = wo2;
         }
-        __syncwarp();
+        __syncwarp();  // every lane's write-back reads of the band and the raw area are done
         if (!more) break;
         item = nitem;
         code = ncode;
         band_of(code, myb);
+#if MACE_K2_RAW
+        issue_windows(code, myb);
+#else
         ewin_of(code, myb, ew, sh);
-        state_of(code, zpre, wpre, vpre);
+#endif
+        if (!MW || wid == 0) state_of(code, zpre, wpre, vpre);
     }
 }
 

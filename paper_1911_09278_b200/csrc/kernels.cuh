@@ -377,9 +377,9 @@ __device__ __forceinline__ void sv_load_recs(const uint32_t* __restrict__ rb, in
 
 template <int K, int NG, bool kW>
 __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n_items, const uint32_t* queue,
-                                                   int n_side, int S, int nb, int W)
+                                                   int n_side, int S, int nb, int W, int CH)
 {
-    extern __shared__ float s_lam[];  // [NG][W][32]
+    extern __shared__ float s_lam[];  // [CH * NG][W][32]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int item = blockIdx.x;
     if (item >= n_items) return;
@@ -389,16 +389,20 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
     const AgentDev& A = agents[code >> kAgentShift];
     const int sv = (int)(code & kSvMask);
     const int r0 = (sv / A.n_sv_side) * S, c0 = (sv % A.n_sv_side) * S;
-    const uint32_t* __restrict__ rbase = A.rec0 + (size_t)sv * nb * 4 * recw;
-    uint32_t* __restrict__ wbase = kW ? A.recw + (size_t)sv * nb * 4 * recw : nullptr;
+    // records [sv][batch][chunk][slot][recw]; this warp takes batches b = warp + 4 k, and for each
+    // the CH chunks (units u = k CH + c), the next unit's records in flight
+    const uint32_t* __restrict__ rbase = A.rec0 + (size_t)sv * nb * CH * 4 * recw;
+    uint32_t* __restrict__ wbase = kW ? A.recw + (size_t)sv * nb * CH * 4 * recw : nullptr;
+    auto unit_ofs = [&](int u) { return ((size_t)(warp + 4 * (u / CH)) * CH + u % CH) * 4 * recw; };
+    const int nu = (warp < nb ? (nb - warp + 3) / 4 : 0) * CH;
 
-    // first batch's records in flight while the window is staged
+    // first unit's records in flight while the window is staged
     float a[4][NG][K];
     uint32_t ow[4];
-    if (warp < nb) sv_load_recs<K, NG>(rbase + (size_t)warp * 4 * recw, lane, a, ow);
+    if (nu > 0) sv_load_recs<K, NG>(rbase + unit_ofs(0), lane, a, ow);
 
     const int2* bt = A.band + (size_t)sv * A.V;
-    for (int g = warp; g < NG; g += 4) {
+    for (int g = warp; g < CH * NG; g += 4) {
         const int j = 32 * g + lane;
         const int2 bj = j < A.V ? bt[j] : make_int2(0, 0);
         float* sl = s_lam + (size_t)g * W * 32 + lane;
@@ -407,25 +411,27 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
     }
     __syncthreads();
     if (!kW) {  // the band's lambda rows, laid out as the K2 shared-memory plane
-        float* lb = A.lb + (size_t)sv * NG * W * 32;
-        for (int i = threadIdx.x; i < NG * W * 32; i += blockDim.x) lb[i] = s_lam[i];
+        float* lb = A.lb + (size_t)sv * CH * NG * W * 32;
+        for (int i = threadIdx.x; i < CH * NG * W * 32; i += blockDim.x) lb[i] = s_lam[i];
     }
 
-    for (int b = warp; b < nb; b += 4) {
+    float t2[4] = {0.f, 0.f, 0.f, 0.f}, cx[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int u = 0; u < nu; ++u) {
+        const int b = warp + 4 * (u / CH), ch = u % CH;
         float an[4][NG][K];
         uint32_t own[4];
-        if (b + 4 < nb) sv_load_recs<K, NG>(rbase + (size_t)(b + 4) * 4 * recw, lane, an, own);
+        if (u + 1 < nu) sv_load_recs<K, NG>(rbase + unit_ofs(u + 1), lane, an, own);
         float l[4][NG][K];
 #pragma unroll
         for (int p = 0; p < 4; ++p)
 #pragma unroll
             for (int g = 0; g < NG; ++g) {
-                const float* sl = s_lam + ((size_t)g * W + ((ow[p] >> (8 * g)) & 0xffu)) * 32 + lane;
+                const float* sl = s_lam + ((size_t)(ch * NG + g) * W + ((ow[p] >> (8 * g)) & 0xffu)) * 32 + lane;
 #pragma unroll
                 for (int q = 0; q < K; ++q) l[p][g][q] = a[p][g][q] != 0.f ? sl[q * 32] : 0.f;
             }
         if (kW) {  // weighted record a sqrt(lambda): theta2 and the cross terms are its plain products
-            uint32_t* wb = wbase + (size_t)b * 4 * recw;
+            uint32_t* wb = wbase + unit_ofs(u);
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 uint32_t* w = wb + (size_t)p * recw;
@@ -450,7 +456,6 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
                 }
             }
         }
-        float t2[4] = {0.f, 0.f, 0.f, 0.f}, cx[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
             int o[4];
@@ -471,21 +476,27 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
                         for (int qj = 0; qj < K; ++qj)  // row o_i + q of pixel i is row o_j + qj of pixel j
                             if (o[i] + q == o[j] + qj) cx[x] = fmaf(a[i][g][q] * a[j][g][qj], l[i][g][q], cx[x]);
         }
+        if (ch == CH - 1) {  // the batch's sums over every chunk's views
 #pragma unroll
-        for (int p = 0; p < 4; ++p) t2[p] = warp_sum(t2[p]);
+            for (int p = 0; p < 4; ++p) t2[p] = warp_sum(t2[p]);
 #pragma unroll
-        for (int x = 0; x < 6; ++x) cx[x] = warp_sum(cx[x]);
-        float v = 0.f;
+            for (int x = 0; x < 6; ++x) cx[x] = warp_sum(cx[x]);
+            float v = 0.f;
 #pragma unroll
-        for (int k = 0; k < 10; ++k)
-            if (lane == k) v = k < 4 ? t2[k & 3] : cx[(k - 4) % 6];
-        if (lane < 16) A.bc[((size_t)sv * nb + b) * 16 + lane] = v;
-        if (lane < 4) {  // theta2 image (cost kernels, diagnostics)
-            const int i = (b % bpc) * 4 + lane, cls = b / bpc;
-            if (i < per_class) {
-                const int lr = (cls >> 1) + 2 * (i / h), lc = (cls & 1) + 2 * (i % h);
-                if (r0 + lr < n_side && c0 + lc < n_side) A.th[(size_t)(r0 + lr) * n_side + c0 + lc] = v;
+            for (int k = 0; k < 10; ++k)
+                if (lane == k) v = k < 4 ? t2[k & 3] : cx[(k - 4) % 6];
+            if (lane < 16) A.bc[((size_t)sv * nb + b) * 16 + lane] = v;
+            if (lane < 4) {  // theta2 image (cost kernels, diagnostics)
+                const int i = (b % bpc) * 4 + lane, cls = b / bpc;
+                if (i < per_class) {
+                    const int lr = (cls >> 1) + 2 * (i / h), lc = (cls & 1) + 2 * (i % h);
+                    if (r0 + lr < n_side && c0 + lc < n_side) A.th[(size_t)(r0 + lr) * n_side + c0 + lc] = v;
+                }
             }
+#pragma unroll
+            for (int p = 0; p < 4; ++p) t2[p] = 0.f;
+#pragma unroll
+            for (int x = 0; x < 6; ++x) cx[x] = 0.f;
         }
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
@@ -764,6 +775,19 @@ __global__ void __launch_bounds__(256) k_tail(const float* __restrict__ W, int n
 }
 
 __global__ void k_reset_head(unsigned* head) { *head = 0u; }
+
+// deterministic mode, after each colour class: e += fixed-point deltas (then zeroed)
+__global__ void k_fold_delta(float* __restrict__ e, unsigned long long* __restrict__ ed, int rows, const int* done)
+{
+    if (done && *done) return;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        const unsigned long long q = ed[r];
+        if (q) {
+            e[r] += (float)((double)(long long)q * (1.0 / kDetScale));
+            ed[r] = 0ull;
+        }
+    }
+}
 
 __global__ void k_fill(float* p, size_t n, float v)
 {

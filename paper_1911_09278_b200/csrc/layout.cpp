@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstring>
 #include <stdexcept>
+#include <string>
 
 #include "internal.h"
 
@@ -74,11 +75,15 @@ void build_raster_layout(const AgentCSC& csc, int n, RasterLayout& out)
 
 void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SVLayout& out, int ng)
 {
-    if (V > 128) throw std::runtime_error("super-voxel layout: at most 128 views per agent (4 lane groups)");
     out.svs = S;
     out.views = V;
-    out.ng = std::max((V + 31) / 32, ng);
-    if (out.ng > 4) throw std::runtime_error("super-voxel layout: at most 4 view groups");
+    // view groups of 32; more than 4 groups (> 128 views per agent) are split into chunks of 3
+    // groups, one warp per chunk of a tile (k_sv.cuh multi-warp tiles)
+    const int ng_total = std::max((V + 31) / 32, ng);
+    out.chunks = ng_total > 4 ? (ng_total + 2) / 3 : 1;
+    out.ng = ng_total > 4 ? 3 : ng_total;
+    if (out.chunks > kSvMaxChunks)
+        throw std::runtime_error("super-voxel layout: at most " + std::to_string(32 * 3 * kSvMaxChunks) + " views per agent");
     out.n_sv_side = (n_side + S - 1) / S;
     out.n_sv = out.n_sv_side * out.n_sv_side;
     out.band.assign((size_t)out.n_sv * V, {0, 0});
@@ -130,7 +135,9 @@ void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SV
     out.nb = sv_batches(S);
     const int G = out.ng, KK = out.K;
     out.rec = G * 32 * KK + 32;
-    const size_t per_tile = (size_t)out.nb * kSvBatch * out.rec;
+    const int CH = out.chunks;
+    if (CH > 1 && KK != 2) throw std::runtime_error("multi-warp super-voxel tiles need at most 2 entries per (pixel, view)");
+    const size_t per_tile = (size_t)out.nb * CH * kSvBatch * out.rec;
     out.data.assign((size_t)out.n_sv * per_tile, 0u);
     // pass 2: scatter each entry into its (slot, group, lane, k) position
     for (int sv = 0; sv < out.n_sv; ++sv) {
@@ -142,9 +149,8 @@ void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SV
             const int r = r0 + k / S, c = c0 + k % S;
             if (r >= n_side || c >= n_side) continue;
             const int64_t s = (int64_t)r * n_side + c;
-            uint32_t* rec = &out.data[(size_t)sv * per_tile + (size_t)t * out.rec];
-            float* pv = reinterpret_cast<float*>(rec);
-            uint32_t* po = rec + G * 32 * KK;
+            // chunk h of slot t: records [sv][batch][chunk][slot][rec]
+            uint32_t* rec0 = &out.data[(size_t)sv * per_tile + ((size_t)(t / kSvBatch) * CH * kSvBatch + t % kSvBatch) * out.rec];
             // entries of one (pixel, view) are consecutive in the column (rows ascending); the slot
             // offset is pulled back so that all K addressed rows stay inside the window (rows past
             // cnt would alias the lane's next window or memory after the band)
@@ -152,7 +158,11 @@ void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SV
             float vals[4] = {0.f, 0.f, 0.f, 0.f};
             auto flush = [&]() {
                 if (cur_j < 0) return;
-                const int g = cur_j >> 5, l = cur_j & 31, cnt = bt[cur_j].y;
+                const int gt = cur_j >> 5, l = cur_j & 31, cnt = bt[cur_j].y;
+                const int g = gt % G;  // group inside the view's chunk gt / G
+                uint32_t* rec = rec0 + (size_t)(gt / G) * kSvBatch * out.rec;
+                float* pv = reinterpret_cast<float*>(rec);
+                uint32_t* po = rec + G * 32 * KK;
                 const int o = std::min(o0, std::max(cnt, KK) - KK);
                 po[l] |= (uint32_t)o << (8 * g);
                 for (int u = 0; u < m; ++u) pv[((size_t)g * 32 + l) * KK + (o0 - o) + u] = vals[u];

@@ -69,7 +69,7 @@ struct AgentMem {
     DBuf<uint32_t> rec, ridx;
     DBuf<uint32_t> recw;  // weighted records a sqrt(lambda) (k_sv_consts; single-slice contexts)
     int R = 0, n_sv_side = 0, n_sv = 0, max_col = 0;
-    int wcap = 0, ng = 1, K = 2, nb = 0, rec_words = 0;  // lane-per-view layout geometry
+    int wcap = 0, ng = 1, K = 2, nb = 0, rec_words = 0, chunks = 1;  // lane-per-view layout geometry
     int64_t entries = 0, nnz = 0, duplicates = 0;
     DBuf<uint32_t> queue;  // this agent alone, colour order
     float beta_eff = 0.f, inv_s2 = 0.f;
@@ -113,6 +113,13 @@ struct Ctx {
     DBuf<double> refpart;
     double ref_norm2 = 0.0;
     int sv_ng = 1, sv_wcap = 1, sv_K = 2;  // lane-per-view band geometry (max over agents)
+    int sv_chunks = 1;                      // view chunks (warps) per tile (agents with > 128 views)
+    // deterministic class-synchronous mode (mace_set_deterministic): one K2 launch per colour class,
+    // e deltas accumulated in fixed point (ED) and folded between classes
+    bool det = false;
+    DBuf<unsigned long long> ED;
+    std::vector<int> cls_all, cls_one;  // class boundaries of the combined and the single-agent queues
+    DBuf<unsigned> heads;               // one work counter per class
     bool weighted = false;                  // K2 on weighted records: e kept as sqrt(lambda) e (k_sv.cuh)
     bool allow_weighted = true;             // mace_set_weighting
     DBuf<float> SQ;                         // sqrt(lambda) per local agent row (weighted mode)
@@ -199,6 +206,7 @@ static void dispatch_sv(Ctx* c, const PassParams& P, int na)
     L.agents_in_queue = na;
     L.K = c->sv_K;
     L.NG = c->sv_ng;
+    L.chunks = c->sv_chunks;
     L.weighted = c->weighted;
     switch (c->S) {
         case 2: sv_launch_s2(L, P); break;
@@ -222,6 +230,7 @@ static PassParams base_params(Ctx* c)
     P.S = c->S;
     P.ng = c->sv_ng;
     P.wcap = c->sv_wcap;
+    P.chunks = c->sv_chunks;
     P.head = c->head.p;
     P.part = c->part.p;
     P.done = c->done.p;
@@ -252,16 +261,36 @@ static void run_pass(Ctx* c, int mode, float rho, const float* gimg, int a0, int
         k2_end(c, ev);
         return;
     }
+    if (na != c->n_local && na != 1) throw std::runtime_error("run_pass: single agent or all agents");
+    const uint32_t* q = na == c->n_local ? c->queue.p : c->am[a0]->queue.p;
+    const int nq = na == c->n_local ? c->n_items : c->am[a0]->n_sv;
+    if (c->det) {
+        // class-synchronous: every tile of a class stages e as it stood when the class started and
+        // adds its change into the fixed-point buffer, folded into e before the next class; the
+        // result does not depend on which warp took which tile or when (bitwise reproducible)
+        const std::vector<int>& cs = na == c->n_local ? c->cls_all : c->cls_one;
+        const int ncls = (int)cs.size() - 1;
+        CK(cudaMemsetAsync(c->heads.p, 0, sizeof(unsigned) * ncls, c->stream));
+        cudaEvent_t ev = k2_begin(c);
+        for (int k = 0; k < ncls; ++k) {
+            if (cs[k + 1] == cs[k]) continue;
+            PassParams Pk = P;
+            Pk.queue = q + cs[k];
+            Pk.n_items = cs[k + 1] - cs[k];
+            Pk.part = c->part.p + (size_t)cs[k] * 4;
+            Pk.head = c->heads.p + k;
+            Pk.det = 1;
+            dispatch_sv(c, Pk, na);
+            k_fold_delta<<<c->num_sms * 4, 256, 0, c->stream>>>(c->E.p, c->ED.p, c->total_rows, c->done.p);
+            CK(cudaGetLastError());
+        }
+        k2_end(c, ev);
+        return;
+    }
     CK(cudaMemsetAsync(c->head.p, 0, sizeof(unsigned), c->stream));
     cudaEvent_t ev = k2_begin(c);
-    if (na == c->n_local) {
-        P.queue = c->queue.p;
-        P.n_items = c->n_items;
-    } else {
-        if (na != 1) throw std::runtime_error("run_pass: single agent or all agents");
-        P.queue = c->am[a0]->queue.p;
-        P.n_items = c->am[a0]->n_sv;
-    }
+    P.queue = q;
+    P.n_items = nq;
     dispatch_sv(c, P, na);
     k2_end(c, ev);
 }
@@ -291,11 +320,11 @@ static void compute_theta2(Ctx* c)
     } else {
         // one block per (agent, tile) item, the tile's lambda window in shared memory
         const int nb = sv_batches(c->S);
-        const size_t smem = sizeof(float) * c->sv_ng * c->sv_wcap * 32;
+        const size_t smem = sizeof(float) * c->sv_chunks * c->sv_ng * c->sv_wcap * 32;
         auto go = [&](auto kern) {
             if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             kern<<<(unsigned)std::max(1, c->n_items), 128, smem, c->stream>>>(c->d_agents.p, c->n_items, c->queue.p,
-                                                                            c->n_side, c->S, nb, c->sv_wcap);
+                                                                            c->n_side, c->S, nb, c->sv_wcap, c->sv_chunks);
         };
         const int key = c->sv_K * 10 + c->sv_ng + (c->weighted ? 100 : 0);
         switch (key) {
@@ -339,6 +368,13 @@ static void consensus(Ctx* c, float scale, float* out, bool with_ref)
     CK(cudaGetLastError());
 }
 
+// dynamic shared memory of one K2 block: one warp region per view chunk (+ the multi-warp area)
+static size_t sv_smem_bytes(Ctx* c, bool weighted)
+{
+    const int wpb = c->sv_chunks > 1 ? c->sv_chunks : kSvThreads / 32;
+    return (size_t)wpb * sv_warp_bytes(c->S, c->sv_ng, c->sv_wcap, weighted) + sv_block_extra_bytes(c->S, c->sv_chunks);
+}
+
 // Switch K2 between plain records (lambda plane in shared memory) and weighted records
 // a sqrt(lambda) with the error sinogram kept as sqrt(lambda) e (k_sv.cuh).  Called when data
 // are loaded; the caller refreshes e afterwards (mace_set_state / mace_states_from).
@@ -365,7 +401,7 @@ static void set_weighted(Ctx* c, bool on)
         A.rec = on ? m.recw.p : m.rec.p;
         A.sq = on ? c->SQ.p + rb[va] : nullptr;
     }
-    c->sv_smem = (kSvThreads / 32) * sv_warp_bytes(c->S, c->sv_ng, c->sv_wcap, on);
+    c->sv_smem = sv_smem_bytes(c, on);
     if (c->sv_smem > 227 * 1024) throw std::runtime_error("super-voxel band does not fit in shared memory");
     CK(cudaMemcpyAsync(c->d_agents.p, c->h_agents.data(), sizeof(AgentDev) * c->n_local, cudaMemcpyHostToDevice,
                        c->stream));
@@ -632,6 +668,7 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
     c->sv_ng = 1;
     c->sv_wcap = 1;
     c->sv_K = 2;
+    c->sv_chunks = 1;
     for (int a = 0; a < n_agents; ++a) {
         AgentMem& m = *c->am[a];
         m.d_views.alloc(m.views.size());
@@ -663,6 +700,7 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
             m.wcap = L.wcap;
             m.ng = L.ng;
             m.K = L.K;
+            m.chunks = L.chunks;
             m.n_sv = L.n_sv;
             m.n_sv_side = L.n_sv_side;
             m.duplicates = L.duplicates;
@@ -678,6 +716,7 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
         c->sv_ng = std::max(c->sv_ng, m.ng);
         c->sv_wcap = std::max(c->sv_wcap, m.wcap);
         c->sv_K = std::max(c->sv_K, m.K);
+        c->sv_chunks = std::max(c->sv_chunks, m.chunks);
     }
     // per local (virtual) agent: data arrays; each {e, lambda} block starts on a 16-byte boundary
     std::vector<int> rb(n_local + 1, 0);
@@ -704,7 +743,7 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
     CK(cudaMemset(c->BC.p, 0, sizeof(float) * std::max<size_t>(bcb[n_local], 1)));
     std::vector<size_t> lbb(n_local + 1, 0);  // band-lambda blocks
     for (int va = 0; va < n_local; ++va)
-        lbb[va + 1] = lbb[va] + (schedule == 0 ? (size_t)c->am[va % n_agents]->n_sv * c->sv_ng * c->sv_wcap * 32 : 0);
+        lbb[va + 1] = lbb[va] + (schedule == 0 ? (size_t)c->am[va % n_agents]->n_sv * c->sv_chunks * c->sv_ng * c->sv_wcap * 32 : 0);
     c->LB.alloc(std::max<size_t>(lbb[n_local], 1));
     c->h_agents.assign(n_local, AgentDev{});
     for (int va = 0; va < n_local; ++va) {
@@ -751,10 +790,12 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
         c->queue.alloc(q.size());
         CK(cudaMemcpy(c->queue.p, q.data(), sizeof(uint32_t) * q.size(), cudaMemcpyHostToDevice));
         c->n_items = (int)q.size();
-        for (int a = 0; a < n_agents; ++a)
+        for (int a = 0; a < n_agents; ++a) {
             if (c->am[a]->K != c->sv_K) throw std::runtime_error("agents with different (pixel, view) slot widths");
+            if (c->am[a]->chunks != c->sv_chunks) throw std::runtime_error("agents with different view-chunk counts");
+        }
         c->weighted = false;
-        c->sv_smem = (kSvThreads / 32) * sv_warp_bytes(c->S, c->sv_ng, c->sv_wcap, false);
+        c->sv_smem = sv_smem_bytes(c, false);
         if (c->sv_smem > 227 * 1024) throw std::runtime_error("super-voxel band does not fit in shared memory");
     } else {
         c->n_items = n_local;
@@ -814,11 +855,57 @@ int mace_set_schedule(void* p, double concurrency, int64_t max_warps)
     API_END
 }
 
+// class boundaries of a colour-ordered queue (build_queue with group 0): item i belongs to class
+// (tile row mod C, tile col mod C); classes must be contiguous and in order
+static std::vector<int> class_bounds(const std::vector<uint32_t>& q, int nss, int colours)
+{
+    const int C = std::max(1, std::min(colours, nss));
+    std::vector<int> cs(C * C + 1, (int)q.size());
+    int prev = -1;
+    for (size_t i = 0; i < q.size(); ++i) {
+        const int sv = (int)(q[i] & kSvMask), k = ((sv / nss) % C) * C + (sv % nss) % C;
+        if (k < prev) throw std::runtime_error("deterministic mode: the work queue is not in colour-class order");
+        for (int j = prev + 1; j <= k; ++j) cs[j] = (int)i;
+        prev = k;
+    }
+    return cs;
+}
+
+// Deterministic super-voxel passes: one K2 launch per colour class, every tile of a
+// class reading e as it stood at the class start, the tiles' e changes summed in 2^-40 fixed point
+// (order-independent) and folded between classes.  Bitwise reproducible run to run and for any grid
+// size / concurrency, at the cost of one launch and one fold per class.
+int mace_set_deterministic(void* p, int on)
+{
+    API_BEGIN
+    Ctx* c = C(p);
+    if (on && c->schedule != 0) throw std::runtime_error("deterministic mode needs the super-voxel schedule");
+    if (on && c->sv_group) throw std::runtime_error("deterministic mode needs agent groups off");
+    sync(c);
+    if (on) {
+        if (!c->ED.p) {
+            c->ED.alloc(c->total_rows);
+            CK(cudaMemset(c->ED.p, 0, sizeof(unsigned long long) * c->total_rows));
+        }
+        std::vector<int> rb(c->n_local + 1, 0);
+        CK(cudaMemcpy(rb.data(), c->row_base.p, sizeof(int) * (c->n_local + 1), cudaMemcpyDeviceToHost));
+        for (int va = 0; va < c->n_local; ++va) c->h_agents[va].ed = c->ED.p + rb[va];
+        CK(cudaMemcpy(c->d_agents.p, c->h_agents.data(), sizeof(AgentDev) * c->n_local, cudaMemcpyHostToDevice));
+        c->cls_all = class_bounds(build_queue(c->n_real, c->n_sv_side, c->colours, c->n_slices, 0), c->n_sv_side,
+                                  c->colours);
+        c->cls_one = class_bounds(build_queue(1, c->n_sv_side, c->colours), c->n_sv_side, c->colours);
+        if (c->heads.n < c->cls_all.size()) c->heads.alloc(c->cls_all.size());
+    }
+    c->det = on != 0;
+    API_END
+}
+
 int mace_set_agent_groups(void* p, int group)
 {
     API_BEGIN
     Ctx* c = C(p);
     if (c->schedule != 0) throw std::runtime_error("agent groups need the super-voxel schedule");
+    if (c->det && group) throw std::runtime_error("agent groups need the deterministic mode off");
     if (group < 0) throw std::runtime_error("group must be >= 0");
     std::vector<uint32_t> q = build_queue(c->n_real, c->n_sv_side, c->colours, c->n_slices, group);
     if ((int)q.size() != c->n_items) throw std::runtime_error("queue size changed");

@@ -21,7 +21,7 @@ import numpy as np
 from . import _native as N
 from .geometry import global_csr
 
-SCHEDULES = {"sv": 0, "raster": 1}
+SCHEDULES = {"sv": 0, "raster": 1, "sv-det": 0}  # sv-det: deterministic class-synchronous super-voxel passes
 SV_SIDES = (2, 4, 6, 8, 12, 16)  # tile sides compiled into k_icd_sv
 DEFAULT_SV = int(os.environ.get("MACE_SV", "8"))
 DEFAULT_COLOURS = int(os.environ.get("MACE_COLOURS", "4"))
@@ -152,7 +152,7 @@ def operator_for(matrices, device: int = 0) -> DeviceOperator:
     return _cached(("op", id(matrices), device), lambda: DeviceOperator(matrices, device), matrices)
 
 
-SV_MAX_VIEWS = 128  # lane-per-view layout: 4 groups of 32 views per agent
+SV_MAX_VIEWS = 16 * 96  # lane-per-view layout: up to 16 view chunks (warps) of 3 x 32 views per tile
 
 
 class AgentPlan(_Context):
@@ -165,15 +165,16 @@ class AgentPlan(_Context):
             raise ValueError(f"schedule must be one of {sorted(SCHEDULES)}")
         self.load_matrix(matrices)
         self.agent_views = [tuple(int(v) for v in vs) for vs in agent_views]
-        if schedule == "sv" and max(len(v) for v in self.agent_views) > SV_MAX_VIEWS and int(n_slices) == 1:
-            # the lane-per-view super-voxel layout holds at most 4 x 32 views per agent;
-            # agents with more views (few agents over many views, centralized ICD) run the raster pass
+        if schedule in ("sv", "sv-det") and max(len(v) for v in self.agent_views) > SV_MAX_VIEWS and int(n_slices) == 1:
+            # the lane-per-view super-voxel layout holds at most 16 chunks of 96 views per agent
+            # (multi-warp tiles); agents with more views run the raster pass
             schedule = "raster"
         self.schedule = schedule
+        det = schedule == "sv-det"
         counts = np.array([len(v) for v in self.agent_views], np.int32)
         flat = np.array([v for vs in self.agent_views for v in vs], np.int32)
         sv_eff = sv
-        if schedule == "sv":
+        if schedule in ("sv", "sv-det"):
             lim = min(sv, self.n_side + (self.n_side & 1))
             sv_eff = max([s for s in SV_SIDES if s <= max(lim, 2)])
         self.n_slices = int(n_slices)
@@ -183,6 +184,8 @@ class AgentPlan(_Context):
         self.n_agents = len(self.agent_views)
         self.n_local = self.n_agents * self.n_slices
         self.set_schedule(DEFAULT_CONCURRENCY, int(os.environ.get("MACE_SV_MAX_WARPS", "0")))
+        if det:
+            self.call("mace_set_deterministic", 1)
         # weighted records (a sqrt(lambda), k_sv.cuh) where the data allow them; MACE_WEIGHTED=0 forbids
         self.set_weighting(os.environ.get("MACE_WEIGHTED", "1") != "0")
 

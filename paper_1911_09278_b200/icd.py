@@ -149,9 +149,12 @@ def prox_solve(ws: AgentWorkspace, v, tol: float, max_passes: int = 500) -> np.n
 
 
 def icd_map_solve(problem, tol: float, beta: float | None = None, max_passes: int = 1000, x0=None,
-                  counter=None, on_pass=None, clamp_nonneg: bool = False, schedule: str = "raster",
+                  counter=None, on_pass=None, clamp_nonneg: bool = False, schedule: str | None = None,
                   device: int = 0) -> np.ndarray:
-    """Centralized full-data ICD without a proximal term (icd.py:306-345)."""
+    """Centralized full-data ICD without a proximal term (icd.py:306-345).
+
+    ``schedule`` None: the reference's raster order up to 65,536 pixels, the parallel super-voxel
+    pass (multi-warp tiles: one warp per 96 views) above; same fixed point."""
     if tol <= 0:
         raise ValueError("tol must be > 0")
     all_views = ViewSubset(0, tuple(range(problem.geom.n_views)))

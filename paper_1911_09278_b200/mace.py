@@ -132,7 +132,8 @@ class EquitCounter:
 @dataclass(frozen=True)
 class MaceConfig:
     """Outer-loop configuration (mace.py:124-163) plus the GPU schedule knobs:
-    ``schedule`` "sv" (parallel super-voxel passes) or "raster" (reference order),
+    ``schedule`` "sv" (parallel super-voxel passes), "sv-det" (the same, class-synchronous and
+    bitwise reproducible) or "raster" (reference order),
     ``sv_side`` / ``colours`` (tile side and colour-class stride of the SV queue)."""
 
     n_subsets: int
@@ -168,8 +169,8 @@ class MaceConfig:
             raise ValueError("tol must be > 0")
         if self.residuals not in ("final", "none"):
             raise ValueError("residuals must be 'final' or 'none'")
-        if self.schedule not in ("sv", "raster"):
-            raise ValueError("schedule must be 'sv' or 'raster'")
+        if self.schedule not in ("sv", "raster", "sv-det"):
+            raise ValueError("schedule must be 'sv', 'sv-det' or 'raster'")
 
 
 class ConvergenceLog:
