@@ -157,6 +157,12 @@ __device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __
 // an occupancy experiment for 16 resident warps per SM)
 #define MACE_K2_LEAN 0
 #endif
+#ifndef MACE_K2_TRIM
+// 1: issue trims of the batch step: the qGGMRF p = 2 / no-clamp path as its own loop copy (no
+// per-batch tests of the prior kind and the clamp), the zt store index computed by the storing lane
+// only, the L2 prefetch pointer advanced per batch, and band addresses by one byte permute
+#define MACE_K2_TRIM 1
+#endif
 #ifndef MACE_K2_MINB
 #define MACE_K2_MINB 12  // resident warps per SM the register budget is sized for
 #endif
@@ -202,8 +208,8 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
 #endif
     const int n = P.n_side;
     const PriorC& PR = P.pr;
-    const bool quad = PR.kind == 0;
-    const bool p2 = PR.p_is_2;
+    const bool quad_ = PR.kind == 0;
+    const bool p2_ = PR.p_is_2;
     const int kk = lane & 7;  // prior: lane 8p + kk owns neighbour kk of batch pixel p (models.py:50-52)
     const int pp = lane >> 3;
     const int ndr = c_dr[kk], ndc = c_dc[kk];
@@ -328,7 +334,7 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
         const int r0 = (sv / nsv) * S, c0 = (sv % nsv) * S;
         const bool full = r0 + S <= n && c0 + S <= n;  // interior tile: no image-edge checks
         const float beta = A.beta_eff, inv_s2 = A.inv_s2;
-        const int clamp = A.clamp;
+        const int clamp_ = A.clamp;
         // records [sv][batch][chunk][slot][RECW]: this warp's chunk, batch stride BST
         const size_t BST = (size_t)CH * 4 * RECW;
         const uint32_t* __restrict__ recs = A.rec + (size_t)sv * NB * BST + (size_t)wid * 4 * RECW;
@@ -465,10 +471,25 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
         __syncwarp();        // ... and every other lane's; band / zt / v / w stores visible
         // kFull: the tile lies inside the image (all but the last tile row / column), so no slot
         // needs the image-edge test
-        auto step = [&](const int b, const SvBatch<K, NG>& C, SvBatch<K, NG>& Nx, auto full_tag) {
+#if MACE_K2_PF > 0 && MACE_K2_TRIM
+        // L2 prefetch pointer of batch b + PF: this tile's records, then the next tile's
+        const uint32_t* pfp = MACE_K2_PF < NB ? recs + (size_t)MACE_K2_PF * BST : nrecs;
+#endif
+        // kFast: qGGMRF with p = 2 (the fused qg_term), no quadratic term, no clamp -- the configured
+        // path of every benchmark -- compiled without the per-batch tests
+        auto step = [&](const int b, const SvBatch<K, NG>& C, SvBatch<K, NG>& Nx, auto full_tag, auto fast_tag) {
             constexpr bool kFull = decltype(full_tag)::value;
+            constexpr bool kFast = decltype(fast_tag)::value;
+            const bool quad = kFast ? false : quad_;
+            const bool p2 = kFast ? true : p2_;
+            const int clamp = kFast ? 0 : clamp_;
             if (b + 1 < NB) load_batch<K, NG>(Nx, recs + (size_t)(b + 1) * BST, lane);
-#if MACE_K2_PF > 0
+#if MACE_K2_PF > 0 && MACE_K2_TRIM
+            if (lane == 0 && pfp)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pfp), "r"((uint32_t)(4 * RECW * 4))
+                             : "memory");
+            pfp = b + MACE_K2_PF + 1 == NB ? nrecs : (pfp ? pfp + BST : nullptr);
+#elif MACE_K2_PF > 0
             // records of batch b + PF (this tile's or the next one's) pulled into L2 by one bulk
             // prefetch (TMA unit, no LSU work, no registers): the register load one batch ahead then
             // sees L2 rather than DRAM latency
@@ -503,12 +524,18 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
 #elif !MACE_K2_LEAN
             float e0v[NG][K];  // pixel 0's rows as gathered (nothing in the batch has touched them yet)
 #endif
-            int ab[4][NG];
+            int ab[4][NG];  // byte offsets of the slots' first rows in the band
             const auto& av = C.a;
+#define BANDB(a, q, plane) (*reinterpret_cast<float*>(reinterpret_cast<char*>(sb) + (a) + 4 * ((q) * U + (plane))))
 #pragma unroll
             for (int p = 0; p < 4; ++p)
 #pragma unroll
-                for (int g = 0; g < NG; ++g) ab[p][g] = (g * W + (int)((C.ob[p] >> (8 * g)) & 0xffu)) * U + lane;
+                for (int g = 0; g < NG; ++g) {
+                    if constexpr (MACE_K2_TRIM && U == 64)  // 4 o U bytes = byte g of the offset word moved to bits 8..15
+                        ab[p][g] = (int)__byte_perm(C.ob[p], 0u, 0x4404u | (g << 4)) + 4 * (g * W * U + lane);
+                    else
+                        ab[p][g] = 4 * ((g * W + (int)((C.ob[p] >> (8 * g)) & 0xffu)) * U + lane);
+                }
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 float a0 = 0.f, a1 = 0.f;
@@ -516,14 +543,14 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
                 for (int g = 0; g < NG; ++g)
 #pragma unroll
                     for (int q = 0; q < K; ++q) {
-                        const float ee = sb[ab[p][g] + q * U];
+                        const float ee = BANDB(ab[p][g], q, 0);
 #if MACE_K2_NORELOAD
                         gv[p][g][q] = ee;
 #elif !MACE_K2_LEAN
                         if (p == 0) e0v[g][q] = ee;
 #endif
                         // kW: a' = a sqrt(lambda) against e' = sqrt(lambda) e
-                        const float al = kW ? av[p][g][q] : av[p][g][q] * sb[ab[p][g] + q * U + 32];
+                        const float al = kW ? av[p][g][q] : av[p][g][q] * BANDB(ab[p][g], q, 32);
                         if (q & 1) a1 = fmaf(al, ee, a1);
                         else a0 = fmaf(al, ee, a0);
                     }
@@ -598,11 +625,15 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
             // the four 1-D solves (icd.py:128-134): everything but the coupling to earlier pixels of
             // the batch is independent across p; the reference skips pixels with den <= 0
             float nm[4], rd[4], zs[4];
+#if !MACE_K2_TRIM
             int ci[4];
+#endif
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 const float den_p = den4[p];
+#if !MACE_K2_TRIM
                 ci[p] = (kx[p] / S + 1) * S2 + kx[p] % S + 1;
+#endif
                 zs[p] = zs4[p];
                 float dn = den_p + bk[p] + inv_s2;
                 nm[p] = num[p];
@@ -637,13 +668,20 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
             {  // lane p < 4 stores pixel p's new value (one store instead of four); the next reads of
                // zt by other lanes come after a __syncwarp
                 float zn = zs[0] + alpha[0];
-                int cw = ci[0];
                 bool okw = ok[0];
+#if MACE_K2_TRIM
+                const int km = (int)((kxw >> (8 * (lane & 3))) & 0xffu);  // this lane's slot pixel
+                const int cw = (km / S + 1) * S2 + km % S + 1;
+#else
+                int cw = ci[0];
+#endif
 #pragma unroll
                 for (int p = 1; p < 4; ++p)
                     if (lane == p) {
                         zn = zs[p] + alpha[p];
+#if !MACE_K2_TRIM
                         cw = ci[p];
+#endif
                         okw = ok[p];
                     }
                 if (lane < 4 && okw) zt[cw] = zn;
@@ -665,7 +703,7 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
                     for (int k = 0; k < K; ++k) ev[k] = gv[p][g][k];
 #pragma unroll
                     for (int q = 0; q < p; ++q) {
-                        const int d = ab[p][g] - ab[q][g];
+                        const int d = (ab[p][g] - ab[q][g]) / 4;
 #pragma unroll
                         for (int k = 0; k < K; ++k) {
                             // the length of q's entry on this row, 0 if q does not touch it (selects, not
@@ -677,7 +715,7 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
                         }
                     }
 #pragma unroll
-                    for (int k = 0; k < K; ++k) sb[ab[p][g] + k * U] = fmaf(-alpha[p], av[p][g][k], ev[k]);
+                    for (int k = 0; k < K; ++k) BANDB(ab[p][g], k, 0) = fmaf(-alpha[p], av[p][g][k], ev[k]);
                 }
 #else
             // scatter e -= alpha_p a_p in pixel order (a row may be shared within the batch, never
@@ -686,7 +724,7 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
 #pragma unroll
             for (int g = 0; g < NG; ++g)
 #pragma unroll
-                for (int q = 0; q < K; ++q) sb[ab[0][g] + q * U] = fmaf(-alpha[0], av[0][g][q], e0v[g][q]);
+                for (int q = 0; q < K; ++q) BANDB(ab[0][g], q, 0) = fmaf(-alpha[0], av[0][g][q], e0v[g][q]);
 #endif
 #pragma unroll
             for (int p = MACE_K2_LEAN ? 0 : 1; p < 4; ++p) {
@@ -694,27 +732,36 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
 #pragma unroll
                 for (int g = 0; g < NG; ++g)
 #pragma unroll
-                    for (int q = 0; q < K; ++q) ev[g][q] = sb[ab[p][g] + q * U];
+                    for (int q = 0; q < K; ++q) ev[g][q] = BANDB(ab[p][g], q, 0);
 #pragma unroll
                 for (int g = 0; g < NG; ++g)
 #pragma unroll
-                    for (int q = 0; q < K; ++q) sb[ab[p][g] + q * U] = fmaf(-alpha[p], av[p][g][q], ev[g][q]);
+                    for (int q = 0; q < K; ++q) BANDB(ab[p][g], q, 0) = fmaf(-alpha[p], av[p][g][q], ev[g][q]);
             }
 #endif
         };
-        if (full) {
-#pragma unroll 1
-            for (int b = 0; b < NB; b += 2) {  // ping-pong record buffers (NB is a multiple of 4)
-                step(b, cur, nxt, std::true_type{});
-                step(b + 1, nxt, cur, std::true_type{});
+        // ping-pong record buffers (NB is a multiple of 4); one loop copy per (full, fast) pair
+#define K2_BATCHES(FT, KT)                                 \
+    _Pragma("unroll 1") for (int b = 0; b < NB; b += 2)    \
+    {                                                      \
+        step(b, cur, nxt, FT{}, KT{});                     \
+        step(b + 1, nxt, cur, FT{}, KT{});                 \
+    }
+        const bool fast = MACE_K2_TRIM && !quad_ && p2_ && !clamp_;
+        if (fast) {
+            if (full) {
+                K2_BATCHES(std::true_type, std::true_type)
+            } else {
+                K2_BATCHES(std::false_type, std::true_type)
             }
         } else {
-#pragma unroll 1
-            for (int b = 0; b < NB; b += 2) {
-                step(b, cur, nxt, std::false_type{});
-                step(b + 1, nxt, cur, std::false_type{});
+            if (full) {
+                K2_BATCHES(std::true_type, std::false_type)
+            } else {
+                K2_BATCHES(std::false_type, std::false_type)
             }
         }
+#undef K2_BATCHES
 
         // -- 5. fold the band's net change into global e (vector red.add over the window's aligned
         // 16-byte span: rows outside the window add +0); write z, Mann, partial norms

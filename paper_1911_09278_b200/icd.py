@@ -148,21 +148,40 @@ def prox_solve(ws: AgentWorkspace, v, tol: float, max_passes: int = 500) -> np.n
     raise ConvergenceError(f"prox_solve: no convergence to {tol:g} in {max_passes} passes", last_iterate=ws.state)
 
 
+CENTRAL_KAPPA = 16.0  # proximal anchor of the parallel centralized pass, x mean(theta2)
+
+
 def icd_map_solve(problem, tol: float, beta: float | None = None, max_passes: int = 1000, x0=None,
                   counter=None, on_pass=None, clamp_nonneg: bool = False, schedule: str | None = None,
-                  device: int = 0) -> np.ndarray:
+                  device: int = 0, kappa: float | None = None) -> np.ndarray:
     """Centralized full-data ICD without a proximal term (icd.py:306-345).
 
     ``schedule`` None: the reference's raster order up to 65,536 pixels, the parallel super-voxel
-    pass (multi-warp tiles: one warp per 96 views) above; same fixed point."""
+    pass (multi-warp tiles: one warp per 96 views) above.  Without a proximal term the tiles a
+    parallel pass runs at once see each other's sinogram updates late, which diverges for the
+    full-data operator (the reason for MACE's view split); the super-voxel
+    schedules therefore anchor every pass at the state it starts from (target v = z, weight
+    kappa x mean(theta2), default CENTRAL_KAPPA) and run at most max(4, tiles / 256) tiles at once:
+    a proximal-point iteration whose fixed point (alpha = 0 with v = z) is the same MAP.  Its
+    per-pass step is damped by about 1 / (1 + kappa), so the stopping test scales relnorm by
+    (1 + kappa)."""
     if tol <= 0:
         raise ValueError("tol must be > 0")
     all_views = ViewSubset(0, tuple(range(problem.geom.n_views)))
     ws = AgentWorkspace(problem, all_views, 1, sigma=None, beta=beta, state=x0, clamp_nonneg=clamp_nonneg,
                         schedule=schedule, device=device)
+    prox = ws.schedule != "raster"
+    scale = 1.0
+    if prox:
+        kappa = CENTRAL_KAPPA if kappa is None else float(kappa)
+        tiles = int(ws.plan.info()["n_items"])
+        ws.plan.set_schedule(max(4.0, tiles / 256.0) / tiles)
+        ws.plan.set_agent_params(0, ws.beta_eff, kappa * float(np.mean(ws.curv_data)), clamp_nonneg)
+        scale = 1.0 + kappa
     v = np.zeros(ws.n)
+    z = ws.state
     for k in range(max_passes):
-        dsq = ws._run_range(v, 0, ws.n)
+        dsq = ws._run_range(z if prox else v, 0, ws.n)
         ws.passes += 1
         if ws.passes % REFRESH_EVERY == 0:
             ws.refresh_error()
@@ -172,7 +191,7 @@ def icd_map_solve(problem, tol: float, beta: float | None = None, max_passes: in
         relnorm = np.sqrt(dsq) / max(float(np.linalg.norm(z)), 1e-300)
         if on_pass is not None:
             on_pass(k + 1, relnorm, z)
-        if relnorm < tol:
+        if relnorm * scale < tol:
             return z
     raise ConvergenceError(f"icd_map_solve: no convergence to {tol:g} in {max_passes} passes",
                            last_iterate=ws.state)

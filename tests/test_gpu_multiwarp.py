@@ -109,8 +109,9 @@ def test_multiwarp_pass_reaches_the_raster_prox_point(nv, weighted, monkeypatch)
 
 
 def _central_sv(config, passes):
-    """icd_map_solve on the super-voxel schedule for a fixed pass budget (tol below the fp32 /
-    float-atomic floor of relnorm, so the solve runs `passes` passes and raises with its iterate)."""
+    """icd_map_solve on the super-voxel schedule (proximal-anchored parallel passes, icd.py
+    CENTRAL_KAPPA) for a fixed pass budget (tol below the fp32 / float-atomic floor of relnorm, so
+    the solve runs `passes` passes and raises with its iterate)."""
     import time
 
     c = gen.CONFIGS[config]

@@ -251,9 +251,10 @@ def test_errors_and_validation(golden):
         mb.prox_solve(ws, np.zeros(prob.n), tol=0.0)
 
 
-def test_agents_with_many_views_take_the_raster_pass():
-    """More than 128 views per agent (beyond the lane-per-view SV layout) -> the raster pass,
-    iterate for iterate equal to the oracle's MACE: 2 agents x 150 views, ragged 37 x 37 image."""
+def test_agents_with_many_views():
+    """More than 128 views per agent: the super-voxel schedule runs multi-warp tiles (two 96-view
+    chunks per 150-view agent, tests/test_gpu_multiwarp.py), and the raster schedule stays iterate
+    for iterate equal to the oracle's MACE: 2 agents x 150 views, ragged 37 x 37 image."""
     ns, nv, nc = 37, 300, 41
     geom = mb.Geometry(ns, 1.0, nv, nc, 1.0)
     mats = mb.build_system_matrix(geom)
@@ -262,9 +263,10 @@ def test_agents_with_many_views_take_the_raster_pass():
     y, lam = gen.poisson_sinogram(gen.host_forward_project(mats, ph), 1e4, seed=9)
     prob = mb.ReconProblem(geom, mats, y, lam, mb.PriorParams("qggmrf", 50.0, 2.0, 1.2, 1.0, 0.01))
     plan = mb.engine.plan_for(mats, [s.view_indices for s in mb.partition_views(nv, 2)], schedule="sv")
-    assert plan.schedule == "raster"
+    assert plan.schedule == "sv" and plan.info()["n_items"] == 2 * 5 * 5
     iters, sigma = 25, 1e-4
-    cfg = mb.MaceConfig(n_subsets=2, rho=0.8, sigma=sigma, max_outer=iters, tol=1e-300, residuals="none")
+    cfg = mb.MaceConfig(n_subsets=2, rho=0.8, sigma=sigma, max_outer=iters, tol=1e-300, residuals="none",
+                        schedule="raster")
     res = _fixed(mb.mace_solve, prob, cfg)
     agents = O.build_agents(mats, y, lam, 2, sigma, O.Prior("qggmrf", 50.0, 2.0, 1.2, 1.0, 0.01), ns)
     run = O.mace_run(agents, iters, 0.8)

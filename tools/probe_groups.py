@@ -19,12 +19,13 @@ ap.add_argument("--config", type=int, default=1)
 ap.add_argument("--groups", default="0,1,2,4,8")
 ap.add_argument("--iters", type=int, default=40)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--sv", type=int, default=8)
 a = ap.parse_args()
 c = gen.CONFIGS[a.config]
 geom, mats, phantom, y, lam = gen.make_scan(a.config)
 N = c["n_agents"]
 prior = mb.PriorParams("qggmrf", beta=c["beta"], p=2.0, q=1.2, T=1.0, sigma_x=0.01)
-plan = plan_for(mats, [s.view_indices for s in mb.partition_views(geom.n_views, N)], schedule="sv", sv=8)
+plan = plan_for(mats, [s.view_indices for s in mb.partition_views(geom.n_views, N)], schedule="sv", sv=a.sv)
 plan.load_data(y, lam)
 plan.set_prior(prior)
 plan.set_agent_params(-1, prior.beta / N, 1.0 / c["sigma"] ** 2, False)
@@ -37,5 +38,5 @@ for rep in range(a.reps):
         plan.k2_timing(True)
         ms = plan.iterate(a.iters, 0, 0.8, False, 1e-300, N, False)
         k2, nl = plan.k2_timing(False)
-        print(f"config {a.config} rep {rep} group {g:2d}: K2 {k2 / nl:.4f} ms/launch, loop {ms / a.iters:.4f} ms/iter",
+        print(f"config {a.config} sv {a.sv} rep {rep} group {g:2d}: K2 {k2 / nl:.4f} ms/launch, loop {ms / a.iters:.4f} ms/iter",
               flush=True)
