@@ -375,8 +375,11 @@ __device__ __forceinline__ void sv_load_recs(const uint32_t* __restrict__ rb, in
     }
 }
 
+#ifndef MACE_CONSTS_MINB
+#define MACE_CONSTS_MINB 4  // resident blocks per SM the register budget (K = 2) is sized for
+#endif
 template <int K, int NG, bool kW>
-__global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n_items, const uint32_t* queue,
+__global__ void __launch_bounds__(128, K == 2 ? MACE_CONSTS_MINB : 1) k_sv_consts(const AgentDev* agents, int n_items, const uint32_t* queue,
                                                    int n_side, int S, int nb, int W, int CH)
 {
     extern __shared__ float s_lam[];  // [CH * NG][W][32]
@@ -407,7 +410,10 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
         const int2 bj = j < A.V ? bt[j] : make_int2(0, 0);
         float* sl = s_lam + (size_t)g * W * 32 + lane;
 #pragma unroll 8
-        for (int o = 0; o < W; ++o) sl[o * 32] = o < bj.y ? A.lam[bj.x + o] : 0.f;
+        // weighted records: the window holds sqrt(lambda) (k_gather_data's A.sq), so a record is
+        // weighted by one multiply instead of an IEEE sqrtf per entry
+        const float* src = kW ? A.sq : A.lam;
+        for (int o = 0; o < W; ++o) sl[o * 32] = o < bj.y ? src[bj.x + o] : 0.f;
     }
     __syncthreads();
     if (!kW) {  // the band's lambda rows, laid out as the K2 shared-memory plane
@@ -440,7 +446,7 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
                 for (int g = 0; g < NG; ++g) {
 #pragma unroll
                     for (int q = 0; q < K; ++q) {
-                        a[p][g][q] *= sqrtf(l[p][g][q]);
+                        a[p][g][q] *= l[p][g][q];  // l = sqrt(lambda) here
                         l[p][g][q] = 1.f;
                     }
                     uint32_t* wq = w + (g * 32 + lane) * K;
@@ -469,23 +475,42 @@ __global__ void __launch_bounds__(128) k_sv_consts(const AgentDev* agents, int n
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = i + 1; j < 4; ++j, ++x)
+                for (int j = i + 1; j < 4; ++j, ++x) {
+                    if constexpr (K == 2) {  // rows shared when |o_j - o_i| <= 1: selects, no branches
+                        const int d = o[j] - o[i];
+                        const float s0 = a[i][g][0] * l[i][g][0], s1 = a[i][g][1] * l[i][g][1];
+                        const float t = d == 0 ? fmaf(s0, a[j][g][0], s1 * a[j][g][1])
+                                               : d == 1 ? s1 * a[j][g][0] : d == -1 ? s0 * a[j][g][1] : 0.f;
+                        cx[x] += t;
+                    } else {
 #pragma unroll
-                    for (int q = 0; q < K; ++q)
+                        for (int q = 0; q < K; ++q)
 #pragma unroll
-                        for (int qj = 0; qj < K; ++qj)  // row o_i + q of pixel i is row o_j + qj of pixel j
-                            if (o[i] + q == o[j] + qj) cx[x] = fmaf(a[i][g][q] * a[j][g][qj], l[i][g][q], cx[x]);
+                            for (int qj = 0; qj < K; ++qj)  // row o_i + q of pixel i is row o_j + qj of pixel j
+                                if (o[i] + q == o[j] + qj) cx[x] = fmaf(a[i][g][q] * a[j][g][qj], l[i][g][q], cx[x]);
+                    }
+                }
         }
         if (ch == CH - 1) {  // the batch's sums over every chunk's views
+            // the ten sums at once by a halving butterfly: at the xor-m stage a lane keeps the half of
+            // its values selected by its lane bit m and adds the partner's copy of that half; after
+            // the xor-2 stage value k sits on lanes 2k and 2k + 1 (16 shuffles instead of 50)
+            float r16[16];
 #pragma unroll
-            for (int p = 0; p < 4; ++p) t2[p] = warp_sum(t2[p]);
+            for (int k = 0; k < 16; ++k) r16[k] = k < 4 ? t2[k] : (k < 10 ? cx[k - 4] : 0.f);
 #pragma unroll
-            for (int x = 0; x < 6; ++x) cx[x] = warp_sum(cx[x]);
-            float v = 0.f;
+            for (int m = 16, h = 8; m >= 2; m >>= 1, h >>= 1) {
+                const bool up = lane & m;
 #pragma unroll
-            for (int k = 0; k < 10; ++k)
-                if (lane == k) v = k < 4 ? t2[k & 3] : cx[(k - 4) % 6];
-            if (lane < 16) A.bc[((size_t)sv * nb + b) * 16 + lane] = v;
+                for (int k = 0; k < h; ++k) {
+                    const float send = up ? r16[k] : r16[k + h];
+                    const float keep = up ? r16[k + h] : r16[k];
+                    r16[k] = keep + __shfl_xor_sync(FULL, send, m);
+                }
+            }
+            float v = r16[0] + __shfl_xor_sync(FULL, r16[0], 1);  // value lane >> 1
+            v = __shfl_sync(FULL, v, 2 * (lane & 15));             // lane k (< 16) takes value k
+            if (lane < 16) A.bc[((size_t)sv * nb + b) * 16 + lane] = lane < 10 ? v : 0.f;
             if (lane < 4) {  // theta2 image (cost kernels, diagnostics)
                 const int i = (b % bpc) * 4 + lane, cls = b / bpc;
                 if (i < per_class) {

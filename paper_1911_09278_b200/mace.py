@@ -272,14 +272,38 @@ class _Comm:
             for t in tensors:
                 self.dist.all_reduce(t, group=self.group)
 
-    def allgather_stack(self, local_rows: dict, N: int, n: int) -> np.ndarray:
-        objs = [None] * self.world
-        self.dist.all_gather_object(objs, local_rows, group=self.group)
-        out = np.zeros((N, n))
-        for d in objs:
-            for i, row in d.items():
-                out[i] = row
+    def allgather_stack(self, w_loc: np.ndarray, N: int, n: int, device=None) -> np.ndarray:
+        """The full (N, n) stack on every rank from each rank's agents {i : i mod world == rank}
+        (float32 rows): one tensor all-gather (NCCL over NVLink when `device` is a GPU) of the
+        [ceil(N / world), n] padded local blocks, then agent i = row (i // world) of rank i % world."""
+        import torch
+
+        per = -(-N // self.world)
+        dev = torch.device("cpu") if device is None else device
+        src = torch.from_numpy(np.ascontiguousarray(w_loc))
+        blk = torch.zeros((per, n), dtype=src.dtype, device=dev)
+        if len(w_loc):
+            blk[: len(w_loc)] = src.to(dev)
+        parts = [torch.empty_like(blk) for _ in range(self.world)]
+        self.dist.all_gather(parts, blk, group=self.group)
+        allp = torch.stack(parts).cpu().numpy()  # [world, per, n]
+        out = np.empty((N, n), allp.dtype)
+        for i in range(N):
+            out[i] = allp[i % self.world, i // self.world]
         return out
+
+
+def _comm_device(comm):
+    """the torch device a collective of this process group runs on (its NCCL device, or the CPU
+    for gloo)"""
+    try:
+        if comm.dist.get_backend(comm.group) == "nccl":
+            import torch
+
+            return torch.device("cuda", torch.cuda.current_device())
+    except Exception:
+        pass
+    return None
 
 
 def _f64(a: np.ndarray) -> np.ndarray:
@@ -494,11 +518,11 @@ def _run_outer(problem, config: MaceConfig, pool, ref_image, w0, denoiser, comm=
     converged = done[0] == 1
     _fill_log(log, rows, counter, N, n)
     image = _f64(_pinned_get(plan, "get_image", 1 if pnp else 0))
-    w_loc = _f64(_pinned_get(plan, "get_stack").reshape(len(local), n))
     if comm is None:
-        stack = w_loc
+        stack = _f64(_pinned_get(plan, "get_stack").reshape(len(local), n))
     else:
-        stack = comm.allgather_stack({i: w_loc[j] for j, i in enumerate(local)}, N, n)
+        w_loc = np.array(_pinned_get(plan, "get_stack").reshape(len(local), n))  # a copy of the pinned view
+        stack = _f64(comm.allgather_stack(w_loc, N, n, device=_comm_device(comm)))
     result = MaceResult(image=image, stack=stack, log=log, iterations=iterations, converged=converged,
                         equits=None if counter is None else counter.equits(), device_ms=device_ms)
     if config.residuals == "final":

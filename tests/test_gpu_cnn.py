@@ -205,6 +205,7 @@ def test_cnn_launch_variants_are_bit_identical(n_side, monkeypatch):
     x = rng.random(n_side * n_side)
     w = cnn_weights(31, scale=1.0)
     outs = {}
+    monkeypatch.setenv("MACE_K5_ROWS", "2")  # the persistent kernel runs row pairs
     for seq in ("0", "1"):
         for last in ("tc", "fma"):
             monkeypatch.setenv("MACE_K5_SEQ", seq)
@@ -214,3 +215,12 @@ def test_cnn_launch_variants_are_bit_identical(n_side, monkeypatch):
     assert np.array_equal(outs[("1", "fma")], outs[("0", "fma")])
     r_tc, r_fma = _net(x, outs[("0", "tc")]), _net(x, outs[("0", "fma")])
     assert rel(r_tc, r_fma) < 1e-5
+    # row units per MMA batch (MACE_K5_ROWS): each output row receives the same UMMAs in another
+    # order (fp32 accumulation), so single rows, pairs and triples agree to bf16 rounding
+    monkeypatch.setenv("MACE_K5_SEQ", "0")
+    monkeypatch.setenv("MACE_K5_LAST", "tc")
+    units = {}
+    for r in ("1", "2", "3"):
+        monkeypatch.setenv("MACE_K5_ROWS", r)
+        units[r] = _net(x, CnnDenoiser(n_side, weights=w)(x))
+    assert rel(units["2"], units["3"]) < 1e-3 and rel(units["1"], units["3"]) < 1e-3
