@@ -34,12 +34,82 @@ def _identity(v):
     return np.array(v, dtype=np.float64)
 
 
+_DENSE_LIMIT = 4096  # pixels up to which the quadratic prox is a dense Cholesky solve (denoisers.py:23)
+
+
+def _laplacian(n_side: int):
+    """Weighted 8-neighbourhood graph Laplacian L = D - W (models.py:169-176: x^T L x =
+    sum over pairs of w (x_s - x_r)^2), assembled from neighbor_table (each pair seen from both
+    ends, so D is the row sum of W)."""
+    import scipy.sparse as sp
+
+    from .models import neighbor_table
+
+    nbr, w = neighbor_table(n_side)
+    n = n_side * n_side
+    s = np.repeat(np.arange(n), nbr.shape[1])
+    r, ww = nbr.ravel(), w.ravel()
+    ok = r >= 0
+    W = sp.csr_matrix((ww[ok], (s[ok], r[ok])), shape=(n, n))
+    return (sp.diags(np.asarray(W.sum(axis=1)).ravel()) - W).tocsr()
+
+
+class QuadraticProx:
+    """H(v) = argmin_z lam/2 z^T L z + 1/2 ||z - v||^2, i.e. (I + lam L) z = v (denoisers.py:43-65):
+    a dense Cholesky factor up to _DENSE_LIMIT pixels, conjugate gradients (rtol 1e-10) above.
+    A host callable, applied once per PnP iteration as the reference applies it."""
+
+    def __init__(self, lam: float, n_side: int):
+        import scipy.linalg as sla
+        import scipy.sparse as sp
+
+        self.n = n_side * n_side
+        self._op = (sp.identity(self.n, format="csr") + lam * _laplacian(n_side)).tocsr()
+        self._cho = sla.cho_factor(self._op.toarray()) if self.n <= _DENSE_LIMIT else None
+
+    def __call__(self, v):
+        import scipy.linalg as sla
+        import scipy.sparse.linalg as spla
+
+        v = np.asarray(v, dtype=np.float64)
+        if self._cho is not None:
+            return sla.cho_solve(self._cho, v)
+        z, info = spla.cg(self._op, v, rtol=1e-10, atol=0.0, maxiter=10 * self.n)
+        if info != 0:
+            raise RuntimeError(f"quadratic-prox CG failed to converge (info={info})")
+        return z
+
+
+class Boxcar:
+    """Mean over the (2 radius + 1)^2 window, renormalised by the in-image count at the borders
+    (denoisers.py:68-89), from a summed-area table."""
+
+    def __init__(self, radius: int, n_side: int):
+        self.radius, self.n_side = int(radius), int(n_side)
+
+    def __call__(self, v):
+        m, r = self.n_side, self.radius
+        sat = np.zeros((m + 1, m + 1))
+        sat[1:, 1:] = np.asarray(v, dtype=np.float64).reshape(m, m).cumsum(0).cumsum(1)
+        i = np.arange(m)
+        lo, hi = np.maximum(i - r, 0), np.minimum(i + r + 1, m)
+        box = sat[np.ix_(hi, hi)] - sat[np.ix_(lo, hi)] - sat[np.ix_(hi, lo)] + sat[np.ix_(lo, lo)]
+        return (box / np.outer(hi - lo, hi - lo)).ravel()
+
+
+_BUILT = {}
+
+
 def make_denoiser(spec: DenoiserSpec, n_side: int):
+    """The reference's built-in denoisers (denoisers.py:92-106), cached per (spec, n_side)."""
     if spec.kind == "identity":
         return _identity
-    raise NotImplementedError(
-        f"built-in denoiser {spec.kind!r} is outside the B200 hot path; pass it as a callable "
-        "(mace_pnp_solve(..., denoiser=H)) or use the CNN denoiser")
+    key = (spec, int(n_side))
+    if key not in _BUILT:
+        if len(_BUILT) >= 32:
+            _BUILT.clear()
+        _BUILT[key] = QuadraticProx(spec.lam, n_side) if spec.kind == "quadratic-prox" else Boxcar(spec.radius, n_side)
+    return _BUILT[key]
 
 
 def denoise(spec: DenoiserSpec, v, n_side: int):

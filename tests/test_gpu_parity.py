@@ -350,3 +350,25 @@ def test_raster_schedule_is_bitwise_deterministic(golden):
     a, b = _fixed(mb.mace_solve, prob, cfg), _fixed(mb.mace_solve, prob, cfg)
     assert np.array_equal(a.image, b.image) and np.array_equal(a.stack, b.stack)
     assert [r["relnorm"] for r in a.log.rows] == [r["relnorm"] for r in b.log.rows]
+
+
+@pytest.mark.parametrize("n", [1, 4])
+def test_mace_pnp_builtin_quadratic_prox_matches_reference(n):
+    """MACE-PnP with the reference's built-in quadratic-prox denoiser (DenoiserSpec, applied on the
+    host once per iteration as the reference does) at one and four agents lands on the reference's
+    own fixed points (tests/golden/golden_denoisers.npz, made by make_denoisers.py; the reference's
+    test_mace.py:298-306 asserts they coincide)."""
+    import os
+
+    from conftest import GOLDEN
+
+    dg = np.load(os.path.join(GOLDEN, "golden_denoisers.npz"))
+    prob = mb_problem(31, 8, 16, 11, "qggmrf", 1.0, 0.5)
+    assert np.array_equal(prob.y, dg["pnp_y"])
+    cfg = mb.MaceConfig(n_subsets=n, rho=0.8, sigma=0.1, mode="pnp",
+                        denoiser=mb.DenoiserSpec(kind="quadratic-prox", lam=2.0), tol=1e-9, max_outer=8000,
+                        residuals="none", schedule="raster")
+    res = mb.mace_pnp_solve(prob, cfg)
+    assert res.converged
+    for k in (1, 4):
+        assert rel(res.image, dg[f"pnp_image_n{k}"]) < 1e-5
