@@ -51,3 +51,13 @@ def test_gpus_n_spawns_n_ranks(gpus):
     assert sorted(i for a in owners.values() for i in a) == [0, 1, 2, 3]
     if gpus == 2:
         assert owners[0] == [0, 2] and owners[1] == [1, 3]
+
+
+def test_multirank_time_to_rmse_path():
+    """--gpus 2 with a time-to-RMSE budget: the per-iteration NRMSE of the global consensus image
+    from a fresh two-rank solve, the first iteration after which it stays <= 1e-3."""
+    lines = _run("--gpus", "2", "--cpu-test", "--steps", "1", "--warmup", "1", "--ttr-iters", "300")
+    d = json.loads(lines[0])
+    t = d["time_to_rmse_1e-3"]
+    assert t["ran_iterations"] == 300 and isinstance(t["iterations"], int) and 1 < t["iterations"] < 300
+    assert t["final_nrmse"] <= 1e-3 and t["seconds"] > 0
