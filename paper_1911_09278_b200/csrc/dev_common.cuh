@@ -6,6 +6,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// slot-record block layout (internal.h sv_len_word): 1 = lane-major (default), 0 = slot-major
+#ifndef MACE_SV_LANE_MAJOR
+#define MACE_SV_LANE_MAJOR 1
+#endif
+
 namespace mace {
 
 constexpr unsigned FULL = 0xffffffffu;

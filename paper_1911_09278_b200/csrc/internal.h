@@ -69,11 +69,30 @@ struct SVLayout {
     int nb = 0;                  // batches per tile
     int rec = 0;                 // words per pixel slot: ng*32*K lengths ([g][lane][k]) + 32 offset words
     std::vector<int2_t> band;    // [n_sv * views] {local row start, cnt}
-    std::vector<uint32_t> data;  // [n_sv][nb][chunks][kSvBatch][rec] (lengths as float bits; empty slots 0)
+    std::vector<uint32_t> data;  // [n_sv][nb][chunks] blocks of kSvBatch x rec words (sv_len_word / sv_ofs_word; empty slots 0)
     int max_col = 0;             // max entries per column (info)
     int64_t entries = 0;         // stored nonzeros (== nnz of the agent)
     int64_t duplicates = 0;      // repeated (row, pixel) pairs merged (never seen in practice)
 };
+// Records of one (tile, batch, chunk) are one block of kSvBatch x rec words, lane-major so that a
+// lane's lengths for a view group are contiguous (one 256-bit load per group for K = 2):
+//   lengths  [g][lane][slot][k]  at ((g * 32 + lane) * kSvBatch + slot) * K + k
+//   offsets  [lane][slot]        at ng * 32 * kSvBatch * K + lane * kSvBatch + slot  (one byte per group)
+// (MACE_SV_LANE_MAJOR 0: slot-major blocks, lengths [slot][g][lane][k] and offsets [slot][lane] --
+// the round-1 layout, kept for A/B)
+#ifndef MACE_SV_LANE_MAJOR
+#define MACE_SV_LANE_MAJOR 1
+#endif
+inline size_t sv_len_word(int ng, int K, int g, int lane, int slot, int k)
+{
+    if (!MACE_SV_LANE_MAJOR) return (size_t)slot * ((size_t)ng * 32 * K + 32) + ((size_t)g * 32 + lane) * K + k;
+    return (((size_t)g * 32 + lane) * kSvBatch + slot) * K + k;
+}
+inline size_t sv_ofs_word(int ng, int K, int lane, int slot)
+{
+    if (!MACE_SV_LANE_MAJOR) return (size_t)slot * ((size_t)ng * 32 * K + 32) + (size_t)ng * 32 * K + lane;
+    return (size_t)ng * 32 * kSvBatch * K + (size_t)lane * kSvBatch + slot;
+}
 // Visit-order slot t of an S x S tile -> local pixel (lr * S + lc), or -1 for a padding slot.
 inline int sv_slot_pixel(int S, int t)
 {

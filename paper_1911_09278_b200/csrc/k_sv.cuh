@@ -22,7 +22,8 @@
 //    c_ip = sum a_i a_p lambda (k_sv_consts): after pixel i moves by alpha_i, theta1_p changes by
 //    -alpha_i c_ip.  The four 1-D solves of a batch are a short scalar recurrence after one warp
 //    reduction, instead of four dependent reductions.
-//  * Slot records (lengths [g][lane][k] + one offset byte per view group) and batch constants
+//  * Slot records (per batch one lane-major block: lengths [g][lane][slot][k], offsets [lane][slot]
+//    with one byte per view group; internal.h) and batch constants
 //    are coalesced register loads, one batch ahead; the band windows are staged with cp.async.
 //  * Epilogue: the band's net change e - e0 is folded into global e with red.add (tiles of the
 //    same agent that share rows run concurrently), then z, the Mann step and norm partials.
@@ -115,28 +116,45 @@ __constant__ typename SvOrder<S>::Table c_svorder = SvOrder<S>::make();
 template <int K, int NG>
 __device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __restrict__ r, int lane)
 {
+#if !MACE_SV_LANE_MAJOR  // slot-major blocks: per (slot, group) one 8- or 16-byte load, per slot one offset word
     constexpr int RECW = sv_rec_words(NG, K);
-    r += lane * K;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
-            const uint32_t* q = r + p * RECW + g * 32 * K;
+            const uint32_t* q = r + p * RECW + (g * 32 + lane) * K;
             if constexpr (K == 2) {
-                asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];"
-                    : "=f"(B.a[p][g][0]), "=f"(B.a[p][g][1])
-                    : "l"(q));
+                asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(B.a[p][g][0]), "=f"(B.a[p][g][1]) : "l"(q));
             } else {
                 asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
                     : "=f"(B.a[p][g][0]), "=f"(B.a[p][g][1]), "=f"(B.a[p][g][2]), "=f"(B.a[p][g][3])
                     : "l"(q));
             }
         }
+        asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(B.ob[p]) : "l"(r + p * RECW + NG * 32 * K + lane));
     }
-    r += lane - lane * K;
+    return;
+#endif
+    // one (batch, chunk) block of records, lane-major (internal.h sv_len_word / sv_ofs_word): the
+    // lane's 4 K lengths of a view group are contiguous (one 256-bit load for K = 2, two for K = 4)
+    // and its four offset words one 128-bit load
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
-        asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(B.ob[p]) : "l"(r + p * RECW + NG * 32 * K));
+    for (int g = 0; g < NG; ++g) {
+        const uint32_t* q = r + ((size_t)g * 32 + lane) * 4 * K;
+#pragma unroll
+        for (int h = 0; h < K / 2; ++h) {  // elements 8h .. 8h + 7 of the lane's [slot][k] run
+            float r8[8];
+            asm("ld.global.nc.L1::no_allocate.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                : "=f"(r8[0]), "=f"(r8[1]), "=f"(r8[2]), "=f"(r8[3]), "=f"(r8[4]), "=f"(r8[5]), "=f"(r8[6]),
+                  "=f"(r8[7])
+                : "l"(q + 8 * h));
+#pragma unroll
+            for (int i = 0; i < 8; ++i) B.a[(8 * h + i) / K][g][i % K] = r8[i];
+        }
+    }
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+        : "=r"(B.ob[0]), "=r"(B.ob[1]), "=r"(B.ob[2]), "=r"(B.ob[3])
+        : "l"(r + (size_t)NG * 32 * 4 * K + 4 * lane));
 }
 
 #ifndef MACE_K2_PF
@@ -162,6 +180,9 @@ __device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __
 // per-batch tests of the prior kind and the clamp), the zt store index computed by the storing lane
 // only, the L2 prefetch pointer advanced per batch, and band addresses by one byte permute
 #define MACE_K2_TRIM 1
+#endif
+#ifndef MACE_K2_V8
+#define MACE_K2_V8 1  // 256-bit e-window loads
 #endif
 #ifndef MACE_K2_MINB
 #define MACE_K2_MINB 12  // resident warps per SM the register budget is sized for
@@ -220,7 +241,10 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
     // current tile
     // float4 loads per group: a window of a parallel-beam tile spans about S sqrt 2 + 2 channels at
     // channel pitch = pixel pitch, plus up to 3 rows of alignment; wider windows take the slow path
-    constexpr int EV = (S * 1414 / 1000 + 8) / 4;
+    // VW floats per window load: 8 = one 256-bit load per lane (LDG.256, 32-byte aligned spans: each
+    // instruction still touches 32 lines, one per lane's view, so fewer loads = fewer L1 wavefronts)
+    constexpr int VW = MACE_K2_V8 ? 8 : 4;
+    constexpr int EV = MACE_K2_V8 ? (S * 1414 / 1000 + 16) / 8 : (S * 1414 / 1000 + 8) / 4;
     auto fetch_item = [&]() {
         unsigned it = 0;
         if (lane == 0) it = atomicAdd(P.head, 1u);
@@ -260,16 +284,35 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
 #endif
     // e windows: 16-byte loads over the aligned span of each window (a lane's window is one
     // contiguous run of rows; the loads of one instruction hit 32 different lines)
-    auto ewin_of = [&](uint32_t cd, const int2 (&mb)[NG], float4 (&ev4)[NG][EV], int (&shf)[NG]) {
+    auto ewin_of = [&](uint32_t cd, const int2 (&mb)[NG], float (&ev)[NG][EV * VW], int (&shf)[NG]) {
         const float* en = P.agents[cd >> kAgentShift].e;
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
             const int st = mb[g].x, cnt = mb[g].y;
-            shf[g] = st & 3;
-            const float4* ep = reinterpret_cast<const float4*>(en + (st - shf[g]));
-            const int nv = (cnt + shf[g] + 3) >> 2;
+            shf[g] = st & (VW - 1);
+            const float* ep = en + (st - shf[g]);
+            const int nv = (cnt + shf[g] + VW - 1) / VW;
 #pragma unroll
-            for (int v = 0; v < EV; ++v) ev4[g][v] = v < nv ? __ldcg(ep + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int v = 0; v < EV; ++v) {
+                float* r = ev[g] + VW * v;
+                if constexpr (VW == 8) {
+                    if (v < nv) {
+                        asm volatile("ld.global.cg.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                                       "=f"(r[6]), "=f"(r[7])
+                                     : "l"(ep + 8 * v));
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) r[i] = 0.f;
+                    }
+                } else {
+                    const float4 q = v < nv ? __ldcg(reinterpret_cast<const float4*>(ep) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    r[0] = q.x;
+                    r[1] = q.y;
+                    r[2] = q.z;
+                    r[3] = q.w;
+                }
+            }
         }
     };
     // tile state (z with its halo, w, and v = 2 G(w) - w or the explicit target), one tile ahead:
@@ -315,7 +358,7 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
     band_of(code, myb);
     issue_windows(code, myb);
 #else
-    float4 ew[NG][EV];
+    float ew[NG][EV * VW];
     int sh[NG];
     float zpre[ZN], wpre[VN], vpre[VN];
     band_of(code, myb);
@@ -444,15 +487,13 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
         for (int g = 0; g < NG; ++g) {
             const int cnt = myb[g].y;
             float* d = sb + g * W * U + lane;
-            if (W <= 4 * EV - 3) {
+            if (W <= VW * EV - (VW - 1)) {
 #pragma unroll
-                for (int v = 0; v < EV; ++v) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int o = 4 * v + i - sh[g];
+                for (int v = 0; v < EV * VW; ++v) {
+                    {
+                        const int o = v - sh[g];
                         if (o >= 0 && o < W) {
-                            const float xi = i == 0 ? ew[g][v].x : i == 1 ? ew[g][v].y : i == 2 ? ew[g][v].z : ew[g][v].w;
-                            const float x = o < cnt ? xi : 0.f;
+                            const float x = o < cnt ? ew[g][v] : 0.f;
                             d[o * U] = x;
                             d[o * U + E0] = x;
                         }

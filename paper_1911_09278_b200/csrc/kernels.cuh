@@ -349,30 +349,37 @@ template <int K, int NG>
 __device__ __forceinline__ void sv_load_recs(const uint32_t* __restrict__ rb, int lane, float (&a)[4][NG][K],
                                              uint32_t (&ow)[4])
 {
+    // one (batch, chunk) block, lane-major (internal.h sv_len_word / sv_ofs_word): per group the
+    // lane's 4 K lengths are contiguous, its four offset words too (streaming loads)
+#if !MACE_SV_LANE_MAJOR
     constexpr int recw = NG * 32 * K + 32;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         const uint32_t* r = rb + (size_t)p * recw;
         ow[p] = __ldcs(r + NG * 32 * K + lane);
 #pragma unroll
-        for (int g = 0; g < NG; ++g) {  // the lane's K lengths are adjacent: one vector load
-            const uint32_t* rq = r + (g * 32 + lane) * K;
-            if constexpr (K == 2) {
-                const uint2 v = __ldcs(reinterpret_cast<const uint2*>(rq));
-                a[p][g][0] = __uint_as_float(v.x);
-                a[p][g][1] = __uint_as_float(v.y);
-            } else if constexpr (K == 4) {
-                const uint4 v = __ldcs(reinterpret_cast<const uint4*>(rq));
-                a[p][g][0] = __uint_as_float(v.x);
-                a[p][g][1] = __uint_as_float(v.y);
-                a[p][g][2] = __uint_as_float(v.z);
-                a[p][g][3] = __uint_as_float(v.w);
-            } else {
+        for (int g = 0; g < NG; ++g)
 #pragma unroll
-                for (int q = 0; q < K; ++q) a[p][g][q] = __uint_as_float(__ldcs(rq + q));
-            }
+            for (int q = 0; q < K; ++q) a[p][g][q] = __uint_as_float(__ldcs(r + (g * 32 + lane) * K + q));
+    }
+    return;
+#endif
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        const uint4* q = reinterpret_cast<const uint4*>(rb + ((size_t)g * 32 + lane) * 4 * K);
+#pragma unroll
+        for (int h = 0; h < K; ++h) {  // 4 words per load: elements 4h .. 4h + 3 of [slot][k]
+            const uint4 v = __ldcs(q + h);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[(4 * h + i) / K][g][(4 * h + i) % K] = __uint_as_float(w[i]);
         }
     }
+    const uint4 o = __ldcs(reinterpret_cast<const uint4*>(rb + (size_t)NG * 32 * 4 * K) + lane);
+    ow[0] = o.x;
+    ow[1] = o.y;
+    ow[2] = o.z;
+    ow[3] = o.w;
 }
 
 #ifndef MACE_CONSTS_MINB
@@ -392,11 +399,11 @@ __global__ void __launch_bounds__(128, K == 2 ? MACE_CONSTS_MINB : 1) k_sv_const
     const AgentDev& A = agents[code >> kAgentShift];
     const int sv = (int)(code & kSvMask);
     const int r0 = (sv / A.n_sv_side) * S, c0 = (sv % A.n_sv_side) * S;
-    // records [sv][batch][chunk][slot][recw]; this warp takes batches b = warp + 4 k, and for each
+    // records: (batch, chunk) blocks of 4 recw words (internal.h); this warp takes batches b = warp + 4 k, and for each
     // the CH chunks (units u = k CH + c), the next unit's records in flight
     const uint32_t* __restrict__ rbase = A.rec0 + (size_t)sv * nb * CH * 4 * recw;
     uint32_t* __restrict__ wbase = kW ? A.recw + (size_t)sv * nb * CH * 4 * recw : nullptr;
-    auto unit_ofs = [&](int u) { return ((size_t)(warp + 4 * (u / CH)) * CH + u % CH) * 4 * recw; };
+    auto unit_ofs = [&](int u) { return ((size_t)(warp + 4 * (u / CH)) * CH + u % CH) * 4 * recw; };  // (batch, chunk) block
     const int nu = (warp < nb ? (nb - warp + 3) / 4 : 0) * CH;
 
     // first unit's records in flight while the window is staged
@@ -439,28 +446,40 @@ __global__ void __launch_bounds__(128, K == 2 ? MACE_CONSTS_MINB : 1) k_sv_const
         if (kW) {  // weighted record a sqrt(lambda): theta2 and the cross terms are its plain products
             uint32_t* wb = wbase + unit_ofs(u);
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                uint32_t* w = wb + (size_t)p * recw;
-                __stcs(w + NG * 32 * K + lane, ow[p]);
+            for (int p = 0; p < 4; ++p)
 #pragma unroll
-                for (int g = 0; g < NG; ++g) {
+                for (int g = 0; g < NG; ++g)
 #pragma unroll
                     for (int q = 0; q < K; ++q) {
                         a[p][g][q] *= l[p][g][q];  // l = sqrt(lambda) here
                         l[p][g][q] = 1.f;
                     }
-                    uint32_t* wq = w + (g * 32 + lane) * K;
-                    if constexpr (K == 2) {
-                        __stcs(reinterpret_cast<uint2*>(wq), make_uint2(__float_as_uint(a[p][g][0]), __float_as_uint(a[p][g][1])));
-                    } else if constexpr (K == 4) {
-                        __stcs(reinterpret_cast<uint4*>(wq), make_uint4(__float_as_uint(a[p][g][0]), __float_as_uint(a[p][g][1]),
-                                                                        __float_as_uint(a[p][g][2]), __float_as_uint(a[p][g][3])));
-                    } else {
+#if !MACE_SV_LANE_MAJOR
 #pragma unroll
-                        for (int q = 0; q < K; ++q) __stcs(wq + q, __float_as_uint(a[p][g][q]));
-                    }
+            for (int p = 0; p < 4; ++p) {
+                uint32_t* w = wb + (size_t)p * recw;
+                __stcs(w + NG * 32 * K + lane, ow[p]);
+#pragma unroll
+                for (int g = 0; g < NG; ++g)
+#pragma unroll
+                    for (int q = 0; q < K; ++q) __stcs(w + (g * 32 + lane) * K + q, __float_as_uint(a[p][g][q]));
+            }
+            if (false)
+#endif
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {  // the same lane-major block: 4 K words per (group, lane)
+                uint4* q = reinterpret_cast<uint4*>(wb + ((size_t)g * 32 + lane) * 4 * K);
+#pragma unroll
+                for (int h = 0; h < K; ++h) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) w[i] = __float_as_uint(a[(4 * h + i) / K][g][(4 * h + i) % K]);
+                    __stcs(q + h, make_uint4(w[0], w[1], w[2], w[3]));
                 }
             }
+            if (MACE_SV_LANE_MAJOR)
+                __stcs(reinterpret_cast<uint4*>(wb + (size_t)NG * 32 * 4 * K) + lane,
+                       make_uint4(ow[0], ow[1], ow[2], ow[3]));
         }
 #pragma unroll
         for (int g = 0; g < NG; ++g) {

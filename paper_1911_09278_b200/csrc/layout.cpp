@@ -149,8 +149,9 @@ void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SV
             const int r = r0 + k / S, c = c0 + k % S;
             if (r >= n_side || c >= n_side) continue;
             const int64_t s = (int64_t)r * n_side + c;
-            // chunk h of slot t: records [sv][batch][chunk][slot][rec]
-            uint32_t* rec0 = &out.data[(size_t)sv * per_tile + ((size_t)(t / kSvBatch) * CH * kSvBatch + t % kSvBatch) * out.rec];
+            // (batch, chunk) blocks of kSvBatch x rec words, lane-major inside (internal.h)
+            const int slot = t % kSvBatch;
+            uint32_t* blk0 = &out.data[(size_t)sv * per_tile + (size_t)(t / kSvBatch) * CH * kSvBatch * out.rec];
             // entries of one (pixel, view) are consecutive in the column (rows ascending); the slot
             // offset is pulled back so that all K addressed rows stay inside the window (rows past
             // cnt would alias the lane's next window or memory after the band)
@@ -160,12 +161,10 @@ void build_sv_layout(const AgentCSC& csc, int n_side, int n_ch, int V, int S, SV
                 if (cur_j < 0) return;
                 const int gt = cur_j >> 5, l = cur_j & 31, cnt = bt[cur_j].y;
                 const int g = gt % G;  // group inside the view's chunk gt / G
-                uint32_t* rec = rec0 + (size_t)(gt / G) * kSvBatch * out.rec;
-                float* pv = reinterpret_cast<float*>(rec);
-                uint32_t* po = rec + G * 32 * KK;
+                uint32_t* blk = blk0 + (size_t)(gt / G) * kSvBatch * out.rec;
                 const int o = std::min(o0, std::max(cnt, KK) - KK);
-                po[l] |= (uint32_t)o << (8 * g);
-                for (int u = 0; u < m; ++u) pv[((size_t)g * 32 + l) * KK + (o0 - o) + u] = vals[u];
+                blk[sv_ofs_word(G, KK, l, slot)] |= (uint32_t)o << (8 * g);
+                for (int u = 0; u < m; ++u) std::memcpy(&blk[sv_len_word(G, KK, g, l, slot, (o0 - o) + u)], &vals[u], 4);
                 out.entries += m;
             };
             uint32_t prev = UINT32_MAX;

@@ -720,8 +720,8 @@ int mace_setup_agents(void* p, int n_agents, const int* view_counts, const int* 
     }
     // per local (virtual) agent: data arrays; each {e, lambda} block starts on a 16-byte boundary
     std::vector<int> rb(n_local + 1, 0);
-    // (K2 reads e windows as aligned float4 spans, which may run up to 3 rows past R)
-    for (int va = 0; va < n_local; ++va) rb[va + 1] = rb[va] + ((c->am[va % n_agents]->R + 3) & ~3);
+    // (K2 reads e windows as 32-byte aligned spans, which may run up to 7 rows past R)
+    for (int va = 0; va < n_local; ++va) rb[va + 1] = rb[va] + ((c->am[va % n_agents]->R + 7) & ~7);
     c->total_rows = rb[n_local];
     c->row_base.alloc(n_local + 1);
     CK(cudaMemcpy(c->row_base.p, rb.data(), sizeof(int) * (n_local + 1), cudaMemcpyHostToDevice));
@@ -1720,22 +1720,24 @@ int mace_sv_layout_probe(int n_side, int n_ch, int n_views, const int64_t* row_p
     SVLayout L;
     build_sv_layout(csc, n_side, n_ch, n_agent_views, svs, L);
     int64_t k = 0;
-    const int S = L.svs, G = L.ng, KK = L.K;
-    const size_t per_tile = (size_t)L.nb * kSvBatch * L.rec;
+    const int S = L.svs, G = L.ng, KK = L.K, CH = L.chunks;
+    const size_t per_tile = (size_t)L.nb * CH * kSvBatch * L.rec;
     for (int sv = 0; sv < L.n_sv; ++sv) {
         const int r0 = (sv / L.n_sv_side) * S, c0 = (sv % L.n_sv_side) * S;
         const int2_t* bt = &L.band[(size_t)sv * L.views];
         std::vector<int> seen(S * S, 0);
         for (int t = 0; t < L.nb * kSvBatch; ++t) {
-            const uint32_t* rec = &L.data[(size_t)sv * per_tile + (size_t)t * L.rec];
+            const int slot = t % kSvBatch;
+            const uint32_t* blk0 = &L.data[(size_t)sv * per_tile + (size_t)(t / kSvBatch) * CH * kSvBatch * L.rec];
             const int q = sv_slot_pixel(S, t);
             if (q >= 0) seen[q]++;
             for (int j = 0; j < L.views; ++j) {
-                const int g = j >> 5, l = j & 31;
-                const int o = (int)((rec[G * 32 * KK + l] >> (8 * g)) & 0xffu);
+                const int gt = j >> 5, g = gt % G, l = j & 31;
+                const uint32_t* blk = blk0 + (size_t)(gt / G) * kSvBatch * L.rec;  // the view's chunk
+                const int o = (int)((blk[sv_ofs_word(G, KK, l, slot)] >> (8 * g)) & 0xffu);
                 for (int e = 0; e < KK; ++e) {
                     float a;
-                    std::memcpy(&a, &rec[((size_t)g * 32 + l) * KK + e], 4);
+                    std::memcpy(&a, &blk[sv_len_word(G, KK, g, l, slot, e)], 4);
                     if (a == 0.0f) continue;
                     if (q < 0) throw std::runtime_error("padding slot with a value");
                     if (o + e >= bt[j].y) throw std::runtime_error("slot outside its band window");
