@@ -181,6 +181,9 @@ __device__ __forceinline__ void load_batch(SvBatch<K, NG>& B, const uint32_t* __
 // only, the L2 prefetch pointer advanced per batch, and band addresses by one byte permute
 #define MACE_K2_TRIM 1
 #endif
+#ifndef MACE_K2_BC8
+#define MACE_K2_BC8 1  // batch constants by one 256-bit + one 64-bit load (3 loads before)
+#endif
 #ifndef MACE_K2_V8
 #define MACE_K2_V8 1  // 256-bit e-window loads
 #endif
@@ -543,10 +546,22 @@ __global__ void __launch_bounds__(MW == 0 ? 32 : (MW == 1 ? 256 : 512),
                                  : "memory");
             }
 #endif
+#if MACE_K2_BC8  // the batch's theta2 x4 and first four cross terms as one 256-bit broadcast load
+            float bk[10];
+            asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                : "=f"(bk[0]), "=f"(bk[1]), "=f"(bk[2]), "=f"(bk[3]), "=f"(bk[4]), "=f"(bk[5]), "=f"(bk[6]), "=f"(bk[7])
+                : "l"(bcs + 16 * b));
+            {
+                const float2 k2 = __ldg(reinterpret_cast<const float2*>(bcs + 16 * b + 8));
+                bk[8] = k2.x;
+                bk[9] = k2.y;
+            }
+#else
             const float4 k0 = __ldg(reinterpret_cast<const float4*>(bcs + 16 * b));
             const float4 k1 = __ldg(reinterpret_cast<const float4*>(bcs + 16 * b) + 1);
             const float2 k2 = __ldg(reinterpret_cast<const float2*>(bcs + 16 * b + 8));
             const float bk[10] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w, k2.x, k2.y};
+#endif
             // local pixel kx = lr S + lc of slot p (visit-order table); ok = real and inside the image
             const uint32_t kxw = c_svorder<S>.v[b];
             int kx[4];
