@@ -27,20 +27,22 @@ ap.add_argument("--groups", default="0,2")
 ap.add_argument("--iters", type=int, default=8000)
 ap.add_argument("--ref", default="")
 ap.add_argument("--save", default="", help="save the final image of each run here (npz)")
+ap.add_argument("--schedule", default="sv", choices=["sv", "sv-det"])
 a = ap.parse_args()
 c = gen.CONFIGS[a.config]
 t = time.time()
 geom, mats, phantom, y, lam = gen.make_scan(a.config)
 N, n = c["n_agents"], geom.n_pixels
 prior = mb.PriorParams("qggmrf", beta=c["beta"], p=2.0, q=1.2, T=1.0, sigma_x=0.01)
-plan = plan_for(mats, [s.view_indices for s in mb.partition_views(geom.n_views, N)], schedule="sv", sv=8)
+plan = plan_for(mats, [s.view_indices for s in mb.partition_views(geom.n_views, N)], schedule=a.schedule, sv=8)
 plan.load_data(y, lam)
 plan.set_prior(prior)
 ref = np.load(a.ref or os.path.join(ROOT, "tests", "golden", f"central_c{a.config}.npz"))["image"].astype(np.float32)
 print(f"setup {time.time() - t:.1f} s; ref {a.ref or 'central_c%d' % a.config}", flush=True)
 saved = {}
 for g in [int(x) for x in a.groups.split(",")]:
-    plan.set_agent_groups(g)
+    if a.schedule == "sv":
+        plan.set_agent_groups(g)
     for sg in [float(x) for x in a.sigmas.split(",")]:
         plan.set_agent_params(-1, prior.beta / N, 1.0 / sg ** 2, False)
         plan.set_ref(ref)
