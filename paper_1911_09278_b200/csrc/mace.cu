@@ -194,14 +194,14 @@ static void launch_raster(Ctx* c, const PassParams& P, int n_agents, int agent_b
 }
 
 // one super-voxel pass over P.queue (k2_inst.cu, one unit per tile side)
-static void dispatch_sv(Ctx* c, const PassParams& P, int na)
+static void dispatch_sv(Ctx* c, const PassParams& P, int na, double frac = -1.0)
 {
     SvLaunch L;
     L.device = c->device;
     L.stream = c->stream;
     L.smem = c->sv_smem;
     L.num_sms = c->num_sms;
-    L.frac = c->sv_frac;
+    L.frac = frac > 0.0 ? frac : c->sv_frac;
     L.max_warps = c->sv_max_warps;
     L.agents_in_queue = na;
     L.K = c->sv_K;
@@ -280,7 +280,9 @@ static void run_pass(Ctx* c, int mode, float rho, const float* gimg, int a0, int
             Pk.part = c->part.p + (size_t)cs[k] * 4;
             Pk.head = c->heads.p + k;
             Pk.det = 1;
-            dispatch_sv(c, Pk, na);
+            // a class is its own concurrency bound (its tiles all read the class-start snapshot), so
+            // every resident warp may take one of its tiles
+            dispatch_sv(c, Pk, na, 1.0);
             k_fold_delta<<<c->num_sms * 4, 256, 0, c->stream>>>(c->E.p, c->ED.p, c->total_rows, c->done.p);
             CK(cudaGetLastError());
         }
