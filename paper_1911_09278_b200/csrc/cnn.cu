@@ -129,8 +129,23 @@ __device__ __forceinline__ void umma_commit_e(uint64_t* bar)
 #ifdef K5_TRACE  // profiling builds only (tools/micro/k5_trace.cu): per-CTA clock64 timeline of a layer
 __device__ long long g_k5_trace[148][64];  // [0] start, [1] weights landed, [2+2t] tile t issued, [3+2t] tile t stored
 #define K5T(i) g_k5_trace[blockIdx.x][(i)] = clock64()
+#define K5V(i, v) g_k5_trace[blockIdx.x][(i)] = (v)
+#define K5ACC(var, stmt)            \
+    {                               \
+        const long long c_ = clock64(); \
+        stmt;                       \
+        var += clock64() - c_;      \
+    }
+__device__ __forceinline__ long long k5_gtime()
+{
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 #else
 #define K5T(i)
+#define K5V(i, v)
+#define K5ACC(var, stmt) stmt;
 #endif
 __global__ void __launch_bounds__(192, 1) k_conv64_tc(const __grid_constant__ CUtensorMap amap,
                                                       const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* out,
@@ -337,7 +352,10 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kAcc);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) K5T(0);
+    if (tid == 0) {
+        K5T(0);
+        K5V(48, k5_gtime());
+    }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int strips = (W + kTileX - 1) / kTileX;
     const int strip = blockIdx.x % strips;
@@ -377,8 +395,12 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
             mbar_expect(wbar, kWBytes);
             bulk_copy(sw, wts, kWBytes, wbar);
             asm volatile("griddepcontrol.wait;" ::: "memory");
+            K5T(30);
             for (int r = y0 - 1; r <= y1; ++r) {
                 const int q = r - rbase, s = q % kSlots, u = q / kSlots;
+#ifdef K5_NO_TMA  // timing experiment only: the ring is filled once, later rows reuse what is there
+                if (q >= kSlots) break;
+#endif
                 if (u >= 1) mbar_wait(sempty + s, (uint32_t)((u - 1) & 1));
                 mbar_expect(sfull + s, kSlotBytes);
                 tma_row(slots + s * kSlotBytes, &amap, x0 / 8 - 1, r, sfull + s);
@@ -390,14 +412,19 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
             mbar_wait(wbar, 0);
             if (lane == 0) K5T(1);
             int landed = y0 - 2;  // halo rows <= landed are known to be in shared memory
+            [[maybe_unused]] long long st_full = 0, st_acc = 0, st_issue = 0;
             for (int t = 0; t < n_units; ++t) {
                 const int y = y0 + R * t, b = t & 1, ub = t >> 1;
                 const int nr = min(R, y1 - y);  // rows in this unit
                 if (ub >= 1) {
-                    mbar_wait(aempty + b, (uint32_t)((ub - 1) & 1));
+                    K5ACC(st_acc, mbar_wait(aempty + b, (uint32_t)((ub - 1) & 1)))
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 }
                 const uint32_t d = tmem + (uint32_t)(b * R * 64);
+#ifdef K5_TRACE
+                int rstamp = 19;
+                if (t == 2 && lane == 0) K5T(18);
+#endif
                 // one halo row r against weight block blk (0 = dy2, 1 = dy1, 2 = dy0) with N = 64 or 128
                 auto row = [&](int r, int blk, uint32_t dcol, uint32_t idesc, bool first) {
                     // wait for halo rows just before their first UMMAs, so the UMMAs already queued keep
@@ -406,15 +433,22 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
                         while (landed < r) {
                             ++landed;
                             const int q = landed - rbase;
-                            mbar_wait(sfull + q % kSlots, (uint32_t)((q / kSlots) & 1));
+#ifdef K5_NO_TMA
+                            if (q >= kSlots) continue;
+#endif
+                            K5ACC(st_full, mbar_wait(sfull + q % kSlots, (uint32_t)((q / kSlots) & 1)))
                         }
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     }
                     const uint64_t a0 = sdesc(sl_base + ((r - rbase) % kSlots) * kSlotBytes + kHaloOff * 16,
                                               kHaloX * 16, 128);
                     const uint64_t b0 = sdesc(sw_base + blk * kC * 16, kW2Icg, 128);
-                    umma_row12(dcol, a0, b0, idesc, first ? 0u : 1u);
+                    K5ACC(st_issue, umma_row12(dcol, a0, b0, idesc, first ? 0u : 1u))
+#ifdef K5_TRACE
+                    if (t == 2 && lane == 0 && rstamp < 24) K5T(rstamp++);
+#endif
                 };
+
                 if (nr == 3) {
                     row(y + 1, 0, d, kIdesc192, true);      // [acc_y | acc_y+1 | acc_y+2] = A_y+1 [W_dy2 | W_dy1 | W_dy0]
                     row(y, 1, d, kIdesc128, false);         // [acc_y | acc_y+1] += A_y [W_dy1 | W_dy0]
@@ -432,9 +466,22 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
                     row(y + 1, 0, d, kIdesc, false);
                 }
                 umma_commit_e(afull + b);
-                if (lane == 0 && t < 14) K5T(2 + 2 * t);
+#ifdef K5_TRACE
+                if (t == 2 && lane == 0) K5T(24);
+#endif
+                if (lane == 0 && t < 8) {
+                    K5T(2 + 2 * t);
+                    K5V(32 + t, st_full);
+                    K5V(40 + t, st_acc);
+                    K5V(56 + t, st_issue);
+                }
+#ifndef K5_NO_SLOTCOMMIT  // (timing experiment with K5_NO_TMA)
                 for (int r = y - 1; r < y - 1 + nr; ++r)  // rows y-1 .. y+nr-2: last read by this unit
                     umma_commit_e(sempty + (r - rbase) % kSlots);
+#endif
+#ifdef K5_TRACE
+                if (t == 2 && lane == 0) K5T(25);
+#endif
             }
         }
     } else {  // ---- epilogue warps 2..5
@@ -447,11 +494,15 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
             for (int rr = 0; rr < nrows; ++rr) {
                 const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * R * 64 + rr * 64);
                 uint32_t r[64];
+#ifdef K5_NO_LD  // timing experiment only: the accumulators are not read
+                for (int i = 0; i < 64; ++i) r[i] = base + i;
+#else
                 LD16(base + 0, (r + 0));
                 LD16(base + 16, (r + 16));
                 LD16(base + 32, (r + 32));
                 LD16(base + 48, (r + 48));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#endif
                 if (rr == nrows - 1) {
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     __syncwarp();
@@ -459,7 +510,7 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
                         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(aempty + b)) : "memory");
                 }
                 const int px = x0 + quad * 32 + lane;
-                if (rr == 0 && warp == 2 && lane == 0 && t < 14) K5T(3 + 2 * t);  // accumulators read
+                if (rr == 0 && warp == 2 && lane == 0 && t < 8) K5T(3 + 2 * t);  // accumulators read
 #ifdef K5_NO_STORE  // timing experiment only: skip the activation stores
                 if (px < 0) {
 #else
@@ -481,12 +532,280 @@ __global__ void __launch_bounds__(192, 1) k_conv64_tc2(const __grid_constant__ C
                     }
                 }
             }
+            if (warp == 2 && lane == 0 && t < 8) K5T(50 + t);  // unit stored
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (tid == 0) {
+        K5T(31);
+        K5V(49, k5_gtime());
+    }
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAccCols) : "memory");
+}
+
+// Rolling-accumulator variant of the 64->64 layer (k_conv64_roll, the default).  The issue path of
+// the row-unit kernels is the bottleneck, not the tensor pipe: a UMMA costs the issuing thread ~45-58
+// cycles whatever its N (tools/micro/umma_rate.cu: 44.7 cycles per M = 128 UMMA at N = 16..64), the
+// N = 64 UMMAs of a unit's first and last halo rows run at 48 cycles for 32 cycles of math, and the
+// four commits and waits at every unit boundary drain the pipe (tools/micro/k5_trace3.cu: 4,750 cycles
+// per row triple against 3,835 for the same 60 UMMAs alone).  Here every halo row r is ONE run of
+// N = 192 UMMAs against [W_dy2 | W_dy1 | W_dy0] into the accumulators of output rows r-1, r, r+1,
+// which sit side by side in TMEM: output row y owns the 64 columns of slot (y - y0) mod 8, so the
+// three accumulators of a halo row are contiguous except where the window wraps (2 rows in 8: split
+// into N = 128 + N = 64).  Row r+1's accumulator starts with this halo row, so the first of the 12
+// (dx, K-step) UMMAs is issued as N = 128 accumulating + N = 64 overwriting and the other 11 as
+// N = 192: 13 UMMAs and 1,168 tensor cycles per output row (1,152 = pure math) instead of 20 UMMAs
+// and 1,280.  One commit per halo row (rowdone) tells the epilogue that output row r-1 is complete
+// and the TMA producer that the halo slot is free; the epilogue drains one row at a time.
+__device__ __forceinline__ void umma_row13(uint32_t d_tmem, uint64_t a0, uint64_t b0)
+{
+    static_assert(kHaloX == 144 && kW2Dx == 24576 && kW2Icg == 3072, "offsets below are hard-coded");
+    asm volatile(
+        "{\n.reg .pred e, f, t;\n.reg .b64 a, b;\n.reg .b32 d2;\n"
+        "elect.sync _|e, 0xffffffff;\nsetp.eq.b32 t, 1, 1;\nsetp.ne.b32 f, 1, 1;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, t;\n"          // rows r-1, r: += A [W_dy2 | W_dy1]
+        "add.u32 d2, %0, 128;\nadd.s64 b, %2, 128;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [d2], %1, b, %4, f;\n"           // row r+1: = A W_dy0
+        "add.s64 a, %1, 288;\nadd.s64 b, %2, 384;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n"
+        "add.s64 a, %1, 576;\nadd.s64 b, %2, 768;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n"
+        "add.s64 a, %1, 864;\nadd.s64 b, %2, 1152;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n"
+        "add.s64 a, %1, 1;\nadd.s64 b, %2, 1536;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n"
+        "add.s64 a, %1, 289;\nadd.s64 b, %2, 1920;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n"
+        "add.s64 a, %1, 577;\nadd.s64 b, %2, 2304;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n"
+        "add.s64 a, %1, 865;\nadd.s64 b, %2, 2688;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n"
+        "add.s64 a, %1, 2;\nadd.s64 b, %2, 3072;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n"
+        "add.s64 a, %1, 290;\nadd.s64 b, %2, 3456;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n"
+        "add.s64 a, %1, 578;\nadd.s64 b, %2, 3840;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n"
+        "add.s64 a, %1, 866;\nadd.s64 b, %2, 4224;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n"
+        "}\n"
+        ::"r"(d_tmem), "l"(a0), "l"(b0), "r"(kIdesc128), "r"(kIdesc), "r"(kIdesc192)
+        : "memory");
+}
+// the 11 (dx, K-step) UMMAs after the first, all accumulating (generic rows: one call per run of
+// contiguous accumulators)
+__device__ __forceinline__ void umma_row11(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc)
+{
+    asm volatile(
+        "{\n.reg .pred e, t;\n.reg .b64 a, b;\n"
+        "elect.sync _|e, 0xffffffff;\nsetp.eq.b32 t, 1, 1;\n"
+        "add.s64 a, %1, 288;\nadd.s64 b, %2, 384;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 576;\nadd.s64 b, %2, 768;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 864;\nadd.s64 b, %2, 1152;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 1;\nadd.s64 b, %2, 1536;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 289;\nadd.s64 b, %2, 1920;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 577;\nadd.s64 b, %2, 2304;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 865;\nadd.s64 b, %2, 2688;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 2;\nadd.s64 b, %2, 3072;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 290;\nadd.s64 b, %2, 3456;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 578;\nadd.s64 b, %2, 3840;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "add.s64 a, %1, 866;\nadd.s64 b, %2, 4224;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "}\n"
+        ::"r"(d_tmem), "l"(a0), "l"(b0), "r"(idesc)
+        : "memory");
+}
+
+// a wrapping halo row as one asm block: run A (12 UMMAs into dA) interleaved with run B (into dB: the first
+// UMMA with its own descriptor and accumulate flag, the other 11 accumulating with idB_rest) and, if hasC,
+// one overwriting N = 64 UMMA into dC next to the first pair
+__device__ __forceinline__ void umma_row_wrap(uint64_t a0, uint32_t dA, uint64_t bA, uint32_t idA, uint32_t dB, uint64_t bB,
+                                              uint32_t idB_first, uint32_t idB_rest, uint32_t accB_first, uint32_t dC,
+                                              uint64_t bC, uint32_t hasC)
+{
+    asm volatile(
+        "{\n.reg .pred e, ec, pb, t, f;\n.reg .b64 a, b, c;\n"
+        "elect.sync _|e, 0xffffffff;\nsetp.eq.b32 t, 1, 1;\nsetp.ne.b32 f, 1, 1;\nsetp.ne.b32 pb, %8, 0;\n"
+        "setp.ne.b32 ec, %11, 0;\nand.pred ec, ec, e;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%1], %0, %2, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%4], %0, %5, %6, pb;\n"
+        "@ec tcgen05.mma.cta_group::1.kind::f16 [%9], %0, %10, %12, f;\n"
+#define WR(ao, bo)                                                                                      \
+    "add.s64 a, %0, " #ao ";\nadd.s64 b, %2, " #bo ";\nadd.s64 c, %5, " #bo ";\n"                     \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%1], a, b, %3, t;\n@e tcgen05.mma.cta_group::1.kind::f16 [%4], a, c, %7, t;\n"
+        WR(288, 384) WR(576, 768) WR(864, 1152) WR(1, 1536) WR(289, 1920) WR(577, 2304) WR(865, 2688) WR(2, 3072)
+        WR(290, 3456) WR(578, 3840) WR(866, 4224)
+#undef WR
+        "}\n"
+        ::"l"(a0), "r"(dA), "l"(bA), "r"(idA), "r"(dB), "l"(bB), "r"(idB_first), "r"(idB_rest), "r"(accB_first), "r"(dC),
+          "l"(bC), "r"(hasC), "r"(kIdesc)
+        : "memory");
+}
+
+constexpr int kRollAcc = 8;  // accumulator slots of 64 fp32 columns: all 512 TMEM columns
+
+__global__ void __launch_bounds__(192, 1) k_conv64_roll(const __grid_constant__ CUtensorMap amap,
+                                                        const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* out,
+                                                        int H, int W, int Wp, int rows_per_cta)
+{
+    extern __shared__ __align__(1024) unsigned char sm[];
+    unsigned char* sw = sm;
+    unsigned char* slots = sm + kWBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + kSlots * kSlotBytes);
+    uint64_t* wbar = bars;
+    uint64_t* sfull = bars + 1;             // [kSlots] halo row landed
+    uint64_t* rowdone = sfull + kSlots;     // [kSlots] the halo row's UMMAs have completed
+    uint64_t* aempty = rowdone + kSlots;    // [kRollAcc] accumulator slot drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kRollAcc);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        K5T(0);
+        K5V(48, k5_gtime());
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int strips = (W + kTileX - 1) / kTileX;
+    const int strip = blockIdx.x % strips;
+    const int x0 = strip * kTileX;
+    const int y0 = (blockIdx.x / strips) * rows_per_cta;
+    const int y1 = min(H, y0 + rows_per_cta);
+    if (y0 >= H) return;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(tmem_slot)),
+                     "n"(kRollAcc * 64)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 32) {
+        mbar_init(wbar, 1);
+        for (int i = 0; i < kSlots; ++i) {
+            mbar_init(sfull + i, 1);
+            mbar_init(rowdone + i, 1);
+        }
+        for (int i = 0; i < kRollAcc; ++i) mbar_init(aempty + i, 4);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const int rbase = y0 - 1;  // halo row r has ring index q = r - rbase
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            mbar_expect(wbar, kWBytes);
+            bulk_copy(sw, wts, kWBytes, wbar);
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            K5T(30);
+            for (int r = y0 - 1; r <= y1; ++r) {
+                const int q = r - rbase, s = q % kSlots, u = q / kSlots;
+                if (u >= 1) mbar_wait(rowdone + s, (uint32_t)((u - 1) & 1));
+                mbar_expect(sfull + s, kSlotBytes);
+                tma_row(slots + s * kSlotBytes, &amap, x0 / 8 - 1, r, sfull + s);
+            }
+        }
+    } else if (warp == 1) {  // ---- MMA issuer (whole warp, one elected lane issues)
+        const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
+        mbar_wait(wbar, 0);
+        if (lane == 0) K5T(1);
+        [[maybe_unused]] long long st_full = 0, st_acc = 0, st_issue = 0, st_commit = 0, st_wrap = 0;
+        for (int r = y0 - 1; r <= y1; ++r) {
+            const int q = r - rbase, s = q % kSlots;
+            // accumulators fed by this halo row: output rows r-1 (W_dy2), r (W_dy1), r+1 (W_dy0)
+            const bool v0 = r - 1 >= y0, v1 = r >= y0 && r < y1, v2 = r + 1 < y1;
+#ifdef K5_TRACE
+            const bool st4 = lane == 0 && q == 4;
+            if (st4) K5T(23);
+#endif
+            if (v2 && q >= kRollAcc) {  // row r+1 starts in slot q mod 8: drained of output row r+1-8?
+                K5ACC(st_acc, mbar_wait(aempty + (q % kRollAcc), (uint32_t)((q / kRollAcc - 1) & 1)))
+            }
+            K5ACC(st_full, mbar_wait(sfull + s, (uint32_t)((q / kSlots) & 1)))
+            if (lane == 0 && q == 0) K5T(31);
+#ifdef K5_TRACE
+            if (st4) K5T(24);
+#endif
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#ifdef K5_TRACE
+            if (st4) K5T(25);
+#endif
+            const uint32_t abase = sl_base + s * kSlotBytes + kHaloOff * 16;
+            const uint64_t a0 = sdesc(abase, kHaloX * 16, 128);
+            const int s0 = (q + kRollAcc - 2) % kRollAcc;  // slot of output row r-1; r: s0+1, r+1: s0+2 (mod 8)
+            // B = [W_dy2 | W_dy1 | W_dy0] from block k on; accumulator of block k in slot (s0 + k) mod 8
+            auto bd = [&](int k) { return sdesc(sw_base + k * kC * 16, kW2Icg, 128); };
+            auto dc = [&](int k) { return tmem + (uint32_t)(((s0 + k) % kRollAcc) * 64); };
+            if (v0 && v1 && v2) {
+                if (s0 + 2 < kRollAcc) {
+#ifdef K5_TRACE
+                    if (st4) K5T(26);
+#endif
+                    K5ACC(st_issue, umma_row13(dc(0), a0, bd(0)))
+#ifdef K5_TRACE
+                    if (st4) K5T(27);
+#endif
+                } else if (s0 + 1 < kRollAcc) {  // slots 6, 7 | 0
+                    K5ACC(st_wrap, umma_row_wrap(a0, dc(0), bd(0), kIdesc128, dc(2), bd(2), kIdesc, kIdesc, 0u, 0u, 0ull, 0u))
+                } else {  // slots 7 | 0, 1: rows r, r+1 share all but the first UMMA (row r+1's overwrites)
+                    K5ACC(st_wrap, umma_row_wrap(a0, dc(0), bd(0), kIdesc, dc(1), bd(1), kIdesc, kIdesc128, 1u, dc(2), bd(2), 1u))
+                }
+            } else if (v1 && v2 && !v0 && (s0 + 1) % kRollAcc + 1 < kRollAcc) {  // the CTA's first image row
+                umma_e(dc(1), a0, bd(1), kIdesc, 1u);
+                umma_e(dc(2), a0, bd(2), kIdesc, 0u);
+                umma_row11(dc(1), a0, bd(1), kIdesc128);
+            } else if (v0 && v1 && !v2 && s0 + 1 < kRollAcc) {  // the CTA's last image row
+                umma_row12(dc(0), a0, bd(0), kIdesc128, 1u);
+            } else {  // top and bottom halo rows, short CTAs: one N = 64 run per accumulator
+                if (v0) umma_row12(dc(0), a0, bd(0), kIdesc, 1u);
+                if (v1) umma_row12(dc(1), a0, bd(1), kIdesc, 1u);
+                if (v2) umma_row12(dc(2), a0, bd(2), kIdesc, 0u);
+            }
+            K5ACC(st_commit, umma_commit_e(rowdone + s))
+#ifdef K5_TRACE
+            if (st4) K5T(28);
+#endif
+            if (lane == 0 && q < 16) K5T(2 + q);
+            if (lane == 0 && q < 14) K5V(50 + q, st_full + st_acc);
+        }
+        if (lane == 0) {
+            K5V(18, st_full);
+            K5V(19, st_acc);
+            K5V(20, st_issue);
+            K5V(21, st_commit);
+            K5V(22, st_wrap);
+        }
+    } else {  // ---- epilogue warps 2..5: output row y is complete once halo row y+1 is done
+        const int quad = warp & 3;
+        for (int y = y0; y < y1; ++y) {
+            const int q = y + 1 - rbase, a = (y - y0) % kRollAcc;
+            mbar_wait(rowdone + q % kSlots, (uint32_t)((q / kSlots) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a * 64);
+            uint32_t r[64];
+            LD16(base + 0, (r + 0));
+            LD16(base + 16, (r + 16));
+            LD16(base + 32, (r + 32));
+            LD16(base + 48, (r + 48));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (warp == 2 && lane == 0 && y - y0 < 14) K5T(32 + y - y0);
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(aempty + a)) : "memory");
+            const int px = x0 + quad * 32 + lane;
+            if (px < W) {
+                uint4* dst = reinterpret_cast<uint4*>(out) + ((size_t)y * Wp + px);
+                const size_t gstride = (size_t)H * Wp;
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const float lo = fmaxf(__uint_as_float(r[8 * g + 2 * h]), 0.f);
+                        const float hi = fmaxf(__uint_as_float(r[8 * g + 2 * h + 1]), 0.f);
+                        const __nv_bfloat162 v2 = __floats2bfloat162_rn(lo, hi);
+                        pk[h] = *reinterpret_cast<const uint32_t*>(&v2);
+                    }
+                    dst[g * gstride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) K5V(49, k5_gtime());
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kRollAcc * 64) : "memory");
 }
 
 // All 15 middle layers in ONE persistent launch (k_conv64_seq): every CTA keeps its (strip, row run)
@@ -1050,8 +1369,8 @@ void Cnn::set_weights(const uint16_t* bf16, int layers, int channels)
     }
     w_mid2.alloc(wm2.size());
     CKC(cudaMemcpy(w_mid2.p, wm2.data(), wm2.size() * 2, cudaMemcpyHostToDevice));
-    const char* ev = std::getenv("MACE_K5_ROWS");  // output rows per MMA unit: 1, 2 or 3
-    rows_unit = ev ? std::max(1, std::min(3, std::atoi(ev))) : 3;  // triples: 0.270 vs 0.278 ms (pairs) per 512^2
+    const char* ev = std::getenv("MACE_K5_ROWS");  // output rows per MMA unit: 1, 2 or 3; 0 = rolling accumulators
+    rows_unit = ev ? std::max(0, std::min(3, std::atoi(ev))) : 0;
     (void)n17;
 
     w_mid.alloc(wm.size());
@@ -1075,6 +1394,7 @@ void Cnn::ensure(int h, int w)
     CKC(cudaFuncSetAttribute(k_conv64_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv64_tc2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv64_tc2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    CKC(cudaFuncSetAttribute(k_conv64_roll, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv_last_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kLSmem));
     CKC(cudaFuncSetAttribute(k_conv64_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     flags.alloc(1024);
@@ -1100,7 +1420,10 @@ void Cnn::launch_mid(int l, const CUtensorMap& m, __nv_bfloat16* dst, cudaStream
     cfg.stream = s;
     cfg.attrs = pdl;
     cfg.numAttrs = pdl_on ? 1 : 0;
-    if (rows_unit == 3)
+    if (rows_unit == 0)
+        CKC(cudaLaunchKernelEx(&cfg, k_conv64_roll, m, (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC), dst,
+                               H, W, Wp, per));
+    else if (rows_unit == 3)
         CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc2<3>, m, (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC),
                                dst, H, W, Wp, per));
     else if (rows_unit == 2)

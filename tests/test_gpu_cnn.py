@@ -51,7 +51,9 @@ def test_cnn_matches_cpu_oracle(n_side, seed):
     assert rel(r_gpu, r_ref) < 4e-2, rel(r_gpu, r_ref)
 
 
-@pytest.mark.parametrize("n_side,seed", [(64, 11), (200, 12), (512, 13)])
+# 16 and 40: one output row per CTA; 200 and 300: short row runs; 512: 14 rows (the rolling accumulators
+# wrap once); 1024: 57 rows per CTA (seven wraps)
+@pytest.mark.parametrize("n_side,seed", [(16, 14), (40, 15), (64, 11), (200, 12), (300, 17), (512, 13), (1024, 16)])
 def test_cnn_exact_taps_channels_padding(n_side, seed):
     """Every middle layer is a single 3x3 tap and a channel permutation (one nonzero product per
     output), so both sides compute exactly: the GPU must reproduce the oracle bit for bit,
@@ -215,7 +217,8 @@ def test_cnn_launch_variants_are_bit_identical(n_side, monkeypatch):
     assert np.array_equal(outs[("1", "fma")], outs[("0", "fma")])
     r_tc, r_fma = _net(x, outs[("0", "tc")]), _net(x, outs[("0", "fma")])
     assert rel(r_tc, r_fma) < 1e-5
-    # row units per MMA batch (MACE_K5_ROWS): each output row receives the same UMMAs in another
+    # row units per MMA batch (MACE_K5_ROWS; 0 = one halo row at a time into rolling accumulators):
+    # each output row receives the same UMMAs in another
     # order (fp32 accumulation), and one-ulp bf16 differences compound over 17 random unit-scale
     # layers -- so single rows, pairs and triples are each held to the CPU oracle like the default
     # (test_cnn_matches_cpu_oracle), and to each other at that level
@@ -223,8 +226,9 @@ def test_cnn_launch_variants_are_bit_identical(n_side, monkeypatch):
     monkeypatch.setenv("MACE_K5_LAST", "tc")
     ref = np.asarray(x, np.float32) - cnn_apply(np.asarray(x, np.float32), w, n_side)
     units = {}
-    for r in ("1", "2", "3"):
+    for r in ("0", "1", "2", "3"):  # "0": rolling accumulators (k_conv64_roll, the default)
         monkeypatch.setenv("MACE_K5_ROWS", r)
         units[r] = _net(x, CnnDenoiser(n_side, weights=w)(x))
         assert rel(units[r], ref) < 4e-2, (r, rel(units[r], ref))
     assert rel(units["2"], units["3"]) < 4e-2 and rel(units["1"], units["3"]) < 4e-2
+    assert rel(units["0"], units["3"]) < 4e-2
