@@ -136,6 +136,8 @@ __device__ long long g_k5_trace[148][64];  // [0] start, [1] weights landed, [2+
         stmt;                       \
         var += clock64() - c_;      \
     }
+__device__ long long g_k5_life[4096][4];  // {smid, start, gdc wait passed, end} in globaltimer ns, one record per CTA
+__device__ unsigned g_k5_life_n;
 __device__ __forceinline__ long long k5_gtime()
 {
     long long t;
@@ -634,9 +636,23 @@ __device__ __forceinline__ void umma_row_wrap(uint64_t a0, uint32_t dA, uint64_t
 
 constexpr int kRollAcc = 8;  // accumulator slots of 64 fp32 columns: all 512 TMEM columns
 
-__global__ void __launch_bounds__(192, 1) k_conv64_roll(const __grid_constant__ CUtensorMap amap,
-                                                        const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* out,
-                                                        int H, int W, int Wp, int rows_per_cta)
+// kSeq: all n_layers middle layers in one cooperative launch.  Every CTA keeps its (strip, row run); the
+// halo ring, the accumulator slots and every mbarrier phase simply run on from layer to layer.  Layer l
+// reads act[l % 2] (map0 / map1) and writes act[(l + 1) % 2].  Between layers a grid-wide arrive / wait on
+// one counter: after a layer's last row the epilogue warps fence their stores and one thread adds 1
+// (release); the producer waits for (epoch x (n_layers - 1) + l) x CTAs arrivals (acquire), then a proxy
+// fence orders the TMA reads behind the other CTAs' generic-proxy stores.  The same wait covers the
+// write-after-read hazard of the ping-pong buffers (every CTA has finished reading layer l - 1's input
+// before anyone writes layer l's output over it).  The next layer's weights are copied in as soon as the
+// layer's last UMMA has completed, i.e. during the wait.
+__device__ unsigned g_k5_sync_timeout;  // set if a grid-wide wait ever gave up (never, unless a CTA died)
+
+template <bool kSeq>
+__global__ void __launch_bounds__(192, 1) k_conv64_roll(const __grid_constant__ CUtensorMap map0,
+                                                        const __grid_constant__ CUtensorMap map1,
+                                                        const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* out0,
+                                                        __nv_bfloat16* out1, int H, int W, int Wp, int rows_per_cta,
+                                                        int n_layers, unsigned* sync_ctr, unsigned sync_base)
 {
     extern __shared__ __align__(1024) unsigned char sm[];
     unsigned char* sw = sm;
@@ -649,17 +665,27 @@ __global__ void __launch_bounds__(192, 1) k_conv64_roll(const __grid_constant__ 
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kRollAcc);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef K5_TRACE
+    __shared__ unsigned life_idx;
     if (tid == 0) {
         K5T(0);
         K5V(48, k5_gtime());
+        life_idx = atomicAdd(&g_k5_life_n, 1u) % 4096u;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_k5_life[life_idx][0] = smid;
+        g_k5_life[life_idx][1] = k5_gtime();
     }
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+    if constexpr (!kSeq) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int strips = (W + kTileX - 1) / kTileX;
     const int strip = blockIdx.x % strips;
     const int x0 = strip * kTileX;
     const int y0 = (blockIdx.x / strips) * rows_per_cta;
     const int y1 = min(H, y0 + rows_per_cta);
-    if (y0 >= H) return;
+    if (y0 >= H) return;  // (never in a kSeq launch: the grid is exactly the CTAs that own rows)
+    const int nrows = y1 - y0, nq = nrows + 2;  // output rows and halo rows per layer
+    const int L = kSeq ? n_layers : 1;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(tmem_slot)),
@@ -680,83 +706,94 @@ __global__ void __launch_bounds__(192, 1) k_conv64_roll(const __grid_constant__ 
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    const int rbase = y0 - 1;  // halo row r has ring index q = r - rbase
+    const int rbase = y0 - 1;  // halo row r of a layer has index q = r - rbase; ring index Q = l nq + q
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
-            mbar_expect(wbar, kWBytes);
-            bulk_copy(sw, wts, kWBytes, wbar);
-            asm volatile("griddepcontrol.wait;" ::: "memory");
-            K5T(30);
-            for (int r = y0 - 1; r <= y1; ++r) {
-                const int q = r - rbase, s = q % kSlots, u = q / kSlots;
-                if (u >= 1) mbar_wait(rowdone + s, (uint32_t)((u - 1) & 1));
-                mbar_expect(sfull + s, kSlotBytes);
-                tma_row(slots + s * kSlotBytes, &amap, x0 / 8 - 1, r, sfull + s);
+            for (int l = 0; l < L; ++l) {
+                if (l > 0) {  // the weights buffer is free once the previous layer's last halo row is done
+                    const int Ql = l * nq - 1;
+                    mbar_wait(rowdone + Ql % kSlots, (uint32_t)((Ql / kSlots) & 1));
+                }
+                mbar_expect(wbar, kWBytes);
+                bulk_copy(sw, wts + (size_t)l * 9 * kC * kC, kWBytes, wbar);
+                if (l == 0) {
+                    asm volatile("griddepcontrol.wait;" ::: "memory");
+                    K5T(30);
+#ifdef K5_TRACE
+                    g_k5_life[life_idx][2] = k5_gtime();
+#endif
+                } else {
+                    // every CTA has stored (and fenced) layer l - 1
+                    const unsigned target = sync_base + (unsigned)l * gridDim.x;
+                    unsigned seen, spins = 0;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(sync_ctr) : "memory");
+                        if ((int)(seen - target) >= 0) break;
+                        if (++spins > (1u << 26)) {  // seconds: a CTA died; give up loudly rather than hang
+                            g_k5_sync_timeout = 1u;
+                            __trap();
+                        }
+                    } while (true);
+                    asm volatile("fence.proxy.async;" ::: "memory");
+                }
+                const CUtensorMap* map = (l & 1) ? &map1 : &map0;
+                for (int q = 0; q < nq; ++q) {
+                    const int Q = l * nq + q, s = Q % kSlots, u = Q / kSlots;
+                    if (u >= 1) mbar_wait(rowdone + s, (uint32_t)((u - 1) & 1));
+                    mbar_expect(sfull + s, kSlotBytes);
+                    tma_row(slots + s * kSlotBytes, map, x0 / 8 - 1, rbase + q, sfull + s);
+                }
             }
         }
     } else if (warp == 1) {  // ---- MMA issuer (whole warp, one elected lane issues)
         const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
-        mbar_wait(wbar, 0);
-        if (lane == 0) K5T(1);
         [[maybe_unused]] long long st_full = 0, st_acc = 0, st_issue = 0, st_commit = 0, st_wrap = 0;
-        for (int r = y0 - 1; r <= y1; ++r) {
-            const int q = r - rbase, s = q % kSlots;
-            // accumulators fed by this halo row: output rows r-1 (W_dy2), r (W_dy1), r+1 (W_dy0)
-            const bool v0 = r - 1 >= y0, v1 = r >= y0 && r < y1, v2 = r + 1 < y1;
-#ifdef K5_TRACE
-            const bool st4 = lane == 0 && q == 4;
-            if (st4) K5T(23);
-#endif
-            if (v2 && q >= kRollAcc) {  // row r+1 starts in slot q mod 8: drained of output row r+1-8?
-                K5ACC(st_acc, mbar_wait(aempty + (q % kRollAcc), (uint32_t)((q / kRollAcc - 1) & 1)))
-            }
-            K5ACC(st_full, mbar_wait(sfull + s, (uint32_t)((q / kSlots) & 1)))
-            if (lane == 0 && q == 0) K5T(31);
-#ifdef K5_TRACE
-            if (st4) K5T(24);
-#endif
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#ifdef K5_TRACE
-            if (st4) K5T(25);
-#endif
-            const uint32_t abase = sl_base + s * kSlotBytes + kHaloOff * 16;
-            const uint64_t a0 = sdesc(abase, kHaloX * 16, 128);
-            const int s0 = (q + kRollAcc - 2) % kRollAcc;  // slot of output row r-1; r: s0+1, r+1: s0+2 (mod 8)
-            // B = [W_dy2 | W_dy1 | W_dy0] from block k on; accumulator of block k in slot (s0 + k) mod 8
-            auto bd = [&](int k) { return sdesc(sw_base + k * kC * 16, kW2Icg, 128); };
-            auto dc = [&](int k) { return tmem + (uint32_t)(((s0 + k) % kRollAcc) * 64); };
-            if (v0 && v1 && v2) {
-                if (s0 + 2 < kRollAcc) {
-#ifdef K5_TRACE
-                    if (st4) K5T(26);
-#endif
-                    K5ACC(st_issue, umma_row13(dc(0), a0, bd(0)))
-#ifdef K5_TRACE
-                    if (st4) K5T(27);
-#endif
-                } else if (s0 + 1 < kRollAcc) {  // slots 6, 7 | 0
-                    K5ACC(st_wrap, umma_row_wrap(a0, dc(0), bd(0), kIdesc128, dc(2), bd(2), kIdesc, kIdesc, 0u, 0u, 0ull, 0u))
-                } else {  // slots 7 | 0, 1: rows r, r+1 share all but the first UMMA (row r+1's overwrites)
-                    K5ACC(st_wrap, umma_row_wrap(a0, dc(0), bd(0), kIdesc, dc(1), bd(1), kIdesc, kIdesc128, 1u, dc(2), bd(2), 1u))
+        for (int l = 0; l < L; ++l) {
+            mbar_wait(wbar, (uint32_t)(l & 1));
+            if (lane == 0 && l == 0) K5T(1);
+            for (int q = 0; q < nq; ++q) {
+                const int r = rbase + q;
+                const int Q = l * nq + q, s = Q % kSlots;
+                // accumulators fed by this halo row: output rows r-1 (W_dy2), r (W_dy1), r+1 (W_dy0); output
+                // row i of layer l has the running index I = l nrows + i and lives in slot I mod 8
+                const bool v0 = r - 1 >= y0, v1 = r >= y0 && r < y1, v2 = r + 1 < y1;
+                const int I2 = l * nrows + q;  // running index of output row r + 1
+                if (v2 && I2 >= kRollAcc) {    // its slot: drained of the row that had it before?
+                    K5ACC(st_acc, mbar_wait(aempty + (I2 % kRollAcc), (uint32_t)((I2 / kRollAcc - 1) & 1)))
                 }
-            } else if (v1 && v2 && !v0 && (s0 + 1) % kRollAcc + 1 < kRollAcc) {  // the CTA's first image row
-                umma_e(dc(1), a0, bd(1), kIdesc, 1u);
-                umma_e(dc(2), a0, bd(2), kIdesc, 0u);
-                umma_row11(dc(1), a0, bd(1), kIdesc128);
-            } else if (v0 && v1 && !v2 && s0 + 1 < kRollAcc) {  // the CTA's last image row
-                umma_row12(dc(0), a0, bd(0), kIdesc128, 1u);
-            } else {  // top and bottom halo rows, short CTAs: one N = 64 run per accumulator
-                if (v0) umma_row12(dc(0), a0, bd(0), kIdesc, 1u);
-                if (v1) umma_row12(dc(1), a0, bd(1), kIdesc, 1u);
-                if (v2) umma_row12(dc(2), a0, bd(2), kIdesc, 0u);
+                K5ACC(st_full, mbar_wait(sfull + s, (uint32_t)((Q / kSlots) & 1)))
+                if (lane == 0 && Q == 0) K5T(31);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t abase = sl_base + s * kSlotBytes + kHaloOff * 16;
+                const uint64_t a0 = sdesc(abase, kHaloX * 16, 128);
+                const int s0 = (I2 + 2 * kRollAcc - 2) % kRollAcc;  // slot of output row r-1; r: s0+1, r+1: s0+2 (mod 8)
+                // B = [W_dy2 | W_dy1 | W_dy0] from block k on; accumulator of block k in slot (s0 + k) mod 8
+                auto bd = [&](int k) { return sdesc(sw_base + k * kC * 16, kW2Icg, 128); };
+                auto dc = [&](int k) { return tmem + (uint32_t)(((s0 + k) % kRollAcc) * 64); };
+                if (v0 && v1 && v2) {
+                    if (s0 + 2 < kRollAcc) {
+                        K5ACC(st_issue, umma_row13(dc(0), a0, bd(0)))
+                    } else if (s0 + 1 < kRollAcc) {  // slots 6, 7 | 0
+                        K5ACC(st_wrap, umma_row_wrap(a0, dc(0), bd(0), kIdesc128, dc(2), bd(2), kIdesc, kIdesc, 0u, 0u, 0ull, 0u))
+                    } else {  // slots 7 | 0, 1: rows r, r+1 share all but the first UMMA (row r+1's overwrites)
+                        K5ACC(st_wrap, umma_row_wrap(a0, dc(0), bd(0), kIdesc, dc(1), bd(1), kIdesc, kIdesc128, 1u, dc(2), bd(2), 1u))
+                    }
+                } else if (v1 && v2 && !v0 && (s0 + 1) % kRollAcc + 1 < kRollAcc) {  // the CTA's first image row
+                    umma_e(dc(1), a0, bd(1), kIdesc, 1u);
+                    umma_e(dc(2), a0, bd(2), kIdesc, 0u);
+                    umma_row11(dc(1), a0, bd(1), kIdesc128);
+                } else if (v0 && v1 && !v2 && s0 + 1 < kRollAcc) {  // the CTA's last image row
+                    umma_row12(dc(0), a0, bd(0), kIdesc128, 1u);
+                } else {  // top and bottom halo rows, short CTAs, wrapping edge rows: one N = 64 run per accumulator
+                    if (v0) umma_row12(dc(0), a0, bd(0), kIdesc, 1u);
+                    if (v1) umma_row12(dc(1), a0, bd(1), kIdesc, 1u);
+                    if (v2) umma_row12(dc(2), a0, bd(2), kIdesc, 0u);
+                }
+                K5ACC(st_commit, umma_commit_e(rowdone + s))
+                if (lane == 0 && Q < 16) K5T(2 + Q);
+                if (lane == 0 && Q < 14) K5V(50 + Q, st_full + st_acc);
             }
-            K5ACC(st_commit, umma_commit_e(rowdone + s))
-#ifdef K5_TRACE
-            if (st4) K5T(28);
-#endif
-            if (lane == 0 && q < 16) K5T(2 + q);
-            if (lane == 0 && q < 14) K5V(50 + q, st_full + st_acc);
         }
         if (lane == 0) {
             K5V(18, st_full);
@@ -767,43 +804,56 @@ __global__ void __launch_bounds__(192, 1) k_conv64_roll(const __grid_constant__ 
         }
     } else {  // ---- epilogue warps 2..5: output row y is complete once halo row y+1 is done
         const int quad = warp & 3;
-        for (int y = y0; y < y1; ++y) {
-            const int q = y + 1 - rbase, a = (y - y0) % kRollAcc;
-            mbar_wait(rowdone + q % kSlots, (uint32_t)((q / kSlots) & 1));
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a * 64);
-            uint32_t r[64];
-            LD16(base + 0, (r + 0));
-            LD16(base + 16, (r + 16));
-            LD16(base + 32, (r + 32));
-            LD16(base + 48, (r + 48));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (warp == 2 && lane == 0 && y - y0 < 14) K5T(32 + y - y0);
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(aempty + a)) : "memory");
-            const int px = x0 + quad * 32 + lane;
-            if (px < W) {
-                uint4* dst = reinterpret_cast<uint4*>(out) + ((size_t)y * Wp + px);
-                const size_t gstride = (size_t)H * Wp;
+        for (int l = 0; l < L; ++l) {
+            __nv_bfloat16* out = (l & 1) ? out1 : out0;
+            for (int y = y0; y < y1; ++y) {
+                const int Q = l * nq + (y + 1 - rbase), a = (l * nrows + (y - y0)) % kRollAcc;
+                mbar_wait(rowdone + Q % kSlots, (uint32_t)((Q / kSlots) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a * 64);
+                uint32_t r[64];
+                LD16(base + 0, (r + 0));
+                LD16(base + 16, (r + 16));
+                LD16(base + 32, (r + 32));
+                LD16(base + 48, (r + 48));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (warp == 2 && lane == 0 && l == 0 && y - y0 < 14) K5T(32 + y - y0);
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(aempty + a)) : "memory");
+                const int px = x0 + quad * 32 + lane;
+                if (px < W) {
+                    uint4* dst = reinterpret_cast<uint4*>(out) + ((size_t)y * Wp + px);
+                    const size_t gstride = (size_t)H * Wp;
 #pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    uint32_t pk[4];
+                    for (int g = 0; g < 8; ++g) {
+                        uint32_t pk[4];
 #pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        const float lo = fmaxf(__uint_as_float(r[8 * g + 2 * h]), 0.f);
-                        const float hi = fmaxf(__uint_as_float(r[8 * g + 2 * h + 1]), 0.f);
-                        const __nv_bfloat162 v2 = __floats2bfloat162_rn(lo, hi);
-                        pk[h] = *reinterpret_cast<const uint32_t*>(&v2);
+                        for (int h = 0; h < 4; ++h) {
+                            const float lo = fmaxf(__uint_as_float(r[8 * g + 2 * h]), 0.f);
+                            const float hi = fmaxf(__uint_as_float(r[8 * g + 2 * h + 1]), 0.f);
+                            const __nv_bfloat162 v2 = __floats2bfloat162_rn(lo, hi);
+                            pk[h] = *reinterpret_cast<const uint32_t*>(&v2);
+                        }
+                        dst[g * gstride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                     }
-                    dst[g * gstride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
+            }
+            if (kSeq && l + 1 < L) {  // this CTA's share of layer l is stored: fence, then one arrival
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (tid == 64) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(sync_ctr) : "memory");
             }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (tid == 0) K5V(49, k5_gtime());
+#ifdef K5_TRACE
+    if (tid == 0) {
+        K5V(49, k5_gtime());
+        g_k5_life[life_idx][3] = k5_gtime();
+    }
+#endif
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kRollAcc * 64) : "memory");
 }
@@ -1308,6 +1358,17 @@ CUtensorMap make_act_map(void* base, int H, int Wp)
 
 #ifdef K5_TRACE
 void k5_trace_copy(long long* host) { cudaMemcpyFromSymbol(host, g_k5_trace, sizeof(g_k5_trace)); }
+unsigned k5_life_copy(long long* host, bool reset)
+{
+    unsigned n = 0;
+    cudaMemcpyFromSymbol(&n, g_k5_life_n, sizeof(n));
+    cudaMemcpyFromSymbol(host, g_k5_life, sizeof(g_k5_life));
+    if (reset) {
+        const unsigned z = 0;
+        cudaMemcpyToSymbol(g_k5_life_n, &z, sizeof(z));
+    }
+    return n;
+}
 #endif
 #ifdef K5SEQ_TRACE
 extern "C" int mace_k5seq_trace(unsigned long long* host)
@@ -1394,12 +1455,14 @@ void Cnn::ensure(int h, int w)
     CKC(cudaFuncSetAttribute(k_conv64_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv64_tc2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv64_tc2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    CKC(cudaFuncSetAttribute(k_conv64_roll, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    CKC(cudaFuncSetAttribute(k_conv64_roll<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    CKC(cudaFuncSetAttribute(k_conv64_roll<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv_last_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kLSmem));
     CKC(cudaFuncSetAttribute(k_conv64_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     flags.alloc(1024);
     CKC(cudaMemset(flags.p, 0, 1024 * sizeof(int)));
     epoch = 0;
+    roll_epoch = 0;
 }
 
 // one 64 -> 64 layer (2..16) from map -> dst on stream s with the current launch geometry
@@ -1421,8 +1484,8 @@ void Cnn::launch_mid(int l, const CUtensorMap& m, __nv_bfloat16* dst, cudaStream
     cfg.attrs = pdl;
     cfg.numAttrs = pdl_on ? 1 : 0;
     if (rows_unit == 0)
-        CKC(cudaLaunchKernelEx(&cfg, k_conv64_roll, m, (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC), dst,
-                               H, W, Wp, per));
+        CKC(cudaLaunchKernelEx(&cfg, k_conv64_roll<false>, m, m, (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC),
+                               dst, dst, H, W, Wp, per, 1, (unsigned*)nullptr, 0u));
     else if (rows_unit == 3)
         CKC(cudaLaunchKernelEx(&cfg, k_conv64_tc2<3>, m, (const __nv_bfloat16*)(w_mid2.p + (size_t)l * 9 * kC * kC),
                                dst, H, W, Wp, per));
@@ -1466,7 +1529,27 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     pdl[0].val.programmaticStreamSerializationAllowed = 1;
-    if (seq && rows_unit == 2) {  // the 15 middle layers as one persistent cooperative launch
+    if (seq && rows_unit == 0) {  // rolling accumulators, the 15 middle layers as one cooperative launch
+        const int strips = (W + kTileX - 1) / kTileX;
+        const int ctas_y = std::max(1, num_sms / strips);
+        const int per = (H + ctas_y - 1) / ctas_y;
+        const int ctas = strips * ((H + per - 1) / per);
+        cudaLaunchAttribute coop[1];
+        coop[0].id = cudaLaunchAttributeCooperative;
+        coop[0].val.cooperative = 1;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(ctas);
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = kSmem;
+        cfg.stream = s;
+        cfg.attrs = coop;
+        cfg.numAttrs = 1;
+        // arrivals so far on the grid-wide counter (flags[1023]): 14 per CTA and denoise at this geometry
+        const unsigned base = (unsigned)roll_epoch * 14u * (unsigned)ctas;
+        ++roll_epoch;
+        CKC(cudaLaunchKernelEx(&cfg, k_conv64_roll<true>, map0, map1, (const __nv_bfloat16*)w_mid2.p, act1.p, act0.p, H,
+                               W, Wp, per, 15, (unsigned*)(flags.p + 1023), base));
+    } else if (seq && rows_unit == 2) {  // the 15 middle layers as one persistent cooperative launch
         const int strips = (W + kTileX - 1) / kTileX;
         const int ctas_y = std::max(1, num_sms / strips);
         const int per = (H + ctas_y - 1) / ctas_y;

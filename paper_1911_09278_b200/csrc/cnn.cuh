@@ -48,6 +48,7 @@ struct Cnn {
     bool seq = false;                    // layers 2..16 in one persistent launch (MACE_K5_SEQ=1; slower)
     DevBuf<int> flags;                   // per-CTA layer-done flags of k_conv64_seq
     int epoch = 0;                       // flag epoch (one per persistent launch)
+    int roll_epoch = 0;                  // persistent rolling-accumulator launches so far at this geometry
     DevBuf<__nv_bfloat16> act0, act1;    // channel-blocked [8 groups][H][Wp][8 ch]
     CUtensorMap map0{}, map1{};
     // weights: 17 layers in PyTorch OIHW order, bf16 bits, concatenated

@@ -232,3 +232,12 @@ def test_cnn_launch_variants_are_bit_identical(n_side, monkeypatch):
         assert rel(units[r], ref) < 4e-2, (r, rel(units[r], ref))
     assert rel(units["2"], units["3"]) < 4e-2 and rel(units["1"], units["3"]) < 4e-2
     assert rel(units["0"], units["3"]) < 4e-2
+    # the rolling-accumulator layers as one cooperative launch with a grid-wide counter between layers
+    # (MACE_K5_SEQ=1 with MACE_K5_ROWS=0): the same UMMAs in the same order, so bit-identical, twice in a
+    # row (the counter runs on from denoise to denoise)
+    monkeypatch.setenv("MACE_K5_ROWS", "0")
+    monkeypatch.setenv("MACE_K5_SEQ", "0")
+    one = CnnDenoiser(n_side, weights=w)(x)
+    monkeypatch.setenv("MACE_K5_SEQ", "1")
+    den = CnnDenoiser(n_side, weights=w)
+    assert np.array_equal(den(x), one) and np.array_equal(den(x), one)

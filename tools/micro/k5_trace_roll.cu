@@ -1,11 +1,12 @@
 // K5 rolling-accumulator layer timeline (k_conv64_roll): cnn.cu built with -DK5_TRACE.
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <vector>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include "../../paper_1911_09278_b200/csrc/cnn.cuh"
-namespace mace { void k5_trace_copy(long long* host); }
+namespace mace { void k5_trace_copy(long long* host); unsigned k5_life_copy(long long* host, bool reset); }
 static long long med(std::vector<long long> v)
 {
     std::sort(v.begin(), v.end());
@@ -57,6 +58,29 @@ int main()
     printf("row q=4 (cycles from row 3's commit stamp): loop top %lld, halo landed %lld, fence %lld, descriptors %lld, issued %lld, committed %lld\n",
            col(23, 5), col(24, 5), col(25, 5), col(26, 5), col(27, 5), col(28, 5));
     printf("median CTA life %lld ns\n", col(49, 48));
+    {   // one denoise alone: per-SM chains of CTA lives (globaltimer)
+        static long long life[4096][4];
+        mace::k5_life_copy(&life[0][0], true);
+        cnn.apply(x, y, n, n, 0, 148, nullptr);
+        cudaDeviceSynchronize();
+        const unsigned cnt = mace::k5_life_copy(&life[0][0], false);
+        std::vector<std::vector<std::array<long long, 3>>> per(256);
+        for (unsigned i = 0; i < cnt && i < 4096; ++i) per[life[i][0]].push_back({life[i][1], life[i][2], life[i][3]});
+        std::vector<long long> gaps, lifes, waits, periods;
+        for (auto& v : per) {
+            std::sort(v.begin(), v.end());
+            for (size_t i = 0; i + 1 < v.size(); ++i) {
+                gaps.push_back(v[i + 1][0] - v[i][2]);
+                periods.push_back(v[i + 1][0] - v[i][0]);
+            }
+            for (auto& r : v) {
+                lifes.push_back(r[2] - r[0]);
+                waits.push_back(r[1] - r[0]);
+            }
+        }
+        printf("%u CTA records: median life %lld ns, start -> gdc wait passed %lld ns, end -> next start on the SM %lld ns, start -> next start %lld ns\n",
+               cnt, med(lifes), med(waits), med(gaps), med(periods));
+    }
 #endif
     return 0;
 }
