@@ -55,8 +55,6 @@ int main()
     for (int q = 0; q < 14; ++q) printf(" %lld", col(50 + q, -1));
     printf("\nissuer totals: halo wait %lld, accumulator wait %lld, in issue (fast rows) %lld, in commits %lld, in issue (wrap rows) %lld\n", col(18, -1),
            col(19, -1), col(20, -1), col(21, -1), col(22, -1));
-    printf("row q=4 (cycles from row 3's commit stamp): loop top %lld, halo landed %lld, fence %lld, descriptors %lld, issued %lld, committed %lld\n",
-           col(23, 5), col(24, 5), col(25, 5), col(26, 5), col(27, 5), col(28, 5));
     printf("median CTA life %lld ns\n", col(49, 48));
     {   // one denoise alone: per-SM chains of CTA lives (globaltimer)
         static long long life[4096][4];
