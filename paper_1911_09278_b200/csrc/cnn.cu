@@ -1219,6 +1219,165 @@ __global__ void __launch_bounds__(192, 1) k_conv_last_tc(const __grid_constant__
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * kLOC) : "memory");
 }
 
+// Layer 17 with rolling accumulators (k_conv_last_roll, the default): k_conv_last_tc issues 36 N = 16 UMMAs
+// per output row one by one and is bound by the issue path (~58 cycles each; 19.7 us per 512^2 layer under
+// ncu against 17.7 us for a 64 -> 64 layer with 64 times the math).  Here, as in k_conv64_roll, every halo
+// row is one run of UMMAs against [W_dy2 | W_dy1 | W_dy0] (16 padded output channels each, N = 48) into
+// the 16-column accumulator slots of output rows r-1, r, r+1: 13 UMMAs per row instead of 36.
+// Weights [dx 3][ic-group 8][dy2 | dy1 | dy0 x 16 oc][8 ic] bf16 (18 KB, oc 1..15 of each block zero).
+constexpr uint32_t kIdescL32 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+constexpr uint32_t kIdescL48 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(48 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+constexpr int kLRIcg = 3 * kLOC * 16;  // 768 B per ic-group: 48 output-channel rows of 8 ic
+constexpr int kLRDx = 8 * kLRIcg;      // 6,144 B per dx
+// (A, B) descriptor steps of the 11 (dx, K-step) UMMAs after the first: A as in umma_row12, B dx x 6,144 + 2 j x 768 (>> 4)
+#define K5_STEPS_LAST(X) X(288, 96) X(576, 192) X(864, 288) X(1, 384) X(289, 480) X(577, 576) X(865, 672) X(2, 768) \
+    X(290, 864) X(578, 960) X(866, 1056)
+#define K5_STEP3(ao, bo) "add.s64 a, %1, " #ao ";\nadd.s64 b, %2, " #bo ";\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+#define K5_STEP5(ao, bo) "add.s64 a, %1, " #ao ";\nadd.s64 b, %2, " #bo ";\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n"
+__device__ __forceinline__ void umma_last12(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc, uint32_t accumulate)
+{
+    static_assert(kHaloX == 144 && kLRDx == 6144 && kLRIcg == 768, "offsets are hard-coded");
+    asm volatile(
+        "{\n.reg .pred e, p, t;\n.reg .b64 a, b;\n"
+        "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\nsetp.eq.b32 t, 1, 1;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        K5_STEPS_LAST(K5_STEP3)
+        "}\n"
+        ::"r"(d_tmem), "l"(a0), "l"(b0), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_last11(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc)
+{
+    asm volatile(
+        "{\n.reg .pred e, t;\n.reg .b64 a, b;\n"
+        "elect.sync _|e, 0xffffffff;\nsetp.eq.b32 t, 1, 1;\n"
+        K5_STEPS_LAST(K5_STEP3)
+        "}\n"
+        ::"r"(d_tmem), "l"(a0), "l"(b0), "r"(idesc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_last13(uint32_t d_tmem, uint64_t a0, uint64_t b0)
+{
+    asm volatile(
+        "{\n.reg .pred e, f, t;\n.reg .b64 a, b;\n.reg .b32 d2;\n"
+        "elect.sync _|e, 0xffffffff;\nsetp.eq.b32 t, 1, 1;\nsetp.ne.b32 f, 1, 1;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, t;\n"  // rows r-1, r: += A [W_dy2 | W_dy1]
+        "add.u32 d2, %0, 32;\nadd.s64 b, %2, 32;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [d2], %1, b, %4, f;\n"   // row r+1: = A W_dy0
+        K5_STEPS_LAST(K5_STEP5)
+        "}\n"
+        ::"r"(d_tmem), "l"(a0), "l"(b0), "r"(kIdescL32), "r"(kIdescL), "r"(kIdescL48)
+        : "memory");
+}
+#undef K5_STEP3
+#undef K5_STEP5
+
+__global__ void __launch_bounds__(192, 1) k_conv_last_roll(const __grid_constant__ CUtensorMap amap,
+                                                           const __nv_bfloat16* __restrict__ wts,
+                                                           const float* __restrict__ x, float* out, int H, int W,
+                                                           int rows_per_cta)
+{
+    extern __shared__ __align__(1024) unsigned char sm[];
+    unsigned char* sw = sm;
+    unsigned char* slots = sm + kLWBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + kSlots * kSlotBytes);
+    uint64_t* wbar = bars;
+    uint64_t* sfull = bars + 1;             // [kSlots] halo row landed
+    uint64_t* rowdone = sfull + kSlots;     // [kSlots] the halo row's UMMAs have completed
+    uint64_t* aempty = rowdone + kSlots;    // [kRollAcc] accumulator slot drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kRollAcc);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int strips = (W + kTileX - 1) / kTileX;
+    const int strip = blockIdx.x % strips;
+    const int x0 = strip * kTileX;
+    const int y0 = (blockIdx.x / strips) * rows_per_cta;
+    const int y1 = min(H, y0 + rows_per_cta);
+    if (y0 >= H) return;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(tmem_slot)),
+                     "n"(kRollAcc * kLOC)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 32) {
+        mbar_init(wbar, 1);
+        for (int i = 0; i < kSlots; ++i) {
+            mbar_init(sfull + i, 1);
+            mbar_init(rowdone + i, 1);
+        }
+        for (int i = 0; i < kRollAcc; ++i) mbar_init(aempty + i, 4);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const int rbase = y0 - 1;
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            mbar_expect(wbar, kLWBytes);
+            bulk_copy(sw, wts, kLWBytes, wbar);
+            asm volatile("griddepcontrol.wait;" ::: "memory");  // the last 64-channel layer
+            for (int r = y0 - 1; r <= y1; ++r) {
+                const int q = r - rbase, s = q % kSlots, u = q / kSlots;
+                if (u >= 1) mbar_wait(rowdone + s, (uint32_t)((u - 1) & 1));
+                mbar_expect(sfull + s, kSlotBytes);
+                tma_row(slots + s * kSlotBytes, &amap, x0 / 8 - 1, r, sfull + s);
+            }
+        }
+    } else if (warp == 1) {  // ---- MMA issuer (whole warp, one elected lane issues)
+        const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
+        mbar_wait(wbar, 0);
+        for (int r = y0 - 1; r <= y1; ++r) {
+            const int q = r - rbase, s = q % kSlots;
+            const bool v0 = r - 1 >= y0, v1 = r >= y0 && r < y1, v2 = r + 1 < y1;
+            if (v2 && q >= kRollAcc) mbar_wait(aempty + (q % kRollAcc), (uint32_t)((q / kRollAcc - 1) & 1));
+            mbar_wait(sfull + s, (uint32_t)((q / kSlots) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t a0 = sdesc(sl_base + s * kSlotBytes + kHaloOff * 16, kHaloX * 16, 128);
+            const int s0 = (q + 2 * kRollAcc - 2) % kRollAcc;  // slot of output row r-1
+            auto bd = [&](int k) { return sdesc(sw_base + k * kLOC * 16, kLRIcg, 128); };
+            auto dc = [&](int k) { return tmem + (uint32_t)(((s0 + k) % kRollAcc) * kLOC); };
+            if (v0 && v1 && v2 && s0 + 2 < kRollAcc) {
+                umma_last13(dc(0), a0, bd(0));
+            } else if (v0 && v1 && v2 && s0 + 1 < kRollAcc) {  // slots 6, 7 | 0
+                umma_last12(dc(0), a0, bd(0), kIdescL32, 1u);
+                umma_last12(dc(2), a0, bd(2), kIdescL, 0u);
+            } else if (v0 && v1 && !v2 && s0 + 1 < kRollAcc) {  // the CTA's last image row
+                umma_last12(dc(0), a0, bd(0), kIdescL32, 1u);
+            } else {  // first rows, top and bottom halo rows, short CTAs, the other wrapping row
+                if (v0) umma_last12(dc(0), a0, bd(0), kIdescL, 1u);
+                if (v1) umma_last12(dc(1), a0, bd(1), kIdescL, 1u);
+                if (v2) umma_last12(dc(2), a0, bd(2), kIdescL, 0u);
+            }
+            umma_commit_e(rowdone + s);
+        }
+    } else {  // ---- epilogue warps 2..5: column 0 of the row's accumulator slot -> out = x - net(x)
+        const int quad = warp & 3;
+        for (int y = y0; y < y1; ++y) {
+            const int q = y + 1 - rbase, a = (y - y0) % kRollAcc;
+            mbar_wait(rowdone + q % kSlots, (uint32_t)((q / kSlots) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a * kLOC);
+            uint32_t v;
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(base));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(aempty + a)) : "memory");
+            const int px = x0 + quad * 32 + lane;
+            if (px < W) {
+                const size_t p = (size_t)y * W + px;
+                out[p] = x[p] - __uint_as_float(v);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kRollAcc * kLOC) : "memory");
+}
+
 // layer 1: x (fp32, rounded to bf16) -> 64 ch, ReLU, bf16 blocked [8][H][W][8].  w1: [9 taps][64 oc] fp32
 // packed fp32 FMA (sm_100 FFMA2): {a.x * b.x + c.x, a.y * b.y + c.y}
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c)
@@ -1401,8 +1560,19 @@ void Cnn::set_weights(const uint16_t* bf16, int layers, int channels)
         w_last_tc.alloc(wt.size());
         CKC(cudaMemcpy(w_last_tc.p, wt.data(), wt.size() * 2, cudaMemcpyHostToDevice));
     }
-    const char* el = std::getenv("MACE_K5_LAST");  // "fma": layer 17 on the CUDA cores
+    // ... and for k_conv_last_roll: [dx][ic-group][dy2 | dy1 | dy0 x 16 oc][8 ic], output channel 0 of each block
+    {
+        std::vector<uint16_t> wt((size_t)kLWBytes / 2, 0);
+        for (int ic = 0; ic < kC; ++ic)
+            for (int dy = 0; dy < 3; ++dy)
+                for (int dx = 0; dx < 3; ++dx)
+                    wt[(size_t)dx * kLRDx / 2 + (ic / 8) * kLRIcg / 2 + (2 - dy) * kLOC * 8 + ic % 8] = wl[ic * 9 + dy * 3 + dx];
+        w_last_roll.alloc(wt.size());
+        CKC(cudaMemcpy(w_last_roll.p, wt.data(), wt.size() * 2, cudaMemcpyHostToDevice));
+    }
+    const char* el = std::getenv("MACE_K5_LAST");  // "fma": layer 17 on the CUDA cores; "tc": one UMMA run per output row
     last_tc = !(el && std::strcmp(el, "fma") == 0);
+    last_roll = !(el && (std::strcmp(el, "fma") == 0 || std::strcmp(el, "tc") == 0));
     const char* es = std::getenv("MACE_K5_SEQ");  // "1": the 15 middle layers as one persistent launch
     seq = es && std::strcmp(es, "1") == 0;
     // middle layers: [layer][tap][ic-group][oc][8 ic]
@@ -1458,6 +1628,7 @@ void Cnn::ensure(int h, int w)
     CKC(cudaFuncSetAttribute(k_conv64_roll<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv64_roll<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv_last_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kLSmem));
+    CKC(cudaFuncSetAttribute(k_conv_last_roll, cudaFuncAttributeMaxDynamicSharedMemorySize, kLSmem));
     CKC(cudaFuncSetAttribute(k_conv64_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     flags.alloc(1024);
     CKC(cudaMemset(flags.p, 0, 1024 * sizeof(int)));
@@ -1584,7 +1755,10 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
         cfg.stream = s;
         cfg.attrs = pdl;
         cfg.numAttrs = 1;
-        CKC(cudaLaunchKernelEx(&cfg, k_conv_last_tc, map1, (const __nv_bfloat16*)w_last_tc.p, x, out, H, W, per));
+        if (last_roll)
+            CKC(cudaLaunchKernelEx(&cfg, k_conv_last_roll, map1, (const __nv_bfloat16*)w_last_roll.p, x, out, H, W, per));
+        else
+            CKC(cudaLaunchKernelEx(&cfg, k_conv_last_tc, map1, (const __nv_bfloat16*)w_last_tc.p, x, out, H, W, per));
     } else {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((W + kLastT - 1) / kLastT, (H + kLastT - 1) / kLastT);

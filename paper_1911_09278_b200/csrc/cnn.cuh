@@ -45,6 +45,8 @@ struct Cnn {
     int rows_unit = 2;                   // output rows per MMA unit (k_conv64_tc2<2|3>; 1 = k_conv64_tc), MACE_K5_ROWS
     DevBuf<__nv_bfloat16> w_last_tc;     // layer 17 for k_conv_last_tc: [9 taps][8 ic-groups][16 oc][8 ic]
     bool last_tc = true;                 // layer 17 on the tensor cores (MACE_K5_LAST=fma: CUDA cores)
+    DevBuf<__nv_bfloat16> w_last_roll;   // layer 17 for k_conv_last_roll: [dx][ic-group][dy2 | dy1 | dy0 x 16 oc][8 ic]
+    bool last_roll = true;               // ... with rolling accumulators (MACE_K5_LAST=tc: one UMMA run per output row)
     bool seq = false;                    // layers 2..16 in one persistent launch (MACE_K5_SEQ=1; slower)
     DevBuf<int> flags;                   // per-CTA layer-done flags of k_conv64_seq
     int epoch = 0;                       // flag epoch (one per persistent launch)

@@ -217,6 +217,8 @@ def test_cnn_launch_variants_are_bit_identical(n_side, monkeypatch):
     assert np.array_equal(outs[("1", "fma")], outs[("0", "fma")])
     r_tc, r_fma = _net(x, outs[("0", "tc")]), _net(x, outs[("0", "fma")])
     assert rel(r_tc, r_fma) < 1e-5
+    monkeypatch.setenv("MACE_K5_LAST", "roll")  # layer 17 with rolling accumulators (k_conv_last_roll, the default)
+    assert rel(_net(x, CnnDenoiser(n_side, weights=w)(x)), r_tc) < 1e-5
     # row units per MMA batch (MACE_K5_ROWS; 0 = one halo row at a time into rolling accumulators):
     # each output row receives the same UMMAs in another
     # order (fp32 accumulation), and one-ulp bf16 differences compound over 17 random unit-scale
