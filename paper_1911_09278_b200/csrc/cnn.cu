@@ -858,6 +858,241 @@ __global__ void __launch_bounds__(192, 1) k_conv64_roll(const __grid_constant__ 
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kRollAcc * 64) : "memory");
 }
 
+// Pipelined persistent variant (k_conv64_pipe, MACE_K5_SEQ=2): all middle layers in one cooperative launch
+// WITHOUT a grid-wide wait between layers.  In odd layers every CTA's row run is shifted up by half a run
+// (run j owns rows [per j - per/2, per (j+1) - per/2); the first run is half as long, the last takes the rest),
+// and every CTA sweeps its run top to bottom.  The rows a CTA needs first in layer l+1 (and their neighbours in
+// the adjacent strips) were then written in the MIDDLE of layer l, half a layer (~4 us) earlier, and the rows
+// written last in layer l are needed last in layer l+1: no CTA ever waits for a row that has only just been
+// stored, so the layers run back to back.  Read-after-write: every epilogue warp publishes, after each output
+// row it has stored and fenced, its running row count in flags[cta][warp] (release); before the TMA producer
+// loads halo row r of layer l+1 it acquires the counts of the (up to three strips') owners of row r in layer l,
+// then orders the async-proxy read behind them (fence.proxy.async).  Write-after-read on the ping-pong buffers
+// follows from the same waits: row r of layer l+1 is stored after rows r-1..r+1 of layer l (strips s-1..s+1)
+// were complete, and computing those is what read the rows of the buffer that row r overwrites.
+struct RowRun {
+    int y0, y1;
+};
+__device__ __forceinline__ RowRun pipe_run(int j, int odd, int per, int nyc, int H)
+{
+    const int half = odd ? per / 2 : 0;
+    RowRun r;
+    r.y0 = max(0, per * j - half);
+    r.y1 = j == nyc - 1 ? H : per * (j + 1) - half;
+    return r;
+}
+__device__ __forceinline__ int pipe_owner(int row, int odd, int per, int nyc)
+{
+    return min(nyc - 1, (row + (odd ? per / 2 : 0)) / per);
+}
+// rows run j has completed before layer l (layers 0, 2, .. are even)
+__device__ __forceinline__ int pipe_cum(int j, int l, int per, int nyc, int H)
+{
+    const RowRun e = pipe_run(j, 0, per, nyc, H), o = pipe_run(j, 1, per, nyc, H);
+    return ((l + 1) / 2) * (e.y1 - e.y0) + (l / 2) * (o.y1 - o.y0);
+}
+
+__global__ void __launch_bounds__(192, 1) k_conv64_pipe(const __grid_constant__ CUtensorMap map0,
+                                                        const __grid_constant__ CUtensorMap map1,
+                                                        const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* out0,
+                                                        __nv_bfloat16* out1, int H, int W, int Wp, int per, int n_layers,
+                                                        unsigned* flags, unsigned flag_base)
+{
+    extern __shared__ __align__(1024) unsigned char sm[];
+    unsigned char* sw = sm;
+    unsigned char* slots = sm + kWBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + kSlots * kSlotBytes);
+    uint64_t* wbar = bars;
+    uint64_t* sfull = bars + 1;
+    // rowdone barriers in a ring of 16 (twice the halo ring): without a grid-wide wait the MMA issuer can be a layer
+    // boundary (two extra halo rows) ahead of the epilogue, so with 8 a waiter could miss a whole phase
+    constexpr int kRD = 16;
+    uint64_t* rowdone = sfull + kSlots;
+    uint64_t* aempty = rowdone + kRD;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kRollAcc);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int strips = (W + kTileX - 1) / kTileX;
+    const int strip = blockIdx.x % strips, jrun = blockIdx.x / strips;
+    const int nyc = gridDim.x / strips;
+    const int x0 = strip * kTileX;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(tmem_slot)),
+                     "n"(kRollAcc * 64)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 32) {
+        mbar_init(wbar, 1);
+        for (int i = 0; i < kSlots; ++i) mbar_init(sfull + i, 1);
+        for (int i = 0; i < kRD; ++i) mbar_init(rowdone + i, 1);
+        for (int i = 0; i < kRollAcc; ++i) mbar_init(aempty + i, 4);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {  // ---- TMA producer (whole warp: lanes 0..11 watch the owners' flags, lane 0 copies)
+        int Qb = 0;   // halo rows before this layer
+        // lane 4 t + w watches epilogue warp w of the owner in strip (strip - 1 + t)
+        const int ft = lane >> 2, fw = lane & 3, fstrip = strip - 1 + ft;
+        const bool watcher = lane < 12 && fstrip >= 0 && fstrip < strips;
+        unsigned seen = flag_base;  // last value read from the flag this lane watched (of whichever owner)
+        int seen_owner = -1;
+        for (int l = 0; l < n_layers; ++l) {
+            const RowRun rr = pipe_run(jrun, l & 1, per, nyc, H);
+            const int nq = rr.y1 - rr.y0 + 2;
+            if (lane == 0) {
+                if (l > 0) mbar_wait(rowdone + (Qb - 1) % kRD, (uint32_t)(((Qb - 1) / kRD) & 1));  // weights free
+                mbar_expect(wbar, kWBytes);
+                bulk_copy(sw, wts + (size_t)l * 9 * kC * kC, kWBytes, wbar);
+            }
+            const CUtensorMap* map = (l & 1) ? &map1 : &map0;
+            for (int q = 0; q < nq; ++q) {
+                const int r = rr.y0 - 1 + q;
+#ifdef K5P_NOPOLL  // (timing experiment)
+                if (false) {
+#else
+                if (l > 0 && r >= 0 && r < H) {  // row r of layer l - 1: stored and visible?
+#endif
+                    const int jo = pipe_owner(r, (l - 1) & 1, per, nyc);
+                    bool polled = false;
+                    if (watcher) {
+                        const RowRun ro = pipe_run(jo, (l - 1) & 1, per, nyc, H);
+                        const unsigned need = flag_base + (unsigned)(pipe_cum(jo, l - 1, per, nyc, H) + r - ro.y0 + 1);
+                        if (seen_owner != jo || (int)(seen - need) < 0) {
+                            const unsigned* f = flags + ((size_t)(jo * strips + fstrip) * 4 + fw);
+                            unsigned spins = 0;
+                            do {
+                                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(f) : "memory");
+                                if ((int)(seen - need) >= 0) break;
+                                if (++spins > (1u << 22)) {  // seconds: give up loudly rather than hang
+                                    g_k5_sync_timeout = 2u;
+                                    __trap();
+                                }
+                            } while (true);
+                            seen_owner = jo;
+                            polled = true;
+                        }
+                    }
+                    if (__any_sync(0xffffffffu, polled)) asm volatile("fence.proxy.async;" ::: "memory");
+                }
+                if (lane == 0) {
+                    const int Q = Qb + q, s = Q % kSlots;
+                    if (Q >= kSlots) mbar_wait(rowdone + (Q - kSlots) % kRD, (uint32_t)(((Q - kSlots) / kRD) & 1));
+                    mbar_expect(sfull + s, kSlotBytes);
+                    tma_row(slots + s * kSlotBytes, map, x0 / 8 - 1, r, sfull + s);
+                }
+                __syncwarp();
+            }
+            Qb += nq;
+        }
+    } else if (warp == 1) {  // ---- MMA issuer (whole warp, one elected lane issues)
+        const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
+        int Qb = 0, Ib = 0;
+        for (int l = 0; l < n_layers; ++l) {
+            const RowRun rr = pipe_run(jrun, l & 1, per, nyc, H);
+            const int y0 = rr.y0, y1 = rr.y1, nq = y1 - y0 + 2;
+            mbar_wait(wbar, (uint32_t)(l & 1));
+            for (int q = 0; q < nq; ++q) {
+                const int r = y0 - 1 + q;
+                const int Q = Qb + q, s = Q % kSlots;
+                const bool v0 = r - 1 >= y0, v1 = r >= y0 && r < y1, v2 = r + 1 < y1;
+                const int I2 = Ib + q;  // running index of output row r + 1
+                if (v2 && I2 >= kRollAcc) mbar_wait(aempty + (I2 % kRollAcc), (uint32_t)((I2 / kRollAcc - 1) & 1));
+                mbar_wait(sfull + s, (uint32_t)((Q / kSlots) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint64_t a0 = sdesc(sl_base + s * kSlotBytes + kHaloOff * 16, kHaloX * 16, 128);
+                const int s0 = (I2 + 2 * kRollAcc - 2) % kRollAcc;
+                auto bd = [&](int k) { return sdesc(sw_base + k * kC * 16, kW2Icg, 128); };
+                auto dc = [&](int k) { return tmem + (uint32_t)(((s0 + k) % kRollAcc) * 64); };
+                if (v0 && v1 && v2) {
+                    if (s0 + 2 < kRollAcc) {
+                        umma_row13(dc(0), a0, bd(0));
+                    } else if (s0 + 1 < kRollAcc) {
+                        umma_row_wrap(a0, dc(0), bd(0), kIdesc128, dc(2), bd(2), kIdesc, kIdesc, 0u, 0u, 0ull, 0u);
+                    } else {
+                        umma_row_wrap(a0, dc(0), bd(0), kIdesc, dc(1), bd(1), kIdesc, kIdesc128, 1u, dc(2), bd(2), 1u);
+                    }
+                } else if (v1 && v2 && !v0 && (s0 + 1) % kRollAcc + 1 < kRollAcc) {
+                    umma_e(dc(1), a0, bd(1), kIdesc, 1u);
+                    umma_e(dc(2), a0, bd(2), kIdesc, 0u);
+                    umma_row11(dc(1), a0, bd(1), kIdesc128);
+                } else if (v0 && v1 && !v2 && s0 + 1 < kRollAcc) {
+                    umma_row12(dc(0), a0, bd(0), kIdesc128, 1u);
+                } else {
+                    if (v0) umma_row12(dc(0), a0, bd(0), kIdesc, 1u);
+                    if (v1) umma_row12(dc(1), a0, bd(1), kIdesc, 1u);
+                    if (v2) umma_row12(dc(2), a0, bd(2), kIdesc, 0u);
+                }
+                umma_commit_e(rowdone + Q % kRD);
+            }
+            Qb += nq;
+            Ib += y1 - y0;
+        }
+    } else {  // ---- epilogue warps 2..5
+        const int quad = warp & 3;
+        unsigned* myflag = flags + ((size_t)blockIdx.x * 4 + quad);
+        int Qb = 0, Ib = 0;
+        for (int l = 0; l < n_layers; ++l) {
+            const RowRun rr = pipe_run(jrun, l & 1, per, nyc, H);
+            const int y0 = rr.y0, y1 = rr.y1;
+            __nv_bfloat16* out = (l & 1) ? out1 : out0;
+            for (int y = y0; y < y1; ++y) {
+                const int Q = Qb + (y - y0 + 2), a = (Ib + (y - y0)) % kRollAcc;
+                mbar_wait(rowdone + Q % kRD, (uint32_t)((Q / kRD) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a * 64);
+                uint32_t r[64];
+                LD16(base + 0, (r + 0));
+                LD16(base + 16, (r + 16));
+                LD16(base + 32, (r + 32));
+                LD16(base + 48, (r + 48));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(aempty + a)) : "memory");
+                const int px = x0 + quad * 32 + lane;
+                if (px < W) {
+                    uint4* dst = reinterpret_cast<uint4*>(out) + ((size_t)y * Wp + px);
+                    const size_t gstride = (size_t)H * Wp;
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        uint32_t pk[4];
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            const float lo = fmaxf(__uint_as_float(r[8 * g + 2 * h]), 0.f);
+                            const float hi = fmaxf(__uint_as_float(r[8 * g + 2 * h + 1]), 0.f);
+                            const __nv_bfloat162 v2 = __floats2bfloat162_rn(lo, hi);
+                            pk[h] = *reinterpret_cast<const uint32_t*>(&v2);
+                        }
+                        dst[g * gstride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    }
+                }
+                if (l + 1 < n_layers) {  // publish: this warp's part of rows .. y is stored and visible
+#ifndef K5P_NOFENCE  // (timing experiment)
+                    __threadfence();
+#endif
+                    __syncwarp();
+                    if (lane == 0) {
+                        const unsigned v = flag_base + (unsigned)(Ib + (y - y0) + 1);
+                        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(myflag), "r"(v) : "memory");
+                    }
+                }
+            }
+            Qb += y1 - y0 + 2;
+            Ib += y1 - y0;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kRollAcc * 64) : "memory");
+}
+
 // All 15 middle layers in ONE persistent launch (k_conv64_seq): every CTA keeps its (strip, row run)
 // for the whole stack, its TMEM allocation and barriers live across layers, and the halo-row ring,
 // accumulator pair ring and mbarrier phases simply continue from layer to layer.  Layer l reads
@@ -1575,6 +1810,7 @@ void Cnn::set_weights(const uint16_t* bf16, int layers, int channels)
     last_roll = !(el && (std::strcmp(el, "fma") == 0 || std::strcmp(el, "tc") == 0));
     const char* es = std::getenv("MACE_K5_SEQ");  // "1": the 15 middle layers as one persistent launch
     seq = es && std::strcmp(es, "1") == 0;
+    seq_pipe = es && std::strcmp(es, "2") == 0;  // "2": pipelined persistent launch (k_conv64_pipe)
     // middle layers: [layer][tap][ic-group][oc][8 ic]
     std::vector<uint16_t> wm(15 * (size_t)9 * kC * kC);
     for (int l = 0; l < 15; ++l) {
@@ -1627,6 +1863,7 @@ void Cnn::ensure(int h, int w)
     CKC(cudaFuncSetAttribute(k_conv64_tc2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv64_roll<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv64_roll<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    CKC(cudaFuncSetAttribute(k_conv64_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv_last_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kLSmem));
     CKC(cudaFuncSetAttribute(k_conv_last_roll, cudaFuncAttributeMaxDynamicSharedMemorySize, kLSmem));
     CKC(cudaFuncSetAttribute(k_conv64_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
@@ -1634,6 +1871,9 @@ void Cnn::ensure(int h, int w)
     CKC(cudaMemset(flags.p, 0, 1024 * sizeof(int)));
     epoch = 0;
     roll_epoch = 0;
+    pflags.alloc(4096);
+    CKC(cudaMemset(pflags.p, 0, 4096 * sizeof(int)));
+    pipe_epoch = 0;
 }
 
 // one 64 -> 64 layer (2..16) from map -> dst on stream s with the current launch geometry
@@ -1700,7 +1940,29 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     pdl[0].val.programmaticStreamSerializationAllowed = 1;
-    if (seq && rows_unit == 0) {  // rolling accumulators, the 15 middle layers as one cooperative launch
+    if (seq_pipe && rows_unit == 0) {  // rolling accumulators, pipelined layers (half-run shifts, row flags)
+        const int strips = (W + kTileX - 1) / kTileX;
+        const int ctas_y = std::max(1, num_sms / strips);
+        const int per = (H + ctas_y - 1) / ctas_y;
+        const int nyc = (H + per - 1) / per;
+        const int ctas = strips * nyc;
+        if (ctas * 4 > 4096) throw std::runtime_error("denoiser grid too large");
+        cudaLaunchAttribute coop[1];
+        coop[0].id = cudaLaunchAttributeCooperative;
+        coop[0].val.cooperative = 1;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(ctas);
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = kSmem;
+        cfg.stream = s;
+        cfg.attrs = coop;
+        cfg.numAttrs = 1;
+        // flag values run on from denoise to denoise: a run publishes at most 15 x (rows per run + per / 2) < 2^16
+        const unsigned base = (unsigned)pipe_epoch << 16;
+        ++pipe_epoch;
+        CKC(cudaLaunchKernelEx(&cfg, k_conv64_pipe, map0, map1, (const __nv_bfloat16*)w_mid2.p, act1.p, act0.p, H, W, Wp,
+                               per, 15, (unsigned*)pflags.p, base));
+    } else if (seq && rows_unit == 0) {  // rolling accumulators, the 15 middle layers as one cooperative launch
         const int strips = (W + kTileX - 1) / kTileX;
         const int ctas_y = std::max(1, num_sms / strips);
         const int per = (H + ctas_y - 1) / ctas_y;

@@ -50,6 +50,9 @@ struct Cnn {
     bool seq = false;                    // layers 2..16 in one persistent launch (MACE_K5_SEQ=1; slower)
     DevBuf<int> flags;                   // per-CTA layer-done flags of k_conv64_seq
     int epoch = 0;                       // flag epoch (one per persistent launch)
+    bool seq_pipe = false;               // layers 2..16 as one pipelined persistent launch (MACE_K5_SEQ=2)
+    DevBuf<int> pflags;                  // k_conv64_pipe: published row counts [cta][epilogue warp]
+    int pipe_epoch = 0;
     int roll_epoch = 0;                  // persistent rolling-accumulator launches so far at this geometry
     DevBuf<__nv_bfloat16> act0, act1;    // channel-blocked [8 groups][H][Wp][8 ch]
     CUtensorMap map0{}, map1{};

@@ -243,3 +243,8 @@ def test_cnn_launch_variants_are_bit_identical(n_side, monkeypatch):
     monkeypatch.setenv("MACE_K5_SEQ", "1")
     den = CnnDenoiser(n_side, weights=w)
     assert np.array_equal(den(x), one) and np.array_equal(den(x), one)
+    # ... and pipelined (MACE_K5_SEQ=2, k_conv64_pipe): row runs shifted by half a run in odd layers, per-row
+    # flags instead of any grid-wide wait; every output row still receives the same UMMAs in the same order
+    monkeypatch.setenv("MACE_K5_SEQ", "2")
+    den = CnnDenoiser(n_side, weights=w)
+    assert np.array_equal(den(x), one) and np.array_equal(den(x), one) and np.array_equal(den(x), one)
