@@ -892,23 +892,27 @@ __device__ __forceinline__ int pipe_cum(int j, int l, int per, int nyc, int H)
     return ((l + 1) / 2) * (e.y1 - e.y0) + (l / 2) * (o.y1 - o.y0);
 }
 
-__global__ void __launch_bounds__(192, 1) k_conv64_pipe(const __grid_constant__ CUtensorMap map0,
-                                                        const __grid_constant__ CUtensorMap map1,
-                                                        const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* out0,
-                                                        __nv_bfloat16* out1, int H, int W, int Wp, int per, int n_layers,
-                                                        unsigned* flags, unsigned flag_base)
+constexpr int kPSlots = 4;                                            // halo ring of k_conv64_pipe
+constexpr int kPSmem = 2 * kWBytes + kPSlots * kSlotBytes + 1024;     // two weight buffers + ring: 222,208 B
+constexpr int kPThreads = 320;                                        // producer, issuer, 2 x 4 epilogue warps
+
+__global__ void __launch_bounds__(kPThreads, 1) k_conv64_pipe(const __grid_constant__ CUtensorMap map0,
+                                                              const __grid_constant__ CUtensorMap map1,
+                                                              const __nv_bfloat16* __restrict__ wts, __nv_bfloat16* out0,
+                                                              __nv_bfloat16* out1, int H, int W, int Wp, int per,
+                                                              int n_layers, unsigned* flags, unsigned flag_base)
 {
     extern __shared__ __align__(1024) unsigned char sm[];
-    unsigned char* sw = sm;
-    unsigned char* slots = sm + kWBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + kSlots * kSlotBytes);
-    uint64_t* wbar = bars;
-    uint64_t* sfull = bars + 1;
-    // rowdone barriers in a ring of 16 (twice the halo ring): without a grid-wide wait the MMA issuer can be a layer
-    // boundary (two extra halo rows) ahead of the epilogue, so with 8 a waiter could miss a whole phase
+    unsigned char* sw = sm;                   // weights of layer l in buffer l & 1
+    unsigned char* slots = sm + 2 * kWBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + kPSlots * kSlotBytes);
+    // rowdone barriers in a ring of 16: without a grid-wide wait the MMA issuer can be a layer boundary (two extra
+    // halo rows) ahead of the epilogue, so with a short ring a parity wait could miss a whole phase
     constexpr int kRD = 16;
-    uint64_t* rowdone = sfull + kSlots;
-    uint64_t* aempty = rowdone + kRD;
+    uint64_t* wbar = bars;                  // [2]
+    uint64_t* sfull = bars + 2;             // [kPSlots]
+    uint64_t* rowdone = sfull + kPSlots;    // [kRD]
+    uint64_t* aempty = rowdone + kRD;       // [kRollAcc]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kRollAcc);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -925,7 +929,8 @@ __global__ void __launch_bounds__(192, 1) k_conv64_pipe(const __grid_constant__ 
     }
     if (tid == 32) {
         mbar_init(wbar, 1);
-        for (int i = 0; i < kSlots; ++i) mbar_init(sfull + i, 1);
+        mbar_init(wbar + 1, 1);
+        for (int i = 0; i < kPSlots; ++i) mbar_init(sfull + i, 1);
         for (int i = 0; i < kRD; ++i) mbar_init(rowdone + i, 1);
         for (int i = 0; i < kRollAcc; ++i) mbar_init(aempty + i, 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -937,20 +942,24 @@ __global__ void __launch_bounds__(192, 1) k_conv64_pipe(const __grid_constant__ 
 
     if (warp == 0) {  // ---- TMA producer (whole warp: lanes 0..11 watch the owners' flags, lane 0 copies)
         int Qb = 0;   // halo rows before this layer
-        // lane 4 t + w watches epilogue warp w of the owner in strip (strip - 1 + t)
+        // lane 4 t + w watches TMEM quarter w of the owners in strip (strip - 1 + t); a run's rows alternate between
+        // its two epilogue groups (running row index mod 2), each with its own count
         const int ft = lane >> 2, fw = lane & 3, fstrip = strip - 1 + ft;
         const bool watcher = lane < 12 && fstrip >= 0 && fstrip < strips;
-        unsigned seen = flag_base;  // last value read from the flag this lane watched (of whichever owner)
+        unsigned seen[2] = {flag_base, flag_base};
         int seen_owner = -1;
+        if (lane == 0) {
+            for (int l = 0; l < 2 && l < n_layers; ++l) {
+                mbar_expect(wbar + l, kWBytes);
+                bulk_copy(sw + l * kWBytes, wts + (size_t)l * 9 * kC * kC, kWBytes, wbar + l);
+            }
+        }
         for (int l = 0; l < n_layers; ++l) {
             const RowRun rr = pipe_run(jrun, l & 1, per, nyc, H);
             const int nq = rr.y1 - rr.y0 + 2;
-            if (lane == 0) {
-                if (l > 0) mbar_wait(rowdone + (Qb - 1) % kRD, (uint32_t)(((Qb - 1) / kRD) & 1));  // weights free
-                mbar_expect(wbar, kWBytes);
-                bulk_copy(sw, wts + (size_t)l * 9 * kC * kC, kWBytes, wbar);
-            }
             const CUtensorMap* map = (l & 1) ? &map1 : &map0;
+            // owner of the current halo row in layer l - 1: its run and the rows it had completed before that layer
+            int jo = -1, oy0 = 0, oy1 = -1, ocum = 0;
             for (int q = 0; q < nq; ++q) {
                 const int r = rr.y0 - 1 + q;
 #ifdef K5P_NOPOLL  // (timing experiment)
@@ -958,52 +967,70 @@ __global__ void __launch_bounds__(192, 1) k_conv64_pipe(const __grid_constant__ 
 #else
                 if (l > 0 && r >= 0 && r < H) {  // row r of layer l - 1: stored and visible?
 #endif
-                    const int jo = pipe_owner(r, (l - 1) & 1, per, nyc);
+                    if (r >= oy1 || jo < 0) {
+                        jo = pipe_owner(r, (l - 1) & 1, per, nyc);
+                        const RowRun ro = pipe_run(jo, (l - 1) & 1, per, nyc, H);
+                        oy0 = ro.y0;
+                        oy1 = ro.y1;
+                        ocum = pipe_cum(jo, l - 1, per, nyc, H);
+                    }
                     bool polled = false;
                     if (watcher) {
-                        const RowRun ro = pipe_run(jo, (l - 1) & 1, per, nyc, H);
-                        const unsigned need = flag_base + (unsigned)(pipe_cum(jo, l - 1, per, nyc, H) + r - ro.y0 + 1);
-                        if (seen_owner != jo || (int)(seen - need) < 0) {
-                            const unsigned* f = flags + ((size_t)(jo * strips + fstrip) * 4 + fw);
-                            unsigned spins = 0;
+                        const int I = ocum + r - oy0;  // the row's running index in its owner
+                        const unsigned need = flag_base + (unsigned)(I + 1);
+                        if (seen_owner != jo) {
+                            seen[0] = seen[1] = flag_base;
+                            seen_owner = jo;
+                        }
+                        if ((int)(seen[I & 1] - need) < 0) {
+                            const unsigned* f = flags + (((size_t)(jo * strips + fstrip) * 4 + fw) * 2 + (I & 1));
+                            unsigned v, spins = 0;
                             do {
-                                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(f) : "memory");
-                                if ((int)(seen - need) >= 0) break;
+                                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                                if ((int)(v - need) >= 0) break;
                                 if (++spins > (1u << 22)) {  // seconds: give up loudly rather than hang
                                     g_k5_sync_timeout = 2u;
                                     __trap();
                                 }
                             } while (true);
-                            seen_owner = jo;
+                            seen[I & 1] = v;
                             polled = true;
                         }
                     }
                     if (__any_sync(0xffffffffu, polled)) asm volatile("fence.proxy.async;" ::: "memory");
                 }
                 if (lane == 0) {
-                    const int Q = Qb + q, s = Q % kSlots;
-                    if (Q >= kSlots) mbar_wait(rowdone + (Q - kSlots) % kRD, (uint32_t)(((Q - kSlots) / kRD) & 1));
+                    const int Q = Qb + q, s = Q % kPSlots;
+                    if (Q >= kPSlots) mbar_wait(rowdone + (Q - kPSlots) % kRD, (uint32_t)(((Q - kPSlots) / kRD) & 1));
                     mbar_expect(sfull + s, kSlotBytes);
                     tma_row(slots + s * kSlotBytes, map, x0 / 8 - 1, r, sfull + s);
+                    // the next layer's weights into the other buffer, once the previous layer (its last user) is done
+                    if (q == min(kPSlots - 1, nq - 1) && l >= 1 && l + 1 < n_layers) {
+                        mbar_wait(rowdone + (Qb - 1) % kRD, (uint32_t)(((Qb - 1) / kRD) & 1));
+                        mbar_expect(wbar + ((l + 1) & 1), kWBytes);
+                        bulk_copy(sw + ((l + 1) & 1) * kWBytes, wts + (size_t)(l + 1) * 9 * kC * kC, kWBytes,
+                                  wbar + ((l + 1) & 1));
+                    }
                 }
                 __syncwarp();
             }
             Qb += nq;
         }
     } else if (warp == 1) {  // ---- MMA issuer (whole warp, one elected lane issues)
-        const uint32_t sw_base = s_u32(sw), sl_base = s_u32(slots);
+        const uint32_t sl_base = s_u32(slots);
         int Qb = 0, Ib = 0;
         for (int l = 0; l < n_layers; ++l) {
             const RowRun rr = pipe_run(jrun, l & 1, per, nyc, H);
             const int y0 = rr.y0, y1 = rr.y1, nq = y1 - y0 + 2;
-            mbar_wait(wbar, (uint32_t)(l & 1));
+            const uint32_t sw_base = s_u32(sw + (l & 1) * kWBytes);
+            mbar_wait(wbar + (l & 1), (uint32_t)((l >> 1) & 1));
             for (int q = 0; q < nq; ++q) {
                 const int r = y0 - 1 + q;
-                const int Q = Qb + q, s = Q % kSlots;
+                const int Q = Qb + q, s = Q % kPSlots;
                 const bool v0 = r - 1 >= y0, v1 = r >= y0 && r < y1, v2 = r + 1 < y1;
                 const int I2 = Ib + q;  // running index of output row r + 1
                 if (v2 && I2 >= kRollAcc) mbar_wait(aempty + (I2 % kRollAcc), (uint32_t)((I2 / kRollAcc - 1) & 1));
-                mbar_wait(sfull + s, (uint32_t)((Q / kSlots) & 1));
+                mbar_wait(sfull + s, (uint32_t)((Q / kPSlots) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint64_t a0 = sdesc(sl_base + s * kSlotBytes + kHaloOff * 16, kHaloX * 16, 128);
                 const int s0 = (I2 + 2 * kRollAcc - 2) % kRollAcc;
@@ -1033,16 +1060,19 @@ __global__ void __launch_bounds__(192, 1) k_conv64_pipe(const __grid_constant__ 
             Qb += nq;
             Ib += y1 - y0;
         }
-    } else {  // ---- epilogue warps 2..5
-        const int quad = warp & 3;
-        unsigned* myflag = flags + ((size_t)blockIdx.x * 4 + quad);
+    } else {  // ---- epilogue warps 2..9: two groups of four (TMEM quarter = warp mod 4), alternating output rows, so
+              // that the fence behind every row's stores has two row times to complete
+        const int quad = warp & 3, grp = (warp - 2) >> 2;
+        unsigned* myflag = flags + (((size_t)blockIdx.x * 4 + quad) * 2 + grp);
         int Qb = 0, Ib = 0;
         for (int l = 0; l < n_layers; ++l) {
             const RowRun rr = pipe_run(jrun, l & 1, per, nyc, H);
             const int y0 = rr.y0, y1 = rr.y1;
             __nv_bfloat16* out = (l & 1) ? out1 : out0;
             for (int y = y0; y < y1; ++y) {
-                const int Q = Qb + (y - y0 + 2), a = (Ib + (y - y0)) % kRollAcc;
+                const int I = Ib + (y - y0);
+                if ((I & 1) != grp) continue;
+                const int Q = Qb + (y - y0 + 2), a = I % kRollAcc;
                 mbar_wait(rowdone + Q % kRD, (uint32_t)((Q / kRD) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a * 64);
@@ -1072,13 +1102,13 @@ __global__ void __launch_bounds__(192, 1) k_conv64_pipe(const __grid_constant__ 
                         dst[g * gstride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                     }
                 }
-                if (l + 1 < n_layers) {  // publish: this warp's part of rows .. y is stored and visible
+                if (l + 1 < n_layers) {  // publish: this warp's part of its rows .. y is stored and visible
 #ifndef K5P_NOFENCE  // (timing experiment)
                     __threadfence();
 #endif
                     __syncwarp();
                     if (lane == 0) {
-                        const unsigned v = flag_base + (unsigned)(Ib + (y - y0) + 1);
+                        const unsigned v = flag_base + (unsigned)(I + 1);
                         asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(myflag), "r"(v) : "memory");
                     }
                 }
@@ -1863,7 +1893,7 @@ void Cnn::ensure(int h, int w)
     CKC(cudaFuncSetAttribute(k_conv64_tc2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv64_roll<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     CKC(cudaFuncSetAttribute(k_conv64_roll<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    CKC(cudaFuncSetAttribute(k_conv64_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    CKC(cudaFuncSetAttribute(k_conv64_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
     CKC(cudaFuncSetAttribute(k_conv_last_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kLSmem));
     CKC(cudaFuncSetAttribute(k_conv_last_roll, cudaFuncAttributeMaxDynamicSharedMemorySize, kLSmem));
     CKC(cudaFuncSetAttribute(k_conv64_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
@@ -1946,14 +1976,14 @@ void Cnn::apply(const float* x, float* out, int h, int w, cudaStream_t s, int nu
         const int per = (H + ctas_y - 1) / ctas_y;
         const int nyc = (H + per - 1) / per;
         const int ctas = strips * nyc;
-        if (ctas * 4 > 4096) throw std::runtime_error("denoiser grid too large");
+        if (ctas * 8 > 4096) throw std::runtime_error("denoiser grid too large");
         cudaLaunchAttribute coop[1];
         coop[0].id = cudaLaunchAttributeCooperative;
         coop[0].val.cooperative = 1;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(ctas);
-        cfg.blockDim = dim3(192);
-        cfg.dynamicSmemBytes = kSmem;
+        cfg.blockDim = dim3(kPThreads);
+        cfg.dynamicSmemBytes = kPSmem;
         cfg.stream = s;
         cfg.attrs = coop;
         cfg.numAttrs = 1;
