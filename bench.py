@@ -427,7 +427,7 @@ def run_ours(args):
         barrier()
         k5_ms = e0.elapsed_time(e1) / reps
         flop = 2.0 * geom.n_pixels * 9 * (64 + 15 * 64 * 64 + 64)
-        line["k5"] = {"kernel": "k_conv64_roll (tcgen05, layers 2-16) + k_conv_first + k_conv_last_tc", "ms_per_denoise": k5_ms,
+        line["k5"] = {"kernel": "k_conv64_roll (tcgen05, layers 2-16) + k_conv_first + k_conv_last_roll", "ms_per_denoise": k5_ms,
                       "flop_per_denoise": flop, "achieved_tflops": flop / (k5_ms / 1e3) / 1e12,
                       "peak_tflops": pk.get("bf16_tflops"), "peak_source": "MEASURED_PEAKS bf16_tflops (burst: "
                       "timed alone)", "frac": flop / (k5_ms / 1e3) / 1e12 / pk.get("bf16_tflops", 1.0),
