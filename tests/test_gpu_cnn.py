@@ -197,6 +197,18 @@ def test_pnp_denoiser_in_device_loop_matches_host_steps():
     assert rel(dev.stack, host.stack) < 1e-6
 
 
+@pytest.mark.parametrize("n_side", [200, 512])
+def test_cnn_is_bitwise_repeatable(n_side):
+    """The rolling-accumulator layers reuse 8 TMEM slots and 8 halo slots behind mbarriers; a missing wait would
+    show up as run-to-run differences on random unit-scale weights.  30 denoises must be bit-identical."""
+    rng = np.random.default_rng(41)
+    x = rng.random(n_side * n_side)
+    den = CnnDenoiser(n_side, weights=cnn_weights(41, scale=1.0))
+    first = den(x)
+    for _ in range(29):
+        assert np.array_equal(den(x), first)
+
+
 @pytest.mark.parametrize("n_side", [64, 200, 512])
 def test_cnn_launch_variants_are_bit_identical(n_side, monkeypatch):
     """The middle layers as 15 launches or as one persistent launch (MACE_K5_SEQ), and the last layer
