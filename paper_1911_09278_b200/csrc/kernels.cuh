@@ -735,7 +735,46 @@ __global__ void __launch_bounds__(256) k_tail(const float* __restrict__ W, int n
     __shared__ double sh[5][256];
     __shared__ bool last;
     double a[5] = {0, 0, 0, 0, 0};
-    for (size_t gs = blockIdx.x * (size_t)blockDim.x + threadIdx.x; gs < n * n_groups;
+    // NL > 0 and n a multiple of 4: four pixels per thread, 128-bit loads and stores (the same tree per pixel)
+    const bool vec4 = NL > 0 && (n & 3) == 0;
+    if constexpr (NL > 0) {
+        if (vec4) {
+            const size_t nq = n / 4;
+            for (size_t gq = blockIdx.x * (size_t)blockDim.x + threadIdx.x; gq < nq * n_groups;
+                 gq += (size_t)gridDim.x * blockDim.x) {
+                const size_t grp = gq / nq, s = (gq % nq) * 4;
+                const float* Wg = W + grp * n_local * n;
+                float4 q[NL];
+#pragma unroll
+                for (int i = 0; i < NL; ++i) q[i] = __ldcg(reinterpret_cast<const float4*>(Wg + (size_t)i * n + s));
+                float acc[NL];
+                float4 v;
+#pragma unroll
+                for (int i = 0; i < NL; ++i) acc[i] = q[i].x;
+                v.x = tree_sum<NL>(acc) / scale;
+#pragma unroll
+                for (int i = 0; i < NL; ++i) acc[i] = q[i].y;
+                v.y = tree_sum<NL>(acc) / scale;
+#pragma unroll
+                for (int i = 0; i < NL; ++i) acc[i] = q[i].z;
+                v.z = tree_sum<NL>(acc) / scale;
+#pragma unroll
+                for (int i = 0; i < NL; ++i) acc[i] = q[i].w;
+                v.w = tree_sum<NL>(acc) / scale;
+                *reinterpret_cast<float4*>(out + grp * n + s) = v;
+                if (ref && grp == 0) {
+                    const float4 r4 = *reinterpret_cast<const float4*>(ref + s);
+                    const double d0 = (double)v.x - (double)r4.x, d1 = (double)v.y - (double)r4.y;
+                    const double d2 = (double)v.z - (double)r4.z, d3 = (double)v.w - (double)r4.w;
+                    a[4] += d0 * d0;
+                    a[4] += d1 * d1;
+                    a[4] += d2 * d2;
+                    a[4] += d3 * d3;
+                }
+            }
+        }
+    }
+    for (size_t gs = blockIdx.x * (size_t)blockDim.x + threadIdx.x; !vec4 && gs < n * n_groups;
          gs += (size_t)gridDim.x * blockDim.x) {
         const size_t grp = gs / n, s = gs % n;
         const float* Wg = W + grp * n_local * n;
